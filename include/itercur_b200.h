@@ -1,0 +1,182 @@
+/*
+ * itercur_b200.h — C-ABI of the B200-native IterativeCUR engine (drop-in boundary).
+ *
+ * Plain pointers and sizes only (no torch / Eigen types). Each entry point replaces one
+ * reference interface (paths relative to /root/reference):
+ *
+ *   itercur_iterative_cur_host / _device
+ *       itercur::iterative_cur            proj/include/itercur/driver.hpp:79-81
+ *                                         (body proj/src/driver.cpp:48-167)
+ *       and the pybind11 binding          proj/bindings/python/module.cpp:82-103
+ *   itercur_config (+ itercur_config_default)
+ *       itercur::StoppingConfig           proj/include/itercur/driver.hpp:18-26
+ *       itercur::SelectionMethod          proj/include/itercur/select.hpp:12-15
+ *   itercur_run_* accessors
+ *       itercur::CurFactors               proj/include/itercur/pinv.hpp:57-66
+ *       itercur::RunTrace / IterationRecord  proj/include/itercur/driver.hpp:32-54
+ *       CurFactors.c_matrix/r_matrix/core_matrix  proj/bindings/python/module.cpp:60-68
+ *   itercur_true_relative_error_device
+ *       itercur::true_relative_error      proj/include/itercur/driver.hpp:85 (driver.cpp:169-190)
+ *   itercur_adjusted_threshold / itercur_gratton_tail
+ *       proj/include/itercur/driver.hpp:64,68 (driver.cpp:28-46)
+ *   itercur_sketch_device
+ *       itercur::make_sketch              proj/include/itercur/sketch.hpp:36 (sketch.cpp:10-24)
+ *   itercur_select_device
+ *       itercur::select_columns / select_rows  proj/include/itercur/select.hpp:31-38
+ *   itercur_gaussian_matrix_device
+ *       itercur::gaussian_matrix          proj/include/itercur/rng.hpp:33-34 (rng.cpp:61-67)
+ *
+ * Matrices are column-major doubles (the reference's Eigen default). Indices are int64
+ * (itercur::Index, proj/include/itercur/matrix.hpp:12).
+ *
+ * Errors: every entry returns ITERCUR_OK or a code naming the reference's exception class
+ * (std::invalid_argument, out_of_range, domain_error, runtime_error, logic_error), or a
+ * CUDA failure; itercur_last_error() returns the message (thread-local), preserving the
+ * reference's texts ("matrix must be nonzero", "block exceeds row count", "block too
+ * small for requested alpha", "not implemented", ...). Non-exceptional ends are reported
+ * through the run status, as in the reference.
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute entry returns
+ * ITERCUR_E_CUDA.
+ */
+#ifndef ITERCUR_B200_H
+#define ITERCUR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ITERCUR_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ITERCUR_API __attribute__((visibility("default")))
+#else
+#define ITERCUR_API
+#endif
+
+enum itercur_status_code {
+  ITERCUR_OK = 0,
+  ITERCUR_E_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  ITERCUR_E_OUT_OF_RANGE = 2,     /* std::out_of_range */
+  ITERCUR_E_DOMAIN = 3,           /* std::domain_error */
+  ITERCUR_E_RUNTIME = 4,          /* std::runtime_error */
+  ITERCUR_E_LOGIC = 5,            /* std::logic_error */
+  ITERCUR_E_CUDA = 10,            /* CUDA launch / runtime failure */
+  ITERCUR_E_OOM = 11              /* device allocation failed */
+};
+
+enum itercur_run_status { ITERCUR_CONVERGED = 0, ITERCUR_MAX_RANK = 1, ITERCUR_RESIDUAL_EXHAUSTED = 2 };
+enum itercur_pivot_kind { ITERCUR_PIVOT_LUPP = 0, ITERCUR_PIVOT_QRCP = 1, ITERCUR_PIVOT_OSINSKY = 2 };
+enum itercur_sketch_kind { ITERCUR_SKETCH_GAUSSIAN = 0, ITERCUR_SKETCH_SPARSE_SIGN = 1 };
+
+/* StoppingConfig + the two SelectionMethods + seed + the new sketch options. */
+typedef struct itercur_config {
+  double epsilon;      /* 1e-6  */
+  int64_t b;           /* 50    */
+  double delta;        /* 0.0   */
+  double alpha;        /* 0.05  */
+  int32_t risk_adjust; /* 0     */
+  int64_t max_rank;    /* 0 -> min(m, n) */
+  int64_t max_iters;   /* 0 -> ceil(min(m, n) / b) + 1 */
+  int32_t col_method;  /* ITERCUR_PIVOT_LUPP */
+  int32_t row_method;  /* ITERCUR_PIVOT_LUPP */
+  double pivot_floor;  /* 1e-13 */
+  uint64_t seed;       /* 0 */
+  int32_t sketch_kind; /* ITERCUR_SKETCH_GAUSSIAN (the reference's only kind) */
+  int32_t sparse_nnz;  /* 8 */
+  int32_t profile;     /* 1: record per-phase CUDA-event times into the trace */
+  int32_t reserved;
+} itercur_config;
+
+/* One IterationRecord (proj/include/itercur/driver.hpp:32-44) plus pivot-margin data. */
+typedef struct itercur_iteration_record {
+  int64_t k;
+  double rho;
+  int64_t cols_added;
+  int64_t rows_added;
+  int32_t col_truncated;
+  int32_t row_truncated;
+  double select_cols_s;
+  double row_residual_s;
+  double select_rows_s;
+  double core_s;
+  double downdate_s;
+  double min_col_margin; /* min over steps of (|best|-|second|)/|best| in the column LUPP */
+  double min_row_margin; /* same for the row LUPP */
+} itercur_iteration_record;
+
+typedef struct itercur_run itercur_run; /* opaque: CurFactors + RunTrace + device buffers */
+
+ITERCUR_API void itercur_config_default(itercur_config* cfg);
+ITERCUR_API const char* itercur_last_error(void);
+ITERCUR_API int itercur_abi_version(void);
+
+/* iterative_cur on a device-resident column-major A (m x n, leading dimension lda).
+   `stream` is a cudaStream_t (NULL = legacy default stream). A must stay alive and
+   unmodified while the run handle is used for c/r/core/error queries. */
+ITERCUR_API int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
+                                 void* stream, itercur_run** out);
+/* Same, from a host buffer: A is copied to the current device inside the call (the copy
+   is part of the call, as in the reference binding's numpy -> Eigen copy). The run keeps
+   the device copy alive until itercur_run_free. */
+ITERCUR_API int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
+                               itercur_run** out);
+
+/* ---- run accessors (CurFactors / RunTrace) ---- */
+ITERCUR_API int64_t itercur_run_rank(const itercur_run* run);
+ITERCUR_API int64_t itercur_run_rows(const itercur_run* run);
+ITERCUR_API int64_t itercur_run_cols(const itercur_run* run);
+ITERCUR_API int itercur_run_indices(const itercur_run* run, int64_t* row_indices, int64_t* col_indices);
+ITERCUR_API int32_t itercur_run_status(const itercur_run* run);
+ITERCUR_API double itercur_run_final_rho(const itercur_run* run);
+ITERCUR_API double itercur_run_threshold(const itercur_run* run);
+ITERCUR_API double itercur_run_sketch_seconds(const itercur_run* run);
+ITERCUR_API double itercur_run_total_seconds(const itercur_run* run);
+ITERCUR_API double itercur_run_ga_norm(const itercur_run* run);
+ITERCUR_API const char* itercur_run_note(const itercur_run* run);
+ITERCUR_API int64_t itercur_run_num_iterations(const itercur_run* run);
+ITERCUR_API int itercur_run_iterations(const itercur_run* run, itercur_iteration_record* out);
+/* per pivot step log: kind (0 col, 1 row), iteration, index, |best|, |second| */
+ITERCUR_API int64_t itercur_run_num_steps(const itercur_run* run);
+ITERCUR_API int itercur_run_steps(const itercur_run* run, int32_t* kind, int64_t* iter, int64_t* index, double* best,
+                      double* second);
+/* C = A(:, J) (m x r), R = A(I, :) (r x n), core = A(I, J)^{-1} (r x r); host outputs,
+   column-major. core is materialised from the engine's block-LU factors on demand
+   (FactoredPinv::materialize, proj/src/pinv.cpp:40-43). */
+ITERCUR_API int itercur_run_c_matrix(const itercur_run* run, double* out);
+ITERCUR_API int itercur_run_r_matrix(const itercur_run* run, double* out);
+ITERCUR_API int itercur_run_core_matrix(const itercur_run* run, double* out);
+/* ||A - CUR||_F / ||A||_F evaluated on the device over column panels. */
+ITERCUR_API int itercur_true_relative_error_device(const itercur_run* run, double* out);
+ITERCUR_API void itercur_run_free(itercur_run* run);
+
+/* ---- helpers ---- */
+ITERCUR_API int itercur_adjusted_threshold(double epsilon, double delta, double alpha, int64_t c, double* out);
+ITERCUR_API int itercur_gratton_tail(int64_t c, double tau, double* out);
+ITERCUR_API int64_t itercur_sketch_rows_for_block(int64_t b);
+
+/* ---- stage-level entries (tests / benchmarks) ---- */
+/* G (rows x cols, column-major, device) with G(i, j) = normal_at(seed, stream, i, j). */
+ITERCUR_API int itercur_gaussian_matrix_device(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* dOut,
+                                   void* stream);
+/* Y = S * A (c x n, ld c), ||Y||_F and ||A||_F; S Gaussian or sparse-sign. */
+ITERCUR_API int itercur_sketch_device(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, uint64_t seed,
+                          int32_t kind, int32_t sparse_nnz, double* dY, double* ga_norm, double* a_norm, void* stream);
+/* LUPP selection on a device matrix M (rows x cols, ld): is_columns = 1 -> select_columns(M, b),
+   0 -> select_rows(M, b). Host outputs (idx capacity >= b). */
+ITERCUR_API int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b, int32_t is_columns,
+                          double pivot_floor, const int64_t* exclude, int64_t n_exclude, int64_t* idx_out,
+                          int64_t* n_idx, int32_t* truncated, double* last_pivot, double* best_out,
+                          double* second_out, void* stream);
+/* Time the sketch-apply DMMA kernel alone (CUDA events on `stream`), `reps` launches;
+   returns the mean milliseconds per launch and the kernel's launch geometry. */
+ITERCUR_API int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, int32_t kind,
+                               int32_t reps, void* stream, double* ms_per_launch, int32_t* ctas, int32_t* splits,
+                               int32_t* uses_tma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ITERCUR_B200_H */

@@ -1,0 +1,1048 @@
+// engine.cu — the C++ host driver of the B200 IterativeCUR engine and its C-ABI
+// (include/itercur_b200.h). It restates the loop of itercur::iterative_cur
+// (proj/src/driver.cpp:48-167) over device-resident state, in the incremental block-LU
+// (Schur) form of SURVEY.md A.7:
+//
+//   sketch    Y = S*A once (DMMA + TMA), ||A||, ||Y||                 sketch.cu
+//   loop k:   J_k  = LUPP(Y^T)                                        lupp.cu
+//             S_row = A(:,J_k) - L * Rt(:,J_k)   -> L_k                gemm.cu
+//             I_k  = LUPP(S_row)                                      lupp.cu
+//             D_k^{-1} from S_row(I_k, :)                             misc.cu
+//             U_k^T = A(I_k,:)^T - Rt^T * L(I_k,:)^T ; Rt_k = D_k^{-1} U_k   gemm.cu
+//             Y   -= Y(:,J_k) * Rt_k  (in place, ||Y||^2 fused)       gemm.cu
+//             rho = ||Y|| / ||S*A||  -> one 64-B+ D2H read per iteration
+//
+// so CUR = L * Rt with C = A(:,J), R = A(I,:), core = A(I,J)^{-1} = (L(I,:) Rt(:,J))^{-1}
+// exported on demand. A is never re-read after the sketch except through the gathered
+// columns / rows of the selected blocks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/itercur_b200.h"
+#include "gemm.h"
+#include "kernels.h"
+#include "misc.h"
+
+using namespace itercur_b200;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError(code, msg); }
+void ck(cudaError_t e, const char* what, int line) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation)
+      fail(ITERCUR_E_OOM, std::string("device allocation failed (") + what + ")");
+    fail(ITERCUR_E_CUDA, std::string("CUDA error '") + cudaGetErrorString(e) + "' at engine.cu:" +
+                             std::to_string(line) + " (" + what + ")");
+  }
+}
+#define CK(x) ck((x), #x, __LINE__)
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ITERCUR_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return ITERCUR_E_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ITERCUR_E_RUNTIME;
+  }
+}
+
+// ------------------------------------------------------------------ device buffers
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  void alloc(size_t n) {
+    reset();
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    count = n;
+  }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(count, o.count);
+  }
+};
+
+struct Events {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t get(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+  ~Events() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return 1e-3 * ms;
+}
+
+}  // namespace
+
+// ====================================================================== the run handle
+struct itercur_run {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t m = 0, n = 0, lda = 0;
+  const double* A = nullptr;
+  DevBuf<double> A_owned;  // host entry: device copy of A
+  itercur_config cfg{};
+  int64_t c = 0, cp = 0;
+  int64_t r = 0;
+  std::vector<int64_t> I, J;
+  std::vector<int64_t> block_start, block_width;
+  int32_t status = ITERCUR_CONVERGED;
+  double final_rho = 1.0, threshold = 0.0, sketch_s = 0.0, total_s = 0.0, ga_norm = 0.0, a_norm = 0.0;
+  std::string note;
+  std::vector<itercur_iteration_record> iters;
+  std::vector<int32_t> step_kind;
+  std::vector<int64_t> step_iter, step_index;
+  std::vector<double> step_best, step_second;
+  // factors (incremental block-LU form)
+  DevBuf<double> L;     // m x capL, column-major, ld ldL
+  DevBuf<double> Rt;    // capL rows of n, row-major (Rt[q * ldR + j])
+  DevBuf<double> Dinv;  // per block: LU of D_k (w x w, ld bmax) at offset start * bmax
+  DevBuf<int64_t> dI, dJ;
+  int64_t ldL = 0, ldR = 0, capL = 0, bmax = 0;
+};
+
+namespace {
+
+int64_t even(int64_t x) { return x + (x & 1); }
+
+// StoppingConfig defaults, proj/include/itercur/driver.hpp:18-26; SelectionMethod select.hpp:12-15
+itercur_config default_config() {
+  itercur_config c{};
+  c.epsilon = 1e-6;
+  c.b = 50;
+  c.delta = 0.0;
+  c.alpha = 0.05;
+  c.risk_adjust = 0;
+  c.max_rank = 0;
+  c.max_iters = 0;
+  c.col_method = ITERCUR_PIVOT_LUPP;
+  c.row_method = ITERCUR_PIVOT_LUPP;
+  c.pivot_floor = 1e-13;
+  c.seed = 0;
+  c.sketch_kind = ITERCUR_SKETCH_GAUSSIAN;
+  c.sparse_nnz = 8;
+  c.profile = 0;
+  return c;
+}
+
+// adjusted_threshold, proj/src/driver.cpp:28-39
+double adjusted_threshold_impl(double epsilon, double delta, double alpha, int64_t c) {
+  if (!(alpha > 0.0 && alpha < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "alpha must lie in (0, 1)");
+  if (delta < 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "delta must be nonnegative");
+  if (c < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "sketch rows must be positive");
+  const double nla = -std::log(alpha);
+  if (static_cast<double>(c) <= 4.0 * nla) fail(ITERCUR_E_DOMAIN, "block too small for requested alpha");
+  const double xi = (1.0 + delta) * std::sqrt(1.0 - 2.0 * std::sqrt(nla / static_cast<double>(c)));
+  return xi * epsilon;
+}
+// gratton_tail, proj/src/driver.cpp:41-46
+double gratton_tail_impl(int64_t c, double tau) {
+  if (c < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "sketch rows must be positive");
+  if (!(tau > 1.0)) fail(ITERCUR_E_DOMAIN, "tau must exceed 1");
+  const double t2 = tau * tau;
+  return std::exp(-static_cast<double>(c) * (t2 - 1.0) * (t2 - 1.0) / (4.0 * t2 * t2));
+}
+
+int64_t sketch_rows(int64_t b) { return (11 * b) / 10; }  // proj/include/itercur/sketch.hpp:10
+
+void check_method(int32_t kind) {
+  if (kind == ITERCUR_PIVOT_OSINSKY) fail(ITERCUR_E_RUNTIME, "Osinsky selection not implemented");
+  if (kind == ITERCUR_PIVOT_QRCP) fail(ITERCUR_E_RUNTIME, "QRCP selection not implemented in the B200 engine");
+  if (kind != ITERCUR_PIVOT_LUPP) fail(ITERCUR_E_LOGIC, "unknown selection method");
+}
+
+// ||A||_F^2 via a dedicated pass (only used when validation must report in the reference's
+// order before the fused sketch pass runs, and for the true-error denominator).
+double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
+  DevBuf<double> part, out;
+  part.alloc(148 * 8);
+  out.alloc(1);
+  CK(launch_sumsq(x, rows, cols, ld, part.p, 148 * 8, out.p, st));
+  double h = 0.0;
+  CK(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+struct Workspace {
+  DevBuf<double> Y, Wc, Wr, Bg, Ut, Yg, lu, part, sk_ws, S;
+  DevBuf<uint8_t> col_mask, row_mask;
+  DevBuf<char> state, lupp_scratch;
+  DevBuf<double> scal;  // [0] asq, [1] ysq
+  DevBuf<unsigned long long> nonfinite;
+  char* h_state = nullptr;  // pinned mirror
+  ~Workspace() {
+    if (h_state) cudaFreeHost(h_state);
+  }
+};
+
+void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
+  if (need <= run->capL) return;
+  int64_t cap = std::max<int64_t>(run->capL * 2, need);
+  const int64_t maxcap = std::min(run->m, run->n) + run->bmax;
+  cap = std::min(cap, maxcap);
+  if (cap < need) cap = need;
+  DevBuf<double> L2, R2, D2;
+  L2.alloc(static_cast<size_t>(run->ldL) * cap);
+  R2.alloc(static_cast<size_t>(run->ldR) * cap);
+  D2.alloc(static_cast<size_t>(run->bmax) * cap);
+  if (run->r > 0) {
+    CK(cudaMemcpyAsync(L2.p, run->L.p, sizeof(double) * run->ldL * run->r, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(R2.p, run->Rt.p, sizeof(double) * run->ldR * run->r, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(D2.p, run->Dinv.p, sizeof(double) * run->bmax * run->r, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  run->L.swap(L2);
+  run->Rt.swap(R2);
+  run->Dinv.swap(D2);
+  run->capL = cap;
+}
+
+double min_margin(const double* best, const double* second, int count) {
+  double mm = std::numeric_limits<double>::infinity();
+  for (int s = 0; s < count; ++s)
+    if (second[s] >= 0.0 && best[s] > 0.0) mm = std::min(mm, (best[s] - second[s]) / best[s]);
+  return mm;
+}
+
+// The driver: proj/src/driver.cpp:48-167 over device state.
+void run_iterative_cur(itercur_run* run) {
+  const itercur_config& cfg = run->cfg;
+  cudaStream_t st = run->stream;
+  const int64_t m = run->m, n = run->n, lda = run->lda;
+  const double* A = run->A;
+  const auto t_start = std::chrono::steady_clock::now();
+
+  // ---- validation (driver.cpp:51-54, sketch.cpp:11-13), in the reference's order ----
+  if (m == 0 || n == 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonempty");
+  if (m < 0 || n < 0 || lda < std::max<int64_t>(m, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "invalid matrix shape");
+  const bool cheap_fail = cfg.epsilon < 0.0 || cfg.b < 1 || cfg.b > m;
+  if (cheap_fail) {
+    const double asq = device_sumsq(A, m, n, lda, st);
+    if (!std::isfinite(asq)) {
+      DevBuf<unsigned long long> cnt;
+      cnt.alloc(1);
+      CK(launch_count_nonfinite(A, m, n, lda, cnt.p, st));
+      unsigned long long h = 0;
+      CK(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (h) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
+    }
+    if (asq == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
+    if (cfg.epsilon < 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "epsilon must be nonnegative");
+    if (cfg.b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
+    fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
+  }
+  if (cfg.b > 2048) fail(ITERCUR_E_INVALID_ARGUMENT, "block size above 2048 is not supported by the B200 engine");
+
+  const int64_t b = cfg.b;
+  const int64_t min_dim = std::min(m, n);
+  const int64_t max_rank = cfg.max_rank > 0 ? std::min(cfg.max_rank, min_dim) : min_dim;
+  const int64_t max_iters = cfg.max_iters > 0 ? cfg.max_iters : (min_dim + b - 1) / b + 1;
+  const int64_t c = sketch_rows(b);
+  const int64_t cp = round_up(c, 8);
+  run->c = c;
+  run->cp = cp;
+  run->bmax = b;
+  run->ldL = even(m);
+  run->ldR = even(n);
+
+  Events evs;
+  evs.on = cfg.profile != 0;
+  Workspace ws;
+  ws.scal.alloc(4);
+  ws.Y.alloc(static_cast<size_t>(cp) * n);
+
+  // ---- sketch (make_sketch, sketch.cpp:10-24), ||A|| fused ----
+  cudaEvent_t e_sk0 = evs.get(0), e_sk1 = evs.get(1);
+  CK(cudaEventRecord(e_sk0, st));
+  {
+    const int64_t ldg = round_up(m, 32);
+    ws.S.alloc(static_cast<size_t>(cp) * ldg);
+    CK(launch_gen_sketch_operator(ws.S.p, cp, ldg, c, m, cfg.seed, cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN
+                                                                       ? kSketchSparseSign
+                                                                       : kSketchGaussian,
+                                  cfg.sparse_nnz, st));
+    const int64_t wse = sketch_workspace_elems(m, n, cp);
+    ws.sk_ws.alloc(wse);
+    double scale = 1.0;
+    if (cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN) {
+      const int ze = static_cast<int>(std::min<int64_t>(std::max(cfg.sparse_nnz, 1), c));
+      scale = 1.0 / std::sqrt(static_cast<double>(ze));
+    }
+    SketchStats stats{ws.scal.p + 0, ws.scal.p + 1};
+    CK(run_sketch_apply(A, m, n, lda, ws.S.p, ldg, cp, scale, ws.Y.p, ws.sk_ws.p, wse, stats, st, nullptr));
+  }
+  CK(cudaEventRecord(e_sk1, st));
+  double hs[2] = {0, 0};
+  CK(cudaMemcpyAsync(hs, ws.scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ws.S.reset();
+  ws.sk_ws.reset();
+  if (!std::isfinite(hs[0])) {
+    ws.nonfinite.alloc(1);
+    CK(launch_count_nonfinite(A, m, n, lda, ws.nonfinite.p, st));
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, ws.nonfinite.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
+  }
+  if (hs[0] == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
+  run->a_norm = std::sqrt(hs[0]);
+  const double ga_norm = std::sqrt(hs[1]);
+  run->ga_norm = ga_norm;
+  run->sketch_s = elapsed_s(e_sk0, e_sk1);
+
+  const double threshold =
+      cfg.risk_adjust ? adjusted_threshold_impl(cfg.epsilon, cfg.delta, cfg.alpha, c) : cfg.epsilon;
+  run->threshold = threshold;
+
+  // rho_0 (downdate with empty factors, sketch.cpp:27-30)
+  double rho = ga_norm > 0.0 ? 1.0 : 0.0;
+  if (rho <= threshold) {
+    run->status = ITERCUR_CONVERGED;
+    run->final_rho = rho;
+    run->note = "threshold at or above the initial estimate; empty factorization";
+    run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return;
+  }
+  // the reference validates the selection methods on the first select_* call
+  if (!(cfg.pivot_floor > 0.0 && cfg.pivot_floor < 1.0))
+    fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+  check_method(cfg.col_method);
+
+  // ---- workspaces ----
+  const int B = static_cast<int>(b);
+  ws.Wc.alloc(static_cast<size_t>(even(n)) * B);
+  ws.Wr.alloc(static_cast<size_t>(even(m)) * B);
+  ws.Ut.alloc(static_cast<size_t>(even(n)) * B);
+  ws.Yg.alloc(static_cast<size_t>(B) * cp);
+  ws.lu.alloc(static_cast<size_t>(B) * B);
+  ws.col_mask.alloc(n);
+  ws.row_mask.alloc(m);
+  CK(cudaMemsetAsync(ws.col_mask.p, 0, n, st));
+  CK(cudaMemsetAsync(ws.row_mask.p, 0, m, st));
+  ws.lupp_scratch.alloc(lupp_scratch_bytes());
+  const size_t state_bytes = iter_state_bytes(B);
+  ws.state.alloc(state_bytes);
+  CK(cudaMemsetAsync(ws.state.p, 0, state_bytes, st));
+  CK(cudaMallocHost(&ws.h_state, state_bytes));
+  IterState* d_state = reinterpret_cast<IterState*>(ws.state.p);
+  const IterArrays arr = iter_arrays(ws.state.p, B);
+  const IterArrays harr = iter_arrays(ws.h_state, B);
+  int64_t part_count = std::max<int64_t>({ts_gemm_grid_size(m, B), ts_gemm_grid_size(n, static_cast<int>(cp)),
+                                          ts_gemm_grid_size(n, B), 4096});
+  ws.part.alloc(part_count);
+  run->dI.alloc(std::max<int64_t>(max_rank + b, 1));
+  run->dJ.alloc(std::max<int64_t>(max_rank + b, 1));
+  run->capL = 0;
+  grow_factors(run, std::min<int64_t>(max_rank + b, std::max<int64_t>(4 * b, 256)), st);
+  ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+
+  // initial Wc = Y^T(:, 0:b)
+  CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, even(n), st));
+  CK(cudaMemcpyAsync(&d_state->ysq, ws.scal.p + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
+
+  uint8_t epoch = 1;
+  int64_t k = 0;
+  int32_t status = ITERCUR_MAX_RANK;
+  while (true) {
+    if (run->r >= max_rank || k >= max_iters) {
+      status = ITERCUR_MAX_RANK;
+      break;
+    }
+    const int64_t r = run->r;
+    const int block = static_cast<int>(std::min<int64_t>(b, max_rank - r));
+    if (r + B > run->capL) {
+      grow_factors(run, r + B, st);
+      ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+    }
+    if (++epoch == 0 || epoch == 1) {  // epochs cycle through 2..255
+      CK(launch_clear_epochs(ws.col_mask.p, n, st));
+      CK(launch_clear_epochs(ws.row_mask.p, m, st));
+      epoch = 2;
+    }
+    itercur_iteration_record rec{};
+    rec.k = k;
+    const size_t e0 = 2 + 6 * static_cast<size_t>(k);
+    if (evs.on) CK(cudaEventRecord(evs.get(e0), st));
+
+    // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
+    int* d_ncols = &d_state->ncols;
+    int* d_nrows = &d_state->nrows;
+    int* d_width = &d_state->width;
+    {
+      LuppArgs la{};
+      la.W = ws.Wc.p;
+      la.rows = n;
+      la.ldw = even(n);
+      la.cols_max = block;
+      la.d_steps = nullptr;
+      la.mask = ws.col_mask.p;
+      la.epoch = epoch;
+      la.d_norm_sq = &d_state->ysq;
+      la.pivot_floor = cfg.pivot_floor;
+      la.d_idx = arr.col_idx;
+      la.d_best = arr.col_best;
+      la.d_second = arr.col_second;
+      la.d_count = d_ncols;
+      CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+    }
+    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
+
+    // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60)
+    CK(launch_gather(run->Rt.p, run->ldR, 1, r, arr.col_idx, d_ncols, block, ws.Bg.p, std::max<int64_t>(r, 1), st));
+    {
+      TsGemmParams p;
+      p.M = m;
+      p.K = r;
+      p.N = block;
+      p.d_n = d_ncols;
+      p.A = run->L.p;
+      p.lda = run->ldL;
+      p.B = ws.Bg.p;
+      p.bsk = 1;
+      p.bsn = std::max<int64_t>(r, 1);
+      p.base_mode = kBaseGatherCols;
+      p.src = A;
+      p.lds = lda;
+      p.idx = arr.col_idx;
+      p.alpha = -1.0;
+      p.out_mode = kOutColMajor;
+      p.C0 = run->L.p + run->ldL * r;
+      p.ldc0 = run->ldL;
+      p.C1 = ws.Wr.p;
+      p.ldc1 = even(m);
+      CK(run_ts_gemm(p, st));
+    }
+    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
+
+    // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
+    {
+      LuppArgs la{};
+      la.W = ws.Wr.p;
+      la.rows = m;
+      la.ldw = even(m);
+      la.cols_max = block;
+      la.d_steps = d_ncols;
+      la.mask = ws.row_mask.p;
+      la.epoch = epoch;
+      la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
+      la.pivot_floor = cfg.pivot_floor;
+      la.d_idx = arr.row_idx;
+      la.d_best = arr.row_best;
+      la.d_second = arr.row_second;
+      la.d_count = d_nrows;
+      CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+    }
+    CK(launch_width(d_state, st));
+    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
+
+    // (4) core step: LU of D_k = S_row(I_k, 0:w) and the new Rt rows
+    double* dlu_k = run->Dinv.p + run->bmax * r;
+    CK(launch_cross_lu(run->L.p + run->ldL * r, run->ldL, arr.row_idx, d_width, block, dlu_k, run->bmax, st));
+    // U_k^T = A(I_k,:)^T - Rt^T * L(I_k, 0:r)^T
+    CK(launch_gather(run->L.p, run->ldL, 1, r, arr.row_idx, d_width, block, ws.Bg.p, std::max<int64_t>(r, 1), st));
+    {
+      TsGemmParams p;
+      p.M = n;
+      p.K = r;
+      p.N = block;
+      p.d_n = d_width;
+      p.A = run->Rt.p;
+      p.lda = run->ldR;
+      p.B = ws.Bg.p;
+      p.bsk = 1;
+      p.bsn = std::max<int64_t>(r, 1);
+      p.base_mode = kBaseGatherRowsT;
+      p.src = A;
+      p.lds = lda;
+      p.idx = arr.row_idx;
+      p.alpha = -1.0;
+      p.out_mode = kOutColMajor;
+      p.C0 = ws.Ut.p;
+      p.ldc0 = even(n);
+      CK(run_ts_gemm(p, st));
+    }
+    // Rt_k^T = U_k^T * D_k^{-T} by row-wise LU solves  ->  rows r..r+w of Rt
+    CK(launch_rows_lu_solve(ws.Ut.p, even(n), n, dlu_k, run->bmax, d_width, block, run->Rt.p + run->ldR * r,
+                            run->ldR, st));
+    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
+
+    // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
+    //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
+    // Yg(h, q) = Y(h, J[q]) (cp x w, ld cp), gathered before Y is overwritten
+    CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, d_width, block, ws.Yg.p, cp, st));
+    {
+      TsGemmParams p;
+      p.M = n;
+      p.K = block;
+      p.d_k = d_width;
+      p.N = static_cast<int>(cp);
+      p.A = run->Rt.p + run->ldR * r;
+      p.lda = run->ldR;
+      p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
+      p.bsk = cp;
+      p.bsn = 1;
+      p.base_mode = kBaseInPlaceRowMajor;
+      p.alpha = -1.0;
+      p.out_mode = kOutRowMajor;
+      p.C0 = ws.Y.p;
+      p.ldc0 = cp;
+      p.Wc = ws.Wc.p;
+      p.ldwc = even(n);
+      p.wc_rows = B;
+      p.norm_part = ws.part.p;
+      CK(run_ts_gemm(p, st));
+      CK(launch_sum_partials(ws.part.p, ts_gemm_grid_size(n, static_cast<int>(cp)), &d_state->ysq, st));
+    }
+    CK(launch_commit(d_state, arr, r, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ga_norm, st));
+    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
+
+    // one D2H read per iteration: the record + this iteration's pivots
+    CK(cudaMemcpyAsync(ws.h_state, ws.state.p, state_bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const IterState* hs_ = reinterpret_cast<const IterState*>(ws.h_state);
+    const int ncols = hs_->ncols, nrows = hs_->nrows;
+    for (int s = 0; s < ncols; ++s) {
+      run->step_kind.push_back(0);
+      run->step_iter.push_back(k);
+      run->step_index.push_back(harr.col_idx[s]);
+      run->step_best.push_back(harr.col_best[s]);
+      run->step_second.push_back(harr.col_second[s]);
+    }
+    if (ncols == 0) {  // driver.cpp:102-105
+      status = ITERCUR_RESIDUAL_EXHAUSTED;
+      break;
+    }
+    for (int s = 0; s < nrows; ++s) {
+      run->step_kind.push_back(1);
+      run->step_iter.push_back(k);
+      run->step_index.push_back(harr.row_idx[s]);
+      run->step_best.push_back(harr.row_best[s]);
+      run->step_second.push_back(harr.row_second[s]);
+    }
+    if (nrows == 0) {  // driver.cpp:118-121
+      status = ITERCUR_RESIDUAL_EXHAUSTED;
+      break;
+    }
+    const int width = hs_->width;
+    for (int q = 0; q < width; ++q) {
+      run->I.push_back(harr.row_idx[q]);
+      run->J.push_back(harr.col_idx[q]);
+    }
+    run->block_start.push_back(r);
+    run->block_width.push_back(width);
+    run->r = r + width;
+    rho = hs_->rho;
+    rec.rho = rho;
+    rec.cols_added = rec.rows_added = width;
+    rec.col_truncated = ncols < block;
+    rec.row_truncated = nrows < ncols;
+    rec.min_col_margin = min_margin(harr.col_best, harr.col_second, ncols);
+    rec.min_row_margin = min_margin(harr.row_best, harr.row_second, nrows);
+    if (evs.on) {
+      rec.select_cols_s = elapsed_s(evs.get(e0), evs.get(e0 + 1));
+      rec.row_residual_s = elapsed_s(evs.get(e0 + 1), evs.get(e0 + 2));
+      rec.select_rows_s = elapsed_s(evs.get(e0 + 2), evs.get(e0 + 3));
+      rec.core_s = elapsed_s(evs.get(e0 + 3), evs.get(e0 + 4));
+      rec.downdate_s = elapsed_s(evs.get(e0 + 4), evs.get(e0 + 5));
+    }
+    ++k;
+    run->iters.push_back(rec);
+    if (rho <= threshold) {  // driver.cpp:156-159
+      status = ITERCUR_CONVERGED;
+      break;
+    }
+  }
+  run->status = status;
+  run->final_rho = rho;
+  run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+// ------------------------------------------------------------------ exports
+void gather_host(const itercur_run* run, const double* src, int64_t row_stride, int64_t col_stride, int64_t K,
+                 const int64_t* d_idx, int64_t w, double* out) {
+  if (K == 0 || w == 0) return;
+  DevBuf<double> tmp;
+  tmp.alloc(static_cast<size_t>(K) * w);
+  CK(launch_gather(src, row_stride, col_stride, K, d_idx, nullptr, static_cast<int>(w), tmp.p, K, run->stream));
+  CK(cudaMemcpyAsync(out, tmp.p, sizeof(double) * K * w, cudaMemcpyDeviceToHost, run->stream));
+  CK(cudaStreamSynchronize(run->stream));
+}
+
+// X^{-1} with X = A(I,J) = Lc * Uc, Lc = L(I,:) block-lower (diagonal blocks D_k),
+// Uc = Rt(:,J) unit block-upper.  Zt = (Lc^{-1})^T by block forward substitution, then
+// Xit = (Uc^{-1} Z)^T by block back substitution; core = Xit^T.
+void core_matrix_impl(const itercur_run* run, double* out) {
+  const int64_t r = run->r;
+  if (r == 0) return;
+  cudaStream_t st = run->stream;
+  const int B = static_cast<int>(run->bmax);
+  DevBuf<double> Zt, Xit, T, Bg;
+  Zt.alloc(static_cast<size_t>(r) * r);
+  Xit.alloc(static_cast<size_t>(r) * r);
+  T.alloc(static_cast<size_t>(r) * B);
+  Bg.alloc(static_cast<size_t>(r) * B);
+  DevBuf<int64_t> seq;
+  {
+    std::vector<int64_t> h(static_cast<size_t>(r));
+    for (int64_t q = 0; q < r; ++q) h[q] = q;
+    seq.alloc(r);
+    CK(cudaMemcpyAsync(seq.p, h.data(), sizeof(int64_t) * r, cudaMemcpyHostToDevice, st));
+  }
+  const size_t nb = run->block_start.size();
+  for (size_t kb = 0; kb < nb; ++kb) {
+    const int64_t s = run->block_start[kb], w = run->block_width[kb];
+    // Bg(k', q) = Lc(s+q, k') = L(I[s+q], k'), k' < s
+    if (s > 0) CK(launch_gather(run->L.p, run->ldL, 1, s, run->dI.p + s, nullptr, static_cast<int>(w), Bg.p, s, st));
+    TsGemmParams p;
+    p.M = r;
+    p.K = s;
+    p.N = static_cast<int>(w);
+    p.A = Zt.p;
+    p.lda = r;
+    p.B = Bg.p;
+    p.bsk = 1;
+    p.bsn = std::max<int64_t>(s, 1);
+    p.base_mode = kBaseIdentityCols;
+    p.col0 = s;
+    p.alpha = -1.0;
+    p.out_mode = kOutColMajor;
+    p.C0 = T.p;
+    p.ldc0 = r;
+    CK(run_ts_gemm(p, st));
+    CK(launch_rows_lu_solve(T.p, r, r, run->Dinv.p + run->bmax * s, run->bmax, nullptr, static_cast<int>(w),
+                            Zt.p + r * s, r, st));
+  }
+  for (size_t kb = nb; kb-- > 0;) {
+    const int64_t s = run->block_start[kb], w = run->block_width[kb];
+    const int64_t e = s + w;
+    // Bg(k', q) = Uc(s+q, e+k') = Rt(s+q, J[e+k'])
+    if (r - e > 0) {
+      CK(launch_gather2(run->Rt.p + run->ldR * s, run->ldR, run->dJ.p + e, r - e, static_cast<int>(w), Bg.p, r - e, st));
+    }
+    TsGemmParams p;
+    p.M = r;
+    p.K = r - e;
+    p.N = static_cast<int>(w);
+    p.A = Xit.p + r * e;
+    p.lda = r;
+    p.B = Bg.p;
+    p.bsk = 1;
+    p.bsn = std::max<int64_t>(r - e, 1);
+    p.base_mode = kBaseContigCols;
+    p.src = Zt.p;
+    p.lds = r;
+    p.col0 = s;
+    p.alpha = -1.0;
+    p.out_mode = kOutColMajor;
+    p.C0 = Xit.p + r * s;
+    p.ldc0 = r;
+    CK(run_ts_gemm(p, st));
+  }
+  std::vector<double> h(static_cast<size_t>(r) * r);
+  CK(cudaMemcpyAsync(h.data(), Xit.p, sizeof(double) * r * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int64_t j = 0; j < r; ++j)
+    for (int64_t i = 0; i < r; ++i) out[i + j * r] = h[j + i * r];  // core = Xit^T
+}
+
+double true_error_impl(const itercur_run* run) {
+  cudaStream_t st = run->stream;
+  const double asq = device_sumsq(run->A, run->m, run->n, run->lda, st);
+  const double a_norm = std::sqrt(asq);
+  if (a_norm == 0.0) return 0.0;
+  if (run->r == 0) return 1.0;
+  TsGemmParams p;
+  p.M = run->m;
+  p.K = run->r;
+  p.N = static_cast<int>(std::min<int64_t>(run->n, 1 << 30));
+  p.A = run->L.p;
+  p.lda = run->ldL;
+  p.B = run->Rt.p;
+  p.bsk = run->ldR;
+  p.bsn = 1;
+  p.base_mode = kBaseContigCols;
+  p.src = run->A;
+  p.lds = run->lda;
+  p.col0 = 0;
+  p.alpha = -1.0;
+  p.out_mode = kOutNone;
+  const int64_t parts = ts_gemm_grid_size(p.M, p.N);
+  DevBuf<double> part, outd;
+  part.alloc(parts);
+  outd.alloc(1);
+  p.norm_part = part.p;
+  CK(run_ts_gemm(p, st));
+  CK(launch_sum_partials(part.p, parts, outd.p, st));
+  double sq = 0.0;
+  CK(cudaMemcpyAsync(&sq, outd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return std::sqrt(sq) / a_norm;
+}
+
+void require_device() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    fail(ITERCUR_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) fail(ITERCUR_E_CUDA, "the B200 engine requires an sm_100 device");
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+void itercur_config_default(itercur_config* cfg) { *cfg = default_config(); }
+const char* itercur_last_error(void) { return g_last_error.c_str(); }
+int itercur_abi_version(void) { return ITERCUR_B200_ABI_VERSION; }
+
+int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
+                                 void* stream, itercur_run** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require_device();
+    auto run = std::make_unique<itercur_run>();
+    CK(cudaGetDevice(&run->device));
+    run->stream = static_cast<cudaStream_t>(stream);
+    run->m = m;
+    run->n = n;
+    run->lda = lda;
+    run->A = dA;
+    run->cfg = cfg ? *cfg : default_config();
+    run_iterative_cur(run.get());
+    *out = run.release();
+  });
+}
+
+int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
+                               itercur_run** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require_device();
+    auto run = std::make_unique<itercur_run>();
+    CK(cudaGetDevice(&run->device));
+    run->stream = nullptr;
+    run->m = m;
+    run->n = n;
+    run->lda = std::max<int64_t>(m, 1);
+    if (m > 0 && n > 0) {
+      run->A_owned.alloc(static_cast<size_t>(m) * n);
+      CK(cudaMemcpy2DAsync(run->A_owned.p, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
+                           cudaMemcpyHostToDevice, run->stream));
+      run->A = run->A_owned.p;
+    }
+    run->cfg = cfg ? *cfg : default_config();
+    run_iterative_cur(run.get());
+    *out = run.release();
+  });
+}
+
+int64_t itercur_run_rank(const itercur_run* run) { return run ? run->r : 0; }
+int64_t itercur_run_rows(const itercur_run* run) { return run ? run->m : 0; }
+int64_t itercur_run_cols(const itercur_run* run) { return run ? run->n : 0; }
+int itercur_run_indices(const itercur_run* run, int64_t* row_indices, int64_t* col_indices) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    if (row_indices) std::copy(run->I.begin(), run->I.end(), row_indices);
+    if (col_indices) std::copy(run->J.begin(), run->J.end(), col_indices);
+  });
+}
+int32_t itercur_run_status(const itercur_run* run) { return run ? run->status : ITERCUR_CONVERGED; }
+double itercur_run_final_rho(const itercur_run* run) { return run ? run->final_rho : 1.0; }
+double itercur_run_threshold(const itercur_run* run) { return run ? run->threshold : 0.0; }
+double itercur_run_sketch_seconds(const itercur_run* run) { return run ? run->sketch_s : 0.0; }
+double itercur_run_total_seconds(const itercur_run* run) { return run ? run->total_s : 0.0; }
+double itercur_run_ga_norm(const itercur_run* run) { return run ? run->ga_norm : 0.0; }
+const char* itercur_run_note(const itercur_run* run) { return run ? run->note.c_str() : ""; }
+int64_t itercur_run_num_iterations(const itercur_run* run) { return run ? static_cast<int64_t>(run->iters.size()) : 0; }
+int itercur_run_iterations(const itercur_run* run, itercur_iteration_record* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    std::copy(run->iters.begin(), run->iters.end(), out);
+  });
+}
+int64_t itercur_run_num_steps(const itercur_run* run) { return run ? static_cast<int64_t>(run->step_index.size()) : 0; }
+int itercur_run_steps(const itercur_run* run, int32_t* kind, int64_t* iter, int64_t* index, double* best,
+                      double* second) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    std::copy(run->step_kind.begin(), run->step_kind.end(), kind);
+    std::copy(run->step_iter.begin(), run->step_iter.end(), iter);
+    std::copy(run->step_index.begin(), run->step_index.end(), index);
+    std::copy(run->step_best.begin(), run->step_best.end(), best);
+    std::copy(run->step_second.begin(), run->step_second.end(), second);
+  });
+}
+int itercur_run_c_matrix(const itercur_run* run, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    // C(i, q) = A(i, J[q]): out(k=i, q) = A[i * 1 + J[q] * lda]
+    gather_host(run, run->A, 1, run->lda, run->m, run->dJ.p, run->r, out);
+  });
+}
+int itercur_run_r_matrix(const itercur_run* run, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    // R^T(j, q) = A(I[q], j): gathered as (n x r), then transposed on the host
+    std::vector<double> t(static_cast<size_t>(run->n) * run->r);
+    gather_host(run, run->A, run->lda, 1, run->n, run->dI.p, run->r, t.data());
+    for (int64_t q = 0; q < run->r; ++q)
+      for (int64_t j = 0; j < run->n; ++j) out[q + j * run->r] = t[j + q * run->n];
+  });
+}
+int itercur_run_core_matrix(const itercur_run* run, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    core_matrix_impl(run, out);
+  });
+}
+int itercur_true_relative_error_device(const itercur_run* run, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    *out = true_error_impl(run);
+  });
+}
+void itercur_run_free(itercur_run* run) { delete run; }
+
+int itercur_adjusted_threshold(double epsilon, double delta, double alpha, int64_t c, double* out) {
+  return guarded([&] { *out = adjusted_threshold_impl(epsilon, delta, alpha, c); });
+}
+int itercur_gratton_tail(int64_t c, double tau, double* out) {
+  return guarded([&] { *out = gratton_tail_impl(c, tau); });
+}
+int64_t itercur_sketch_rows_for_block(int64_t b) { return sketch_rows(b); }
+
+int itercur_gaussian_matrix_device(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* dOut,
+                                   void* stream) {
+  return guarded([&] {
+    require_device();
+    CK(launch_gaussian_matrix(rows, cols, seed, stream_tag, dOut, static_cast<cudaStream_t>(stream)));
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int itercur_sketch_device(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, uint64_t seed, int32_t kind,
+                          int32_t sparse_nnz, double* dY, double* ga_norm, double* a_norm, void* stream) {
+  return guarded([&] {
+    require_device();
+    // make_sketch validation, proj/src/sketch.cpp:11-13
+    if (b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
+    if (m == 0 || n == 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonempty");
+    if (b > m) fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
+    DevBuf<double> S, Yp, wsb, scal;
+    S.alloc(static_cast<size_t>(cp) * ldg);
+    Yp.alloc(static_cast<size_t>(cp) * n);
+    const int64_t wse = sketch_workspace_elems(m, n, cp);
+    wsb.alloc(wse);
+    scal.alloc(2);
+    const int k = kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
+    CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, seed, k, sparse_nnz, st));
+    double scale = 1.0;
+    if (k == kSketchSparseSign)
+      scale = 1.0 / std::sqrt(static_cast<double>(std::min<int64_t>(std::max(sparse_nnz, 1), c)));
+    SketchStats stats{scal.p, scal.p + 1};
+    CK(run_sketch_apply(dA, m, n, lda, S.p, ldg, cp, scale, Yp.p, wsb.p, wse, stats, st, nullptr));
+    // compact to ld = c
+    CK(cudaMemcpy2DAsync(dY, sizeof(double) * c, Yp.p, sizeof(double) * cp, sizeof(double) * c, n,
+                         cudaMemcpyDeviceToDevice, st));
+    double h[2];
+    CK(cudaMemcpyAsync(h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (a_norm) *a_norm = std::sqrt(h[0]);
+    if (ga_norm) *ga_norm = std::sqrt(h[1]);
+  });
+}
+
+int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b, int32_t is_columns,
+                          double pivot_floor, const int64_t* exclude, int64_t n_exclude, int64_t* idx_out,
+                          int64_t* n_idx, int32_t* truncated, double* last_pivot, double* best_out,
+                          double* second_out, void* stream) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // select.cpp:24-28, 124-126, 143
+    if (!(pivot_floor > 0.0 && pivot_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+    if (is_columns && (b < 0 || b > rows))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "select_columns: block size " + std::to_string(b) + " exceeds sketch rows " +
+                                           std::to_string(rows));
+    if (!is_columns && b < 0) fail(ITERCUR_E_INVALID_ARGUMENT, "select_rows: negative block size");
+    // LUPP works on W = M^T (columns) or M (rows); candidates are W's rows
+    const int64_t wrows = is_columns ? cols : rows;
+    const int64_t wcols = is_columns ? rows : cols;
+    const int64_t steps = std::min<int64_t>(is_columns ? b : std::min(b, cols), wcols);
+    std::vector<uint8_t> hmask(static_cast<size_t>(std::max<int64_t>(wrows, 1)), 0);
+    for (int64_t q = 0; q < n_exclude; ++q) {
+      const int64_t e = exclude[q];
+      if (e < 0 || e >= wrows)
+        fail(ITERCUR_E_OUT_OF_RANGE, std::string(is_columns ? "select_columns" : "select_rows") +
+                                         ": excluded index " + std::to_string(e) + " out of range");
+      hmask[e] = 1;
+    }
+    if (rows * cols > 0) {
+      const unsigned long long zero = 0;
+      (void)zero;
+      DevBuf<unsigned long long> cnt;
+      cnt.alloc(1);
+      CK(launch_count_nonfinite(dM, rows, cols, ldm, cnt.p, st));
+      unsigned long long h = 0;
+      CK(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (h) fail(ITERCUR_E_INVALID_ARGUMENT, "selection input must be finite");
+    }
+    *n_idx = 0;
+    *last_pivot = 0.0;
+    if (steps <= 0 || wrows == 0) {
+      *truncated = (0 < b) ? 1 : 0;
+      return;
+    }
+    DevBuf<double> W, scal;
+    DevBuf<uint8_t> mask;
+    DevBuf<char> scratch, outs;
+    const int64_t ldw = even(wrows);
+    W.alloc(static_cast<size_t>(ldw) * steps);
+    if (is_columns)
+      CK(launch_transpose_rows(dM, ldm, cols, static_cast<int>(steps), W.p, ldw, st));
+    else
+      CK(cudaMemcpy2DAsync(W.p, sizeof(double) * ldw, dM, sizeof(double) * ldm, sizeof(double) * rows, steps,
+                           cudaMemcpyDeviceToDevice, st));
+    scal.alloc(1);
+    DevBuf<double> part;
+    part.alloc(148 * 8);
+    CK(launch_sumsq(dM, rows, cols, ldm, part.p, 148 * 8, scal.p, st));
+    mask.alloc(wrows);
+    CK(cudaMemcpyAsync(mask.p, hmask.data(), wrows, cudaMemcpyHostToDevice, st));
+    scratch.alloc(lupp_scratch_bytes());
+    const int S = static_cast<int>(steps);
+    outs.alloc(sizeof(int64_t) * S * 3 + 16);
+    int64_t* d_idx = reinterpret_cast<int64_t*>(outs.p);
+    double* d_best = reinterpret_cast<double*>(d_idx + S);
+    double* d_second = d_best + S;
+    int* d_count = reinterpret_cast<int*>(d_second + S);
+    LuppArgs la{};
+    la.W = W.p;
+    la.rows = wrows;
+    la.ldw = ldw;
+    la.cols_max = S;
+    la.mask = mask.p;
+    la.epoch = 2;
+    la.d_norm_sq = scal.p;
+    la.pivot_floor = pivot_floor;
+    la.d_idx = d_idx;
+    la.d_best = d_best;
+    la.d_second = d_second;
+    la.d_count = d_count;
+    CK(run_lupp_with_scratch(la, scratch.p, st, nullptr));
+    std::vector<char> h(outs.count);
+    CK(cudaMemcpyAsync(h.data(), outs.p, outs.count, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t* hi = reinterpret_cast<const int64_t*>(h.data());
+    const double* hb = reinterpret_cast<const double*>(hi + S);
+    const double* hsd = hb + S;
+    const int cnt = *reinterpret_cast<const int*>(hsd + S);
+    *n_idx = cnt;
+    for (int q = 0; q < cnt; ++q) {
+      idx_out[q] = hi[q];
+      if (best_out) best_out[q] = hb[q];
+      if (second_out) second_out[q] = hsd[q];
+    }
+    *last_pivot = cnt > 0 ? hb[cnt - 1] : 0.0;
+    *truncated = cnt < b ? 1 : 0;
+  });
+}
+
+int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, int32_t kind,
+                               int32_t reps, void* stream, double* ms_per_launch, int32_t* ctas, int32_t* splits,
+                               int32_t* uses_tma) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
+    DevBuf<double> S, Y, wsb;
+    S.alloc(static_cast<size_t>(cp) * ldg);
+    Y.alloc(static_cast<size_t>(cp) * n);
+    const int64_t wse = sketch_workspace_elems(m, n, cp);
+    wsb.alloc(wse);
+    CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, 0, kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign
+                                                                                          : kSketchGaussian,
+                                  8, st));
+    SketchLaunchInfo info;
+    CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, wse, st, &info));  // warm-up
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    for (int q = 0; q < reps; ++q) CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, wse, st, &info));
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_per_launch = ms / std::max(reps, 1);
+    if (ctas) *ctas = info.ctas;
+    if (splits) *splits = info.splits;
+    if (uses_tma) *uses_tma = info.tma ? 1 : 0;
+  });
+}
+
+}  // extern "C"

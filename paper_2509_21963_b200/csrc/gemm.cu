@@ -1,0 +1,221 @@
+// gemm.cu — tall-skinny FP64 DMMA GEMM with gather/in-place epilogues, the workhorse of
+// the per-iteration stages of the incremental (block-LU / Schur) form of IterativeCUR
+// (SURVEY.md A.7), replacing the reference's per-iteration Eigen products:
+//   row residual  S_row = A(:,J_k) - L * Rt(:,J_k)           (proj/src/sketch.cpp:43-60)
+//   new U block   U_k^T = A(I_k,:)^T - Rt^T * L(I_k,:)^T      (proj/src/pinv.cpp:94-111 rebuild)
+//   Rt block      Rt_k^T = U_k^T * D_k^{-T}
+//   Y downdate    Y^T -= Rt_k^T * Y(:,J_k)^T  in place         (proj/src/sketch.cpp:26-41)
+//   verification  ||A(:,P) - L * Rt(:,P)||^2                   (proj/src/driver.cpp:169-190)
+//
+//   C (M x N) = base(M x N) + alpha * Aop(M x K) * B(K x N)
+// Aop is M-contiguous (column-major, even ld); B has arbitrary strides (tiny). The M and K
+// dimensions are permuted inside each 16x8x8 DMMA so that every A and B fragment pair is
+// one 16-byte shared load: logical rows (g, g+8) -> physical (2g, 2g+1), logical k
+// (t, t+4) -> physical (2t, 2t+1). Tiles are staged with cp.async in a 4-deep ring.
+#include <algorithm>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace itercur_b200 {
+
+constexpr int kGemmWarps = 8;
+constexpr int kGemmThreads = kGemmWarps * 32;
+constexpr int kGemmBM = kGemmWarps * 16;  // 128 rows per CTA
+constexpr int kGemmKT = 16;               // k per stage
+constexpr int kGemmStages = 4;
+constexpr int kBPitch = kGemmKT + 2;      // doubles; 144 B rows -> conflict-free 16-B fragment loads
+
+template <int NT>
+struct GemmSmem {
+  static constexpr int A_ELEMS = kGemmKT * kGemmBM;
+  static constexpr int B_ELEMS = NT * 8 * kBPitch;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int BYTES = kGemmStages * STAGE_ELEMS * 8;
+};
+
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int NT>
+__device__ __forceinline__ void gemm_load_stage(const TsGemmParams& p, double* sA, double* sB, int64_t i0, int64_t k0,
+                                                int64_t q0, int nvalid, int64_t K) {
+  // A tile: [kGemmKT][kGemmBM], 16-byte chunks of two consecutive rows
+  constexpr int A_CHUNKS = kGemmKT * kGemmBM / 2;
+  for (int c = threadIdx.x; c < A_CHUNKS; c += kGemmThreads) {
+    const int kl = c / (kGemmBM / 2), il = (c % (kGemmBM / 2)) * 2;
+    const int64_t k = k0 + kl, i = i0 + il;
+    int bytes = 0;
+    const double* src = p.A;
+    if (k < K && i < p.M) {
+      bytes = (i + 1 < p.M) ? 16 : 8;
+      src = p.A + i + k * p.lda;
+    }
+    cp_async_16(sA + kl * kGemmBM + il, src, bytes);
+  }
+  // B tile: [NT*8][kBPitch], element (k, q) -> sB[q * kBPitch + k]
+  constexpr int B_ELEMS = NT * 8 * kGemmKT;
+  for (int e = threadIdx.x; e < B_ELEMS; e += kGemmThreads) {
+    const int ql = e / kGemmKT, kl = e % kGemmKT;
+    const int64_t k = k0 + kl;
+    const int64_t q = q0 + ql;
+    int bytes = 0;
+    const double* src = p.B;
+    if (k < K && ql < nvalid) {
+      bytes = 8;
+      src = p.B + k * p.bsk + q * p.bsn;
+    }
+    cp_async_8(sB + ql * kBPitch + kl, src, bytes);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kGemmThreads, 2) ts_gemm_kernel(TsGemmParams p) {
+  using SM = GemmSmem<NT>;
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ double red[kGemmWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kGemmBM;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * (NT * 8);
+  int n_total = p.N;
+  if (p.d_n) n_total = min(n_total, *p.d_n);
+  int64_t nv = static_cast<int64_t>(n_total) - q0;
+  nv = nv < 0 ? 0 : (nv > NT * 8 ? NT * 8 : nv);
+  const int nvalid = static_cast<int>(nv);
+
+  double acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
+
+  int64_t K = p.K;
+  if (p.d_k) K = min(K, static_cast<int64_t>(*p.d_k));
+  const int nk = nvalid > 0 ? static_cast<int>(ceil_div(K, kGemmKT)) : 0;
+#pragma unroll
+  for (int s = 0; s < kGemmStages - 1; ++s) {
+    if (s < nk) gemm_load_stage<NT>(p, gsm + s * SM::STAGE_ELEMS, gsm + s * SM::STAGE_ELEMS + SM::A_ELEMS, i0,
+                                    static_cast<int64_t>(s) * kGemmKT, q0, nvalid, K);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<kGemmStages - 2>();
+    __syncthreads();
+    const int nxt = it + kGemmStages - 1;
+    if (nxt < nk) {
+      double* base = gsm + (nxt % kGemmStages) * SM::STAGE_ELEMS;
+      gemm_load_stage<NT>(p, base, base + SM::A_ELEMS, i0, static_cast<int64_t>(nxt) * kGemmKT, q0, nvalid, K);
+    }
+    cp_async_commit();
+    const double* sA = gsm + (it % kGemmStages) * SM::STAGE_ELEMS;
+    const double* sB = sA + SM::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < kGemmKT; kk += 8) {
+      const int rb = warp * 16 + 2 * g;
+      const double2 a01 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t) * kGemmBM + rb);
+      const double2 a23 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t + 1) * kGemmBM + rb);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 b = *reinterpret_cast<const double2*>(sB + (nt * 8 + g) * kBPitch + kk + 2 * t);
+        dmma_16x8x8(acc[nt], a01.x, a01.y, a23.x, a23.y, b.x, b.y);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---------------- epilogue: physical rows (2g, 2g+1), columns (2t, 2t+1) ----------
+  double sq = 0.0;
+  const int64_t r0 = i0 + warp * 16 + 2 * g;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq) {
+      const int ql = nt * 8 + 2 * t + dq;
+      if (ql >= nvalid) continue;
+      const int64_t q = q0 + ql;
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int64_t i = r0 + dr;
+        if (i >= p.M) continue;
+        double base = 0.0;
+        switch (p.base_mode) {
+          case kBaseGatherCols: base = p.src[i + p.idx[q] * p.lds]; break;
+          case kBaseGatherRowsT: base = p.src[p.idx[q] + i * p.lds]; break;
+          case kBaseContigCols: base = p.src[i + (p.col0 + q) * p.lds]; break;
+          case kBaseInPlaceRowMajor: base = p.C0[i * p.ldc0 + q]; break;
+          case kBaseIdentityCols: base = (i == p.col0 + q) ? 1.0 : 0.0; break;
+          default: break;
+        }
+        const double v = base + p.alpha * acc[nt][dr * 2 + dq];
+        sq = fma(v, v, sq);
+        if (p.out_mode == kOutColMajor) {
+          p.C0[i + q * p.ldc0] = v;
+          if (p.C1) p.C1[i + q * p.ldc1] = v;
+        } else if (p.out_mode == kOutRowMajor) {
+          p.C0[i * p.ldc0 + q] = v;
+          if (p.Wc && q < p.wc_rows) p.Wc[i + q * p.ldwc] = v;
+        }
+      }
+    }
+  }
+  if (p.norm_part) {
+    sq = warp_sum(sq);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kGemmWarps; ++w) s += red[w];
+      p.norm_part[blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+template <int NT>
+static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
+  const int smem = GemmSmem<NT>::BYTES;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(ts_gemm_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(p.M, kGemmBM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
+  ts_gemm_kernel<NT><<<grid, kGemmThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+int ts_gemm_nt(int n) { return static_cast<int>(std::min<int64_t>(9, std::max<int64_t>(1, ceil_div(n, 8)))); }
+
+int64_t ts_gemm_grid_size(int64_t M, int N) {
+  const int nt = ts_gemm_nt(N);
+  return ceil_div(M, kGemmBM) * ceil_div(N, nt * 8);
+}
+
+cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  switch (ts_gemm_nt(p.N)) {
+    case 1: return launch_nt<1>(p, st);
+    case 2: return launch_nt<2>(p, st);
+    case 3: return launch_nt<3>(p, st);
+    case 4: return launch_nt<4>(p, st);
+    case 5: return launch_nt<5>(p, st);
+    case 6: return launch_nt<6>(p, st);
+    case 7: return launch_nt<7>(p, st);
+    case 8: return launch_nt<8>(p, st);
+    default: return launch_nt<9>(p, st);
+  }
+}
+
+}  // namespace itercur_b200

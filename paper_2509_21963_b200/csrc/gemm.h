@@ -1,0 +1,54 @@
+// gemm.h — parameters of the tall-skinny DMMA GEMM (gemm.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace itercur_b200 {
+
+enum GemmBase {
+  kBaseNone = 0,
+  kBaseGatherCols = 1,
+  kBaseGatherRowsT = 2,
+  kBaseContigCols = 3,
+  kBaseInPlaceRowMajor = 4,
+  kBaseIdentityCols = 5  // base(i, q) = (i == col0 + q)
+};
+enum GemmOut { kOutNone = 0, kOutColMajor = 1, kOutRowMajor = 2 };
+
+// C(M x N) = base(M x N) + alpha * Aop(M x K) * B(K x N)
+//   Aop(i, k) = A[i + k * lda]        (lda even, A 16-byte aligned)
+//   B(k, q)   = B[k * bsk + q * bsn]
+//   base: none | src(i, idx[q]) | src(idx[q], i) | src(i, col0 + q) | C0(i, q) row-major
+//   out:  none (norm only) | C0/C1 column-major | C0 row-major (+ Wc(i, q) = C for q < wc_rows)
+struct TsGemmParams {
+  int64_t M = 0, K = 0;
+  const int* d_k = nullptr;  // optional dynamic cap on K (device int)
+  int N = 0;               // columns (host bound); grid.y covers N in chunks of 8*NT
+  const int* d_n = nullptr;  // optional dynamic cap on N (device int)
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* B = nullptr;
+  int64_t bsk = 0, bsn = 0;
+  int base_mode = kBaseNone;
+  const double* src = nullptr;
+  int64_t lds = 0;
+  const int64_t* idx = nullptr;
+  int64_t col0 = 0;
+  double alpha = -1.0;
+  int out_mode = kOutColMajor;
+  double* C0 = nullptr;
+  int64_t ldc0 = 0;
+  double* C1 = nullptr;
+  int64_t ldc1 = 0;
+  double* Wc = nullptr;
+  int64_t ldwc = 0;
+  int wc_rows = 0;
+  double* norm_part = nullptr;  // [grid.y * grid.x] per-CTA sum of squares of C
+};
+
+cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st);
+int64_t ts_gemm_grid_size(int64_t M, int N);
+
+}  // namespace itercur_b200

@@ -1,0 +1,68 @@
+// kernels.h — host-side launchers of the sm_100a IterativeCUR kernels (internal API).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace itercur_b200 {
+
+constexpr uint32_t kStreamSketch = 1;      // RngStream::Sketch, proj/include/itercur/rng.hpp:13
+constexpr uint32_t kStreamSparseSign = 7;  // new tag
+constexpr int kSketchGaussian = 0;
+constexpr int kSketchSparseSign = 1;
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+// ---------------------------------------------------------------------------- sketch
+// Dense sketch operator S (rows_pad x ldg, row-major: S[h * ldg + k]), rows h >= c and
+// columns k >= m are zero. Gaussian: S(h,k) = normal_at(seed, Sketch, h, k)
+// (proj/src/sketch.cpp:19 -> rng.cpp:61-67). Sparse-sign: +-1 at the A.8 positions.
+cudaError_t launch_gen_sketch_operator(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed,
+                                       int kind, int zeta, cudaStream_t st);
+
+struct SketchStats {
+  double* d_asq;  // ||A||_F^2 (device scalar)
+  double* d_ysq;  // ||Y||_F^2 (device scalar)
+};
+
+// Y (c_pad x n, ld c_pad, column-major) = scale * S(0:c_pad, :) * A, plus ||A||^2 and ||Y||^2
+// reduced deterministically into device scalars. Uses TMA when A's layout allows it.
+// Returns the split count and timing info via out params (host side).
+struct SketchLaunchInfo {
+  int splits = 1;
+  int ctas = 0;
+  int nt = 0;
+  bool tma = false;
+  int dominant_launches = 0;  // launches of the DMMA kernel
+};
+cudaError_t run_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
+                             int64_t c_pad, double scale, double* Y, double* workspace, int64_t workspace_elems,
+                             const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info);
+int64_t sketch_workspace_elems(int64_t m, int64_t n, int64_t c_pad);
+// Stand-alone timing hook: the DMMA kernel only (for roofline measurement).
+cudaError_t run_sketch_dmma_only(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
+                                 int64_t c_pad, double* Y, double* workspace, int64_t workspace_elems, cudaStream_t st,
+                                 SketchLaunchInfo* info);
+
+// ------------------------------------------------------------------------------ LUPP
+struct LuppArgs {
+  double* W;                // rows x cols_max column-major working copy (modified in place)
+  int64_t rows;
+  int64_t ldw;
+  int cols_max;             // columns present in W
+  const int* d_steps;       // dynamic requested steps (device int), capped by cols_max
+  uint8_t* mask;            // per-row ban mask: 1 = permanently banned, `epoch` = banned in this call
+  uint8_t epoch;
+  const double* d_norm_sq;  // ||M||_F^2 for the absolute floor; nullptr -> computed from W
+  double pivot_floor;
+  int64_t* d_idx;           // out: pivots
+  double* d_best;           // out: |pivot|
+  double* d_second;         // out: runner-up magnitude (margin log)
+  int* d_count;             // out: accepted pivots
+  int requested_b;          // for `truncated` semantics (host side)
+};
+size_t lupp_scratch_bytes();
+cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used);
+cudaError_t launch_clear_epochs(uint8_t* mask, int64_t count, cudaStream_t st);
+
+}  // namespace itercur_b200

@@ -1,0 +1,255 @@
+// misc.cu — small per-iteration kernels: gathers of the selected rows/columns
+// (proj/src/matrix.cpp:134-227 gather_cols / gather_rows / gather_block), the w x w
+// cross-block inverse D_k^{-1} (the reference's per-iteration COD of the r x r cross
+// block, proj/src/pinv.cpp:45-65, becomes an O(w^3) block step), deterministic norm
+// reductions and the iteration commit (index append, masks, rho = ||Y||/||GA||,
+// proj/src/sketch.cpp:40 and proj/src/driver.cpp:123-159).
+#include <algorithm>
+
+#include "common.cuh"
+#include "misc.h"
+
+namespace itercur_b200 {
+
+// Wc(j, h) = Y(h, j) for h < rows  (Wc column-major n x rows)
+__global__ void transpose_rows_kernel(const double* __restrict__ Y, int64_t cp, int64_t n, int rows,
+                                      double* __restrict__ Wc, int64_t ldwc) {
+  const int64_t total = n * rows;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = e / n, j = e - h * n;
+    Wc[j + h * ldwc] = Y[h + j * cp];
+  }
+}
+
+// out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < w (dynamic), zero for q >= w
+__global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride, int64_t col_stride, int64_t K,
+                              const int64_t* __restrict__ idx, const int* __restrict__ d_w, int w_max,
+                              double* __restrict__ out, int64_t ldo) {
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  const int64_t total = K * w_max;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / K, k = e - q * K;
+    out[k + q * ldo] = q < w ? src[k * row_stride + idx[q] * col_stride] : 0.0;
+  }
+}
+
+cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int rows, double* Wc, int64_t ldwc,
+                                  cudaStream_t st) {
+  const int64_t total = n * rows;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  transpose_rows_kernel<<<blocks, 256, 0, st>>>(Y, cp, n, rows, Wc, ldwc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
+                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st) {
+  const int64_t total = K * w_max;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  gather_kernel<<<blocks, 256, 0, st>>>(src, row_stride, col_stride, K, d_idx, d_w, w_max, out, ldo);
+  return cudaGetLastError();
+}
+
+__global__ void gather2_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ idx, int64_t K,
+                               int w, double* __restrict__ out, int64_t ldo) {
+  const int64_t total = K * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / K, k = e - q * K;
+    out[k + q * ldo] = src[idx[k] + q * ld];
+  }
+}
+cudaError_t launch_gather2(const double* src, int64_t ld, const int64_t* d_idx, int64_t K, int w, double* out,
+                           int64_t ldo, cudaStream_t st) {
+  const int64_t total = K * w;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  gather2_kernel<<<blocks, 256, 0, st>>>(src, ld, d_idx, K, w, out, ldo);
+  return cudaGetLastError();
+}
+
+__global__ void gaussian_matrix_kernel(int64_t rows, int64_t cols, uint64_t seed, uint32_t tag, double* __restrict__ out) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    out[e] = normal_at_dev(seed, tag, i, j);
+  }
+}
+cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* out,
+                                   cudaStream_t st) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 16));
+  gaussian_matrix_kernel<<<blocks, 256, 0, st>>>(rows, cols, seed, stream_tag, out);
+  return cudaGetLastError();
+}
+
+// D(p, q) = L_k(I_k[p], q) for p, q < w. Doolittle LU without pivoting — the rows are
+// already in LUPP pivot order, so these are exactly the row-LUPP's eliminations. The
+// factors (unit-lower multipliers below the diagonal, U on and above) stay in `lu`; the
+// block is never inverted explicitly (an explicit inverse loses accuracy in proportion to
+// cond(D_k), which reaches 1e9+ once pivots hit the noise floor).
+__global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
+                                const int* __restrict__ d_w, int w_max, double* __restrict__ lu, int64_t ldd) {
+  const int w = min(*d_w, w_max);
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int p = e % w, q = e / w;
+    lu[p + q * ldd] = Lk[rows[p] + q * ldl];
+  }
+  __syncthreads();
+  for (int s = 0; s < w; ++s) {
+    const double piv = lu[s + s * ldd];
+    const int rem = w - s - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int p = s + 1 + e % rem;
+      const int tq = s + 1 + e / rem;
+      const double f = __ddiv_rn(lu[p + s * ldd], piv);
+      lu[p + tq * ldd] = __dsub_rn(lu[p + tq * ldd], __dmul_rn(f, lu[s + tq * ldd]));
+    }
+    __syncthreads();
+    for (int p = s + 1 + threadIdx.x; p < w; p += blockDim.x) lu[p + s * ldd] = __ddiv_rn(lu[p + s * ldd], piv);
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
+                            double* lu, int64_t ldd, cudaStream_t st) {
+  cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd);
+  return cudaGetLastError();
+}
+
+// Row-wise solves D x = u with D = Lhat * Uhat (cross_lu_kernel layout) for every row u of
+// X (M x w, column-major), i.e. out = X * D^{-T}: forward substitution with the unit-lower
+// Lhat, then back substitution with Uhat. One thread per row; the factors sit in shared
+// memory. Backward stable, unlike multiplying by an explicit D^{-1}.
+template <int WMAX>
+__global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                     const double* __restrict__ lu, int64_t ldd, const int* __restrict__ d_w,
+                                     int w_max, double* __restrict__ out, int64_t ldo) {
+  extern __shared__ double slu[];
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+  __syncthreads();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+    double x[WMAX];
+#pragma unroll 4
+    for (int q = 0; q < w; ++q) x[q] = X[j + q * ldx];
+    for (int q = 1; q < w; ++q) {  // Lhat y = u
+      double v = x[q];
+      for (int p = 0; p < q; ++p) v = __dsub_rn(v, __dmul_rn(slu[q + p * w], x[p]));
+      x[q] = v;
+    }
+    for (int q = w - 1; q >= 0; --q) {  // Uhat x = y
+      double v = x[q];
+      for (int p = q + 1; p < w; ++p) v = __dsub_rn(v, __dmul_rn(slu[q + p * w], x[p]));
+      x[q] = __ddiv_rn(v, slu[q + q * w]);
+    }
+    for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q];
+  }
+}
+
+cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
+                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st) {
+  if (M <= 0 || w_max <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 8));
+  const size_t smem = sizeof(double) * static_cast<size_t>(w_max) * w_max;
+  if (w_max <= 64) {
+    rows_lu_solve_kernel<64><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo);
+  } else if (w_max <= 256) {
+    cudaFuncSetAttribute(rows_lu_solve_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    rows_lu_solve_kernel<256><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo);
+  } else {
+    return cudaErrorInvalidValue;  // blocks wider than 256 are rejected by the driver
+  }
+  return cudaGetLastError();
+}
+
+// Sum `count` partials into *out in a fixed order (one CTA).
+__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t count, double* __restrict__ out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += p[i];
+  const double b = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *out = b;
+}
+cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st) {
+  sum_partials_kernel<<<1, 256, 0, st>>>(partials, count, d_out);
+  return cudaGetLastError();
+}
+
+// Per-block sum of squares over a strided 2D region (rows x cols, ld), then fixed-order sum.
+__global__ void sumsq_kernel(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                             double* __restrict__ part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const double v = x[i + j * ld];
+    s = fma(v, v, s);
+  }
+  const double b = block_sum<256>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = b;
+}
+cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partials, int max_parts,
+                         double* d_out, cudaStream_t st) {
+  const int64_t total = rows * cols;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), max_parts)));
+  sumsq_kernel<<<blocks, 256, 0, st>>>(x, rows, cols, ld, partials);
+  sum_partials_kernel<<<1, 256, 0, st>>>(partials, blocks, d_out);
+  return cudaGetLastError();
+}
+
+// count of non-finite entries (exact check behind a non-finite ||A||^2)
+__global__ void nonfinite_kernel(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                 unsigned long long* __restrict__ count) {
+  unsigned long long c = 0;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    if (!isfinite(x[i + j * ld])) ++c;
+  }
+  if (c) atomicAdd(count, c);
+}
+cudaError_t launch_count_nonfinite(const double* x, int64_t rows, int64_t cols, int64_t ld, unsigned long long* d_count,
+                                   cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows * cols, 256), 148 * 8)));
+  nonfinite_kernel<<<blocks, 256, 0, st>>>(x, rows, cols, ld, d_count);
+  return cudaGetLastError();
+}
+
+// Iteration commit: width = min(|cols|, |rows|) (driver.cpp:123), append the first `width`
+// pivots to I, J (device lists), ban them for later iterations, rho = ||Y|| / ||GA||.
+__global__ void commit_kernel(IterState* s, IterArrays arr, int64_t r, int64_t* __restrict__ I_all,
+                              int64_t* __restrict__ J_all, uint8_t* __restrict__ row_mask,
+                              uint8_t* __restrict__ col_mask, double ga_norm) {
+  const int width = min(s->ncols, s->nrows);
+  if (threadIdx.x == 0) {
+    s->width = width;
+    s->rho = ga_norm > 0.0 ? sqrt(s->ysq) / ga_norm : 0.0;
+  }
+  for (int q = threadIdx.x; q < width; q += blockDim.x) {
+    I_all[r + q] = arr.row_idx[q];
+    J_all[r + q] = arr.col_idx[q];
+    row_mask[arr.row_idx[q]] = 1;
+    col_mask[arr.col_idx[q]] = 1;
+  }
+}
+cudaError_t launch_commit(IterState* s, const IterArrays& arr, int64_t r, int64_t* I_all, int64_t* J_all,
+                          uint8_t* row_mask, uint8_t* col_mask, double ga_norm, cudaStream_t st) {
+  commit_kernel<<<1, 256, 0, st>>>(s, arr, r, I_all, J_all, row_mask, col_mask, ga_norm);
+  return cudaGetLastError();
+}
+
+// width = min(ncols, nrows) published before the U/Rt/Y stages of the same iteration.
+__global__ void width_kernel(IterState* s) {
+  s->width = min(s->ncols, s->nrows);
+}
+cudaError_t launch_width(IterState* s, cudaStream_t st) {
+  width_kernel<<<1, 1, 0, st>>>(s);
+  return cudaGetLastError();
+}
+
+}  // namespace itercur_b200

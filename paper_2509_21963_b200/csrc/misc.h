@@ -1,0 +1,71 @@
+// misc.h — small per-iteration kernels (misc.cu) and the device iteration record.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace itercur_b200 {
+
+// Device-side record of one iteration. Lives at the head of one allocation followed by
+// six arrays of `b` entries (col_idx, row_idx as int64; col_best, col_second, row_best,
+// row_second as double) so one D2H copy returns everything the host loop needs.
+struct IterState {
+  int ncols;   // accepted column pivots (col LUPP)
+  int nrows;   // accepted row pivots (row LUPP)
+  int width;   // min(ncols, nrows)
+  int pad;
+  double ysq;  // ||Y||_F^2 after the downdate
+  double rho;  // ||Y||_F / ||GA||_F
+  double pad2[4];
+};
+static_assert(sizeof(IterState) == 64, "IterState header is 64 bytes");
+
+struct IterArrays {
+  int64_t* col_idx;
+  int64_t* row_idx;
+  double* col_best;
+  double* col_second;
+  double* row_best;
+  double* row_second;
+};
+inline IterArrays iter_arrays(void* base, int b) {
+  char* p = static_cast<char*>(base) + sizeof(IterState);
+  IterArrays a;
+  a.col_idx = reinterpret_cast<int64_t*>(p);
+  a.row_idx = a.col_idx + b;
+  a.col_best = reinterpret_cast<double*>(a.row_idx + b);
+  a.col_second = a.col_best + b;
+  a.row_best = a.col_second + b;
+  a.row_second = a.row_best + b;
+  return a;
+}
+inline size_t iter_state_bytes(int b) { return sizeof(IterState) + 6 * sizeof(double) * static_cast<size_t>(b); }
+
+cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int rows, double* Wc, int64_t ldwc,
+                                  cudaStream_t st);
+// out(k, q) = src[k * row_stride + idx[q] * col_stride], k < K, q < min(*d_w, w_max); zero beyond
+cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
+                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st);
+// out(k, q) = src[idx[k] + q * ld] for k < K, q < w (row-indexed gather)
+cudaError_t launch_gather2(const double* src, int64_t ld, const int64_t* d_idx, int64_t K, int w, double* out,
+                           int64_t ldo, cudaStream_t st);
+// G(i, j) = normal_at(seed, stream_tag, i, j), rows x cols column-major (rng.cpp:61-67)
+cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* out,
+                                   cudaStream_t st);
+// LU (no pivoting; rows already in LUPP order) of D = Lk(rows, 0:w) into lu (ld ldd)
+cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
+                            double* lu, int64_t ldd, cudaStream_t st);
+// out(j, :) = X(j, :) * D^{-T} (each row solves D x = u) via the LU factors (in place allowed)
+cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
+                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st);
+cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partials, int max_parts,
+                         double* d_out, cudaStream_t st);
+cudaError_t launch_count_nonfinite(const double* x, int64_t rows, int64_t cols, int64_t ld,
+                                   unsigned long long* d_count, cudaStream_t st);
+cudaError_t launch_commit(IterState* s, const IterArrays& arr, int64_t r, int64_t* I_all, int64_t* J_all,
+                          uint8_t* row_mask, uint8_t* col_mask, double ga_norm, cudaStream_t st);
+cudaError_t launch_width(IterState* s, cudaStream_t st);
+
+}  // namespace itercur_b200

@@ -1,0 +1,463 @@
+// sketch.cu — the O(mn) stage: Y = S * A applied once over the full matrix
+// (proj/src/sketch.cpp:10-24 make_sketch -> proj/src/matrix.cpp:285-289 G*A), with the
+// reference's separate ||A||_F zero check (proj/src/driver.cpp:52) fused into the same pass.
+//
+// Layout: A is column-major m x n (ld lda). The contraction is run as
+//     Y^T (n x Np) = A^T (n x m) * S^T (m x Np)
+// so the MMA "M" dimension is the columns of A (K = rows of A is contiguous in memory)
+// and "N" is the sketch rows padded to a multiple of 8. Tiles of A (16 rows x BM
+// columns per TMA box, 128-B swizzle) and of S are staged into shared memory by a
+// producer warp with cp.async.bulk.tensor (TMA) through a STAGES-deep mbarrier ring;
+// 8 consumer warps run FP64 mma.sync m16n8k8 (DMMA) with K permuted so every fragment
+// is one conflict-free 16-byte shared load. ||A||^2 is accumulated from the A fragments
+// (each element is loaded exactly once per CTA). Split-K partials are reduced in a fixed
+// order by a second kernel, so results are deterministic run to run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace itercur_b200 {
+
+// ------------------------------------------------------------------ operator generation
+// One thread per (h, k) for the Gaussian sketch; one thread per column k of Omega for
+// the sparse-sign sketch (partial Fisher-Yates over [0,c), one Philox
+// block per slot, sign = low bit of word 1).
+__global__ void gen_gaussian_kernel(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed) {
+  const int64_t total = rows_pad * ldg;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = e / ldg, k = e - h * ldg;
+    S[e] = (h < c && k < m) ? normal_at_dev(seed, kStreamSketch, h, k) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void sparse_sign_slots(uint64_t seed, int64_t i, int64_t c, int zeta_eff, int32_t* rows,
+                                                  int8_t* signs) {
+  // partial Fisher-Yates over [0, c): only the <= 2*zeta touched positions are tracked
+  int32_t pos[32], val[32];
+  int nover = 0;
+  auto get = [&](int32_t p) {
+    for (int q = 0; q < nover; ++q)
+      if (pos[q] == p) return val[q];
+    return p;
+  };
+  auto set = [&](int32_t p, int32_t v) {
+    for (int q = 0; q < nover; ++q)
+      if (pos[q] == p) { val[q] = v; return; }
+    pos[nover] = p;
+    val[nover] = v;
+    ++nover;
+  };
+  for (int t = 0; t < zeta_eff; ++t) {
+    const U4 r = philox4x32_10(counter_for(kStreamSparseSign, i, t), static_cast<uint32_t>(seed),
+                               static_cast<uint32_t>(seed >> 32));
+    const uint64_t span = static_cast<uint64_t>(c - t);
+    const int32_t jt = t + static_cast<int32_t>((static_cast<uint64_t>(r.x) * span) >> 32);
+    const int32_t vt = get(t), vj = get(jt);
+    set(t, vj);
+    set(jt, vt);
+    rows[t] = vj;
+    signs[t] = (r.y & 1u) ? -1 : 1;
+  }
+}
+
+__global__ void gen_sparse_sign_kernel(double* S, int64_t ldg, int64_t c, int64_t m, uint64_t seed, int zeta_eff) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    int32_t rows[16];
+    int8_t signs[16];
+    sparse_sign_slots(seed, k, c, zeta_eff, rows, signs);
+    for (int t = 0; t < zeta_eff; ++t) S[rows[t] * ldg + k] = signs[t] > 0 ? 1.0 : -1.0;
+  }
+}
+
+cudaError_t launch_gen_sketch_operator(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed,
+                                       int kind, int zeta, cudaStream_t st) {
+  if (kind == kSketchGaussian) {
+    const int64_t total = rows_pad * ldg;
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 16));
+    gen_gaussian_kernel<<<blocks, 256, 0, st>>>(S, rows_pad, ldg, c, m, seed);
+  } else {
+    cudaError_t e = cudaMemsetAsync(S, 0, sizeof(double) * rows_pad * ldg, st);
+    if (e != cudaSuccess) return e;
+    const int ze = static_cast<int>(std::min<int64_t>(zeta, c));
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 148 * 16));
+    gen_sparse_sign_kernel<<<blocks, 256, 0, st>>>(S, ldg, c, m, seed, ze);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ DMMA sketch kernel
+constexpr int kWarps = 8;        // consumer warps
+constexpr int kThreads = (kWarps + 1) * 32;
+
+template <int NT, int MT, int KS>
+struct SketchCfg {
+  static constexpr int BM = kWarps * MT * 16;  // columns of A per CTA
+  static constexpr int N = NT * 8;             // sketch rows handled per CTA
+  static constexpr int SUB = KS / 16;          // 16-row TMA boxes per stage
+  static constexpr int A_SUB_BYTES = BM * 128;
+  static constexpr int G_SUB_BYTES = N * 128;
+  static constexpr int STAGE_BYTES = SUB * (A_SUB_BYTES + G_SUB_BYTES);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES >= 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int NT, int MT, int KS>
+__device__ __forceinline__ void compute_stage(const char* sA, const char* sG, double (&acc)[MT][NT][4], double& asq,
+                                              int warp, int lane) {
+  using Cfg = SketchCfg<NT, MT, KS>;
+  const uint32_t g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int sub = 0; sub < Cfg::SUB; ++sub) {
+    const char* a_sub = sA + sub * Cfg::A_SUB_BYTES;
+    const char* g_sub = sG + sub * Cfg::G_SUB_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 8) {
+      double2 af[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint32_t row0 = (warp * MT + mt) * 16 + g;
+        af[mt][0] = *reinterpret_cast<const double2*>(a_sub + sw128_offset(row0, kk + 2 * t));
+        af[mt][1] = *reinterpret_cast<const double2*>(a_sub + sw128_offset(row0 + 8, kk + 2 * t));
+        asq = fma(af[mt][0].x, af[mt][0].x, asq);
+        asq = fma(af[mt][0].y, af[mt][0].y, asq);
+        asq = fma(af[mt][1].x, af[mt][1].x, asq);
+        asq = fma(af[mt][1].y, af[mt][1].y, asq);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 bf = *reinterpret_cast<const double2*>(g_sub + sw128_offset(nt * 8 + g, kk + 2 * t));
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          dmma_16x8x8(acc[mt][nt], af[mt][0].x, af[mt][1].x, af[mt][0].y, af[mt][1].y, bf.x, bf.y);
+      }
+    }
+  }
+}
+
+// grid: x = column tiles (BM), y = K splits, z = N chunks (each NT*8 sketch rows)
+template <int NT, int MT, int KS, bool TMA>
+__global__ void __launch_bounds__(kThreads, 1)
+    sketch_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmG,
+                       const double* __restrict__ A, int64_t lda, const double* __restrict__ S, int64_t ldg,
+                       int64_t m, int64_t n, int64_t Np, int64_t k_per_split, double* __restrict__ Yout,
+                       int64_t split_stride, double* __restrict__ asq_part) {
+  using Cfg = SketchCfg<NT, MT, KS>;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  __shared__ double red[kWarps + 1];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * Cfg::BM;
+  const int64_t k_begin = static_cast<int64_t>(blockIdx.y) * k_per_split;
+  const int64_t k_end = min(m, k_begin + k_per_split);
+  const int64_t n_off = static_cast<int64_t>(blockIdx.z) * Cfg::N;
+  const int nk = static_cast<int>(k_end > k_begin ? ceil_div(k_end - k_begin, KS) : 0);
+
+  auto stageA = [&](int s, int sub) { return smem + s * Cfg::STAGE_BYTES + sub * Cfg::A_SUB_BYTES; };
+  auto stageG = [&](int s, int sub) {
+    return smem + s * Cfg::STAGE_BYTES + Cfg::SUB * Cfg::A_SUB_BYTES + sub * Cfg::G_SUB_BYTES;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TMA ? kWarps : kThreads);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mt][nt][v] = 0.0;
+  double asq = 0.0;
+
+  if constexpr (TMA) {
+    if (warp == kWarps) {
+      // ---------------- producer warp: one elected lane drives the TMA ring ----------
+      if (lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmG);
+        for (int it = 0; it < nk; ++it) {
+          const int s = it % Cfg::STAGES;
+          const uint32_t phase = (it / Cfg::STAGES) & 1u;
+          mbar_wait(&empty[s], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          const int32_t kc = static_cast<int32_t>(k_begin + static_cast<int64_t>(it) * KS);
+#pragma unroll
+          for (int sub = 0; sub < Cfg::SUB; ++sub) {
+            tma_load_2d(stageA(s, sub), &tmA, &full[s], kc + sub * 16, static_cast<int32_t>(j0));
+            tma_load_2d(stageG(s, sub), &tmG, &full[s], kc + sub * 16, static_cast<int32_t>(n_off));
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+      // ---------------- consumer warps ------------------------------------------------
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % Cfg::STAGES;
+        const uint32_t phase = (it / Cfg::STAGES) & 1u;
+        mbar_wait(&full[s], phase);
+        compute_stage<NT, MT, KS>(stageA(s, 0), stageG(s, 0), acc, asq, warp, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+  } else {
+    // ------------- fallback (A not TMA-compatible, e.g. odd lda): all threads stage ---
+    for (int it = 0; it < nk; ++it) {
+      const int64_t kc = k_begin + static_cast<int64_t>(it) * KS;
+      char* sa = stageA(0, 0);
+      char* sg = stageG(0, 0);
+      for (int e = threadIdx.x; e < Cfg::BM * KS; e += kThreads) {
+        const int jl = e / KS, kl = e % KS;
+        const int64_t k = kc + kl, j = j0 + jl;
+        const double v = (k < m && j < n) ? A[k + j * lda] : 0.0;
+        *reinterpret_cast<double*>(sa + (kl / 16) * Cfg::A_SUB_BYTES + sw128_offset(jl, kl % 16)) = v;
+      }
+      for (int e = threadIdx.x; e < Cfg::N * KS; e += kThreads) {
+        const int hl = e / KS, kl = e % KS;
+        const int64_t k = kc + kl, h = n_off + hl;
+        const double v = (k < m && h < Np) ? S[h * ldg + k] : 0.0;
+        *reinterpret_cast<double*>(sg + (kl / 16) * Cfg::G_SUB_BYTES + sw128_offset(hl, kl % 16)) = v;
+      }
+      __syncthreads();
+      if (warp < kWarps) compute_stage<NT, MT, KS>(sa, sg, acc, asq, warp, lane);
+      __syncthreads();
+    }
+  }
+
+  // ---------------- epilogue: Y^T tile rows j, sketch rows h (16-byte stores) ----------
+  if (warp < kWarps) {
+    const int g = lane >> 2, t = lane & 3;
+    double* out = Yout + static_cast<int64_t>(blockIdx.y) * split_stride;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int64_t j = j0 + (warp * MT + mt) * 16 + g + 8 * half;
+        if (j < n) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int64_t h = n_off + nt * 8 + 2 * t;
+            if (h < Np)
+              *reinterpret_cast<double2*>(out + j * Np + h) =
+                  make_double2(acc[mt][nt][2 * half], acc[mt][nt][2 * half + 1]);
+          }
+        }
+      }
+    }
+  }
+  // ||A||^2 partial: only the z == 0 slice owns it (every slice re-reads the same A).
+  double v = warp < kWarps ? warp_sum(asq) : 0.0;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int w = 0; w < kWarps; ++w) tsum += red[w];
+    if (blockIdx.z == 0) asq_part[blockIdx.y * gridDim.x + blockIdx.x] = tsum;
+  }
+}
+
+// Fixed-order split reduction + scale + ||Y||^2 block partials.
+__global__ void sketch_reduce_kernel(const double* __restrict__ part, int splits, int64_t split_stride,
+                                     double scale, double* __restrict__ Y, int64_t total, double* __restrict__ ysq_part) {
+  __shared__ double red[8];
+  double sq = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < splits; ++p) s += part[p * split_stride + e];
+    s *= scale;
+    Y[e] = s;
+    sq = fma(s, s, sq);
+  }
+  const double b = block_sum<256>(sq, red);
+  if (threadIdx.x == 0) ysq_part[blockIdx.x] = b;
+}
+
+// Sum `count` partials in index order into *out (single block; deterministic).
+__global__ void reduce_partials_kernel(const double* __restrict__ p, int count, double* __restrict__ out) {
+  __shared__ double red[8];
+  // strided accumulation per thread, then fixed tree: deterministic for fixed count
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += p[i];
+  const double b = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *out = b;
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static bool make_tmap_2d(CUtensorMap* map, const double* base, uint64_t dim0, uint64_t dim1, uint64_t ld_elems,
+                         uint32_t box0, uint32_t box1) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0 || (ld_elems * 8) % 16 != 0) return false;
+  if (dim0 >= (1ull << 32) || dim1 >= (1ull << 32)) return false;
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {ld_elems * 8};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+using SketchKernelFn = void (*)(CUtensorMap, CUtensorMap, const double*, int64_t, const double*, int64_t, int64_t,
+                                int64_t, int64_t, int64_t, double*, int64_t, double*);
+
+template <int NT>
+static SketchKernelFn pick_kernel(bool tma, int* smem_bytes, int* bm) {
+  constexpr int MT = 1, KS = 32;
+  using Cfg = SketchCfg<NT, MT, KS>;
+  *smem_bytes = Cfg::SMEM_BYTES;
+  *bm = Cfg::BM;
+  if (tma) return sketch_dmma_kernel<NT, MT, KS, true>;
+  return sketch_dmma_kernel<NT, MT, KS, false>;
+}
+
+static SketchKernelFn kernel_for_nt(int nt, bool tma, int* smem, int* bm) {
+  switch (nt) {
+    case 1: return pick_kernel<1>(tma, smem, bm);
+    case 2: return pick_kernel<2>(tma, smem, bm);
+    case 3: return pick_kernel<3>(tma, smem, bm);
+    case 4: return pick_kernel<4>(tma, smem, bm);
+    case 5: return pick_kernel<5>(tma, smem, bm);
+    case 6: return pick_kernel<6>(tma, smem, bm);
+    case 7: return pick_kernel<7>(tma, smem, bm);
+    case 8: return pick_kernel<8>(tma, smem, bm);
+    default: return pick_kernel<9>(tma, smem, bm);
+  }
+}
+
+struct SketchPlan {
+  int nt, nchunks, bm, smem, splits, col_tiles;
+  int64_t kps;
+  bool tma;
+};
+
+static SketchPlan plan_sketch(int64_t m, int64_t n, int64_t lda, const double* A, int64_t c_pad) {
+  SketchPlan p{};
+  const int ntiles_total = static_cast<int>(c_pad / 8);
+  p.nchunks = static_cast<int>(ceil_div(ntiles_total, 9));
+  p.nt = static_cast<int>(ceil_div(ntiles_total, p.nchunks));
+  p.tma = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && ((lda * 8) % 16 == 0) && get_encode_fn() != nullptr &&
+          m < (1ll << 31) && n < (1ll << 31);
+  kernel_for_nt(p.nt, p.tma, &p.smem, &p.bm);
+  p.col_tiles = static_cast<int>(ceil_div(n, p.bm));
+  // choose K splits so the grid fills whole waves of 148 SMs (1 CTA / SM)
+  const int64_t ktiles = ceil_div(m, 32);
+  int best_s = 1;
+  double best_score = -1.0;
+  for (int s = 1; s <= 64 && s <= ktiles; ++s) {
+    const int64_t ctas = static_cast<int64_t>(p.col_tiles) * s * p.nchunks;
+    const double waves = static_cast<double>(ctas) / kNumSMs;
+    const double eff = waves / std::ceil(waves);
+    const double per_cta_k = static_cast<double>(ktiles) / s;
+    // penalise tiny K per CTA (pipeline fill) and partial traffic
+    const double score = eff - (per_cta_k < 8 ? 0.2 : 0.0) - 0.004 * s;
+    if (score > best_score + 1e-9) { best_score = score; best_s = s; }
+  }
+  p.splits = best_s;
+  p.kps = ceil_div(ktiles, best_s) * 32;
+  p.splits = static_cast<int>(ceil_div(m, p.kps));
+  return p;
+}
+
+int64_t sketch_workspace_elems(int64_t m, int64_t n, int64_t c_pad) {
+  SketchPlan p = plan_sketch(m, n, m + (m & 1), reinterpret_cast<const double*>(uintptr_t(256)), c_pad);
+  // partial Y per split (only when splits > 1) + asq partials + ysq partials
+  return (p.splits > 1 ? static_cast<int64_t>(p.splits) * n * c_pad : 0) +
+         static_cast<int64_t>(p.col_tiles) * p.splits + 4096;
+}
+
+static cudaError_t launch_dmma(const SketchPlan& p, const double* A, int64_t m, int64_t n, int64_t lda,
+                               const double* S, int64_t ldg, int64_t c_pad, double* out, int64_t split_stride,
+                               double* asq_part, cudaStream_t st) {
+  int smem = 0, bm = 0;
+  SketchKernelFn fn = kernel_for_nt(p.nt, p.tma, &smem, &bm);
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  CUtensorMap tmA{}, tmG{};
+  if (p.tma) {
+    if (!make_tmap_2d(&tmA, A, m, n, lda, 16, bm)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tmG, S, ldg, c_pad, ldg, 16, p.nt * 8)) return cudaErrorInvalidValue;
+  }
+  dim3 grid(p.col_tiles, p.splits, p.nchunks);
+  fn<<<grid, kThreads, smem, st>>>(tmA, tmG, A, lda, S, ldg, m, n, c_pad, p.kps, out, split_stride, asq_part);
+  return cudaGetLastError();
+}
+
+cudaError_t run_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
+                             int64_t c_pad, double scale, double* Y, double* ws, int64_t ws_elems,
+                             const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info) {
+  SketchPlan p = plan_sketch(m, n, lda, A, c_pad);
+  const int64_t part_elems = p.splits > 1 ? static_cast<int64_t>(p.splits) * n * c_pad : 0;
+  const int64_t asq_count = static_cast<int64_t>(p.col_tiles) * p.splits;
+  if (part_elems + asq_count + 4096 > ws_elems) return cudaErrorInvalidValue;
+  double* part = ws;
+  double* asq_part = ws + part_elems;
+  double* ysq_part = asq_part + asq_count;
+  double* out = p.splits > 1 ? part : Y;
+  cudaError_t e = launch_dmma(p, A, m, n, lda, S, ldg, c_pad, out, n * c_pad, asq_part, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = n * c_pad;
+  const int rblocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 2048));
+  sketch_reduce_kernel<<<rblocks, 256, 0, st>>>(part_elems ? part : Y, p.splits > 1 ? p.splits : 1, n * c_pad,
+                                                scale, Y, total, ysq_part);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(ysq_part, rblocks, stats.d_ysq);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(asq_part, static_cast<int>(asq_count), stats.d_asq);
+  if (info) {
+    info->splits = p.splits;
+    info->ctas = p.col_tiles * p.splits * p.nchunks;
+    info->nt = p.nt;
+    info->tma = p.tma;
+    info->dominant_launches = 1;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t run_sketch_dmma_only(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
+                                 int64_t c_pad, double* Y, double* ws, int64_t ws_elems, cudaStream_t st,
+                                 SketchLaunchInfo* info) {
+  SketchPlan p = plan_sketch(m, n, lda, A, c_pad);
+  const int64_t part_elems = p.splits > 1 ? static_cast<int64_t>(p.splits) * n * c_pad : 0;
+  const int64_t asq_count = static_cast<int64_t>(p.col_tiles) * p.splits;
+  if (part_elems + asq_count + 4096 > ws_elems) return cudaErrorInvalidValue;
+  double* out = p.splits > 1 ? ws : Y;
+  if (info) {
+    info->splits = p.splits;
+    info->ctas = p.col_tiles * p.splits * p.nchunks;
+    info->nt = p.nt;
+    info->tma = p.tma;
+    info->dominant_launches = 1;
+  }
+  return launch_dmma(p, A, m, n, lda, S, ldg, c_pad, out, n * c_pad, ws + part_elems, st);
+}
+
+}  // namespace itercur_b200

@@ -1,0 +1,205 @@
+"""GPU parity of the full IterativeCUR path (public API -> C-ABI -> sm_100a kernels) against
+the CPU oracle, plus the reference's own driver / smoke tests restated through the engine."""
+import math
+
+import numpy as np
+import pytest
+
+from parity_util import compare_runs
+
+pytestmark = pytest.mark.gpu
+
+
+def exp_decay(n, ratio, seed_rng):
+    q1, _ = np.linalg.qr(seed_rng.standard_normal((n, n)))
+    q2, _ = np.linalg.qr(seed_rng.standard_normal((n, n)))
+    return (q1 * ratio ** np.arange(n)) @ q2.T
+
+
+def low_rank_plus_noise(oracle, m, n, r, rel_noise, seed):
+    a = oracle.random_gaussian(m, r, seed) @ oracle.random_gaussian(n, r, seed + 1).T
+    noise = oracle.random_gaussian(m, n, seed + 2)
+    return a + (rel_noise * np.linalg.norm(a) / np.linalg.norm(noise)) * noise
+
+
+@pytest.mark.parametrize("case", ["expdecay600", "lowrank_noise", "rbf1500", "sparse_sign", "odd_shape"])
+def test_engine_matches_oracle(engine, oracle, case):
+    rng = np.random.default_rng(11)
+    kw = dict(epsilon=1e-6, b=10, seed=0)
+    if case == "expdecay600":
+        a = exp_decay(600, 10 ** (-1 / 20), rng)
+    elif case == "lowrank_noise":
+        a = low_rank_plus_noise(oracle, 500, 400, 60, 1e-9, 5)
+        kw.update(epsilon=1e-7, b=16, seed=3)
+    elif case == "rbf1500":
+        x, y = rng.random((1500, 3)), rng.random((1200, 3))
+        d2 = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+        a = np.exp(-d2 / (2 * 0.5 ** 2))
+        kw.update(epsilon=1e-8, b=32, seed=1)
+    elif case == "sparse_sign":
+        u, _ = np.linalg.qr(rng.standard_normal((800, 400)))
+        v, _ = np.linalg.qr(rng.standard_normal((400, 400)))
+        a = (u * (np.arange(1, 401) ** -2.0)) @ v.T
+        kw.update(epsilon=1e-4, b=20, seed=2, sketch="sparse_sign")
+    else:
+        a = low_rank_plus_noise(oracle, 333, 217, 25, 1e-11, 9)
+        kw.update(epsilon=1e-9, b=7, seed=4)
+    f, t = engine.iterative_cur(a, **kw)
+    o = oracle.iterative_cur(a, **kw)
+    v = compare_runs(o, f, t)
+    assert v["status_equal"], (o.status, t.status)
+    assert v["identical"], v
+    err = engine.true_relative_error(a, f)
+    err_o = oracle.true_relative_error(a, o.row_indices, o.col_indices)
+    assert abs(err - err_o) <= 1e-8, (err, err_o)
+    if v["full_identical"]:
+        assert len(t.rhos) == len(o.rhos)
+        assert np.allclose(t.rhos, o.rhos, rtol=1e-6, atol=1e-14)
+    # the device-evaluated error agrees with the oracle's for the engine's own indices
+    err_e_o = oracle.true_relative_error(a, f.row_indices, f.col_indices)
+    assert abs(err - err_e_o) <= 1e-10 + 1e-6 * err_e_o
+
+
+def test_config1_full_size_matches_oracle(engine, oracle):
+    """BASELINE config 1 at full size: 2000 x 2000, sigma_i = 10^(-(i-1)/20), b = 10, tol 1e-6."""
+    rng = np.random.default_rng(1)
+    a = exp_decay(2000, 10 ** (-1 / 20), rng)
+    kw = dict(epsilon=1e-6, b=10, seed=0)
+    f, t = engine.iterative_cur(a, **kw)
+    o = oracle.iterative_cur(a, **kw)
+    v = compare_runs(o, f, t)
+    assert v["status_equal"] and v["identical"], v
+    err = engine.true_relative_error(a, f)
+    err_o = oracle.true_relative_error(a, o.row_indices, o.col_indices)
+    assert abs(err - err_o) <= 1e-8
+
+
+# ------------------------- proj/tests/test_driver.cpp restated through the engine --------
+def test_rank1_converges_in_one_iteration(engine, oracle):
+    a = oracle.random_gaussian(100, 1, 5) @ oracle.random_gaussian(80, 1, 6).T
+    f, t = engine.iterative_cur(a, epsilon=1e-8, b=5, seed=3)
+    assert t.status == "Converged" and len(t.iterations) == 1 and f.rank <= 5
+    assert engine.true_relative_error(a, f) <= 1e-10
+
+
+def test_exact_rank20_two_blocks_of_10(engine, oracle):
+    a = oracle.random_gaussian(300, 20, 7) @ oracle.random_gaussian(250, 20, 8).T
+    f, t = engine.iterative_cur(a, epsilon=1e-6, b=10, seed=11)
+    assert t.status == "Converged" and f.rank == 20 and len(t.iterations) == 2
+    assert engine.true_relative_error(a, f) <= 1e-10
+
+
+def test_risk_adjust_block_too_small(engine, oracle):
+    with pytest.raises(ValueError, match="block too small"):
+        engine.iterative_cur(oracle.random_dense(40, 40, 23), epsilon=1e-4, b=2, alpha=0.1, risk_adjust=True, seed=1)
+
+
+def test_epsilon_at_or_above_one(engine, oracle):
+    f, t = engine.iterative_cur(oracle.random_dense(10, 10, 29), epsilon=1.0, b=2, seed=0)
+    assert t.status == "Converged" and f.rank == 0 and t.final_rho == 1.0 and t.note
+    assert engine.true_relative_error(oracle.random_dense(10, 10, 29), f) == 1.0
+
+
+def test_zero_matrix_rejected(engine):
+    with pytest.raises(ValueError):
+        engine.iterative_cur(np.zeros((4, 4)), epsilon=1e-3, b=2)  # test_smoke.py:81-84
+    with pytest.raises(ValueError, match="nonzero"):
+        engine.iterative_cur(np.zeros((5, 5)))
+
+
+def test_validation_messages(engine, oracle):
+    a = oracle.random_dense(4, 6, 1)
+    with pytest.raises(ValueError, match="block exceeds row count"):
+        engine.iterative_cur(a, b=5)
+    with pytest.raises(ValueError, match="block size"):
+        engine.iterative_cur(a, b=0)
+    with pytest.raises(ValueError, match="epsilon"):
+        engine.iterative_cur(a, epsilon=-1.0, b=2)
+    with pytest.raises(ValueError, match="non-finite"):
+        bad = a.copy()
+        bad[1, 1] = np.nan
+        engine.iterative_cur(bad, b=2)
+    with pytest.raises(RuntimeError, match="not implemented"):
+        engine.iterative_cur(oracle.random_dense(20, 20, 3), b=2, col_method="osinsky")
+    with pytest.raises(ValueError, match="unknown selection method"):
+        engine.iterative_cur(a, b=2, col_method="bogus")
+
+
+def test_fixed_rank_stops_at_max_rank(engine, oracle):
+    f, t = engine.iterative_cur(oracle.random_dense(50, 45, 31), epsilon=0.0, b=7, max_rank=23, seed=2)
+    assert t.status == "MaxRank" and f.rank == 23
+
+
+def test_rank_grows_by_recorded_blocks(engine, oracle):
+    a = low_rank_plus_noise(oracle, 60, 50, 12, 1e-4, 37)
+    f, t = engine.iterative_cur(a, epsilon=1e-3, b=5, seed=4)
+    assert sum(r.cols_added for r in t.iterations) == f.rank == len(f.row_indices)
+    assert all(r.cols_added == r.rows_added >= 1 for r in t.iterations)
+
+
+def test_iteration_budget(engine, oracle):
+    for seed in range(3):
+        a = low_rank_plus_noise(oracle, 40, 30, 6, 1e-2, 600 + seed)
+        _, t = engine.iterative_cur(a, epsilon=1e-8, b=4, seed=seed)
+        assert len(t.iterations) <= (30 + 3) // 4 + 1
+
+
+def test_exact_interpolation_2x2(engine):
+    a = np.array([[1.0, 0.0], [0.0, 0.0]])
+    f, t = engine.iterative_cur(a, epsilon=0.0, b=1, max_rank=2, seed=3)
+    assert t.status == "Converged" and t.final_rho == 0.0 and f.rank == 1
+    assert engine.true_relative_error(a, f) <= 1e-14
+
+
+def test_past_numerical_rank(engine, oracle):
+    a = oracle.random_gaussian(30, 3, 41) @ oracle.random_gaussian(25, 3, 42).T
+    f, t = engine.iterative_cur(a, epsilon=0.0, b=3, max_rank=10, seed=5)
+    assert 3 <= f.rank <= 10
+    assert engine.true_relative_error(a, f) <= 1e-10
+
+
+def test_factors_reconstruct_the_matrix(engine, oracle):  # test_smoke.py:46-52
+    a = oracle.random_gaussian(40, 5, 1) @ oracle.random_gaussian(30, 5, 2).T
+    f, _ = engine.iterative_cur(a, epsilon=1e-8, b=5, seed=2)
+    approx = f.c_matrix() @ f.core_matrix() @ f.r_matrix()
+    assert np.linalg.norm(a - approx) / np.linalg.norm(a) <= 1e-9
+    assert np.array_equal(f.c_matrix(), a[:, f.col_indices])
+    assert np.array_equal(f.r_matrix(), a[f.row_indices, :])
+    core_o = oracle.core_matrix(a, f.row_indices, f.col_indices)
+    assert np.allclose(f.core_matrix(), core_o, rtol=1e-8, atol=1e-10 * np.abs(core_o).max())
+
+
+def test_core_matrix_multi_block(engine, oracle):
+    a = low_rank_plus_noise(oracle, 200, 150, 30, 1e-6, 71)
+    f, t = engine.iterative_cur(a, epsilon=1e-9, b=8, seed=1)
+    assert len(t.iterations) >= 3
+    core = f.core_matrix()
+    X = a[np.ix_(f.row_indices, f.col_indices)]
+    assert np.linalg.norm(core @ X - np.eye(f.rank)) <= 1e-8 * np.linalg.cond(X)
+
+
+def test_sketched_estimate_tracks_truth(engine, oracle):  # test_driver.cpp:307-320 (20 draws)
+    in_band = 0
+    for seed in range(20):
+        a = low_rank_plus_noise(oracle, 150, 150, 10, 1e-5, 1000 + seed * 3)
+        f, t = engine.iterative_cur(a, epsilon=1e-4, b=50, seed=seed)
+        truth = engine.true_relative_error(a, f)
+        if 0.5 <= t.final_rho / truth <= 2.0:
+            in_band += 1
+    assert in_band >= 18
+
+
+def test_device_entry_with_torch_tensor(engine, oracle):
+    import torch
+
+    a = oracle.random_gaussian(300, 20, 7) @ oracle.random_gaussian(250, 20, 8).T
+    t_a = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()  # column-major view
+    f, t = engine.iterative_cur(engine.MatrixHandle.device(t_a), epsilon=1e-6, b=10, seed=11)
+    f2, t2 = engine.iterative_cur(a, epsilon=1e-6, b=10, seed=11)
+    assert f.row_indices == f2.row_indices and f.col_indices == f2.col_indices
+    assert t.rhos == t2.rhos  # deterministic run to run
+
+
+def test_closed_forms(engine):  # test_smoke.py:65-69
+    assert engine.adjusted_threshold(1.0, 0.0, 1e-10, 100) == pytest.approx(1 / 4.98, rel=5e-4)
+    assert engine.gratton_tail(4, math.sqrt(2.0)) == pytest.approx(math.exp(-0.25))

@@ -1,0 +1,127 @@
+"""GPU parity of the individual stages through the C-ABI against the CPU oracle."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _stages():
+    from paper_2509_21963_b200 import stages
+
+    return stages
+
+
+def _ulp_diff(a, b):
+    ai = np.asarray(a, dtype=np.float64).view(np.int64)
+    bi = np.asarray(b, dtype=np.float64).view(np.int64)
+    return np.abs(ai - bi)
+
+
+def test_device_normals_vs_reference_stream(engine):
+    """Philox + to_unit are bit-exact; CUDA log/cos vs glibc differ by <= 2 ulp on a few entries (F4)."""
+    S = _stages()
+    with open(os.path.join(GOLD, "rng_kat.json")) as f:
+        g = json.load(f)
+    block = np.array([[float.fromhex(h) for h in row] for row in g["sketch_block_seed0_11x512"]])
+    dev = S.gaussian_matrix(11, 512, 0, 1).cpu().numpy()
+    d = _ulp_diff(dev, block)
+    assert d.max() <= 4, d.max()
+    assert (d == 0).mean() >= 0.98, (d != 0).sum()
+    for seed, stream, i, j, hx in g["normal_at"][:200]:
+        if i > 100000 or j > 250000:
+            continue
+        got = S.gaussian_matrix(i + 1, j + 1, int(seed), stream)[i, j].item() if (i + 1) * (j + 1) < 5e6 else None
+        if got is not None:
+            assert _ulp_diff(got, float.fromhex(hx)) <= 4
+
+
+def test_sketch_of_identity_is_the_operator(engine, oracle):
+    S = _stages()
+    m = 37
+    eye = S.colmajor(np.eye(m))
+    # Gaussian: Y = G exactly (sums of one nonzero term)
+    y, _, _ = S.sketch(eye, 5, 9)
+    g = oracle.gaussian_matrix(5, m, 9, 1)
+    assert np.all(_ulp_diff(y.cpu().numpy(), g) <= 4)
+    # sparse-sign: integer-only Philox path -> bit-exact positions and signs
+    for b, seed in ((20, 3), (8, 0)):
+        c = oracle.sketch_rows_for_block(b)
+        y, _, _ = S.sketch(S.colmajor(np.eye(c + 40)), b, seed, kind="sparse_sign")
+        y_or, _, _ = oracle.sketch(np.eye(c + 40), b, seed, kind="sparse_sign")
+        assert np.array_equal(y.cpu().numpy(), y_or)
+
+
+@pytest.mark.parametrize("m,n,b,kind", [(300, 200, 10, "gaussian"), (257, 131, 7, "gaussian"),
+                                        (2000, 600, 32, "gaussian"), (1000, 700, 64, "gaussian"),
+                                        (513, 300, 20, "sparse_sign"), (800, 900, 50, "sparse_sign"),
+                                        (64, 1000, 3, "gaussian"), (5000, 40, 10, "gaussian")])
+def test_sketch_matches_oracle(engine, oracle, m, n, b, kind):
+    S = _stages()
+    a = oracle.random_gaussian(m, n, 1234 + m)
+    y, ga, an = S.sketch(S.colmajor(a), b, 5, kind=kind)
+    y_or, ga_or, an_or = oracle.sketch(a, b, 5, kind=kind)
+    y = y.cpu().numpy()
+    rel = np.linalg.norm(y - y_or) / np.linalg.norm(y_or)
+    assert rel <= 1e-13, rel
+    assert abs(ga - ga_or) <= 1e-12 * ga_or and abs(an - an_or) <= 1e-12 * an_or
+
+
+def test_sketch_non_tma_path_odd_lda(engine, oracle):
+    """lda odd -> the A tile cannot be described to TMA; the generic staging path runs."""
+    import torch
+
+    S = _stages()
+    m, n, lda = 201, 150, 203
+    a = oracle.random_dense(m, n, 77)
+    buf = torch.zeros(n, lda, dtype=torch.float64, device="cuda")
+    buf[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    dev = buf.t()[:m]  # (m, n) view with strides (1, lda)
+    assert dev.stride() == (1, lda)
+    y, _, _ = S.sketch(dev, 12, 3)
+    y_or, _, _ = oracle.sketch(a, 12, 3)
+    assert np.linalg.norm(y.cpu().numpy() - y_or) <= 1e-13 * np.linalg.norm(y_or)
+
+
+@pytest.mark.parametrize("rows,cols,b,is_columns", [(11, 2000, 10, True), (22, 777, 20, True),
+                                                    (5000, 20, 20, False), (50, 5, 5, False),
+                                                    (64, 40000, 50, True)])
+def test_lupp_bit_exact_vs_oracle(engine, oracle, rows, cols, b, is_columns):
+    """Same input bits -> the same pivot sequence and bit-identical pivot magnitudes."""
+    S = _stages()
+    m = oracle.random_gaussian(rows, cols, rows * 7 + cols)
+    ex = [3, 17, 19] if (cols if is_columns else rows) > 20 else []
+    if is_columns:
+        got = S.select_columns(S.colmajor(m), b, exclude=ex)
+        want = oracle.select_columns(m, b, exclude=ex)
+    else:
+        got = S.select_rows(S.colmajor(m), b, exclude=ex)
+        want = oracle.select_rows(m, b, exclude=ex)
+    assert got.indices == want.indices
+    assert got.best == want.best
+    assert got.truncated == want.truncated
+
+
+def test_lupp_reference_cases(engine, oracle):
+    """proj/tests/test_select.cpp cases on the device."""
+    S = _stages()
+    got = S.select_columns(S.colmajor(np.array([[1.0, 0, 3], [0, 2, 0]])), 1)
+    assert got.indices == [2] and got.last_pivot_magnitude == 3.0
+    m = oracle.random_gaussian(8, 2, 61) @ oracle.random_gaussian(30, 2, 62).T
+    got = S.select_columns(S.colmajor(m), 5)
+    assert got.truncated and len(got.indices) == 2
+    empty = S.select_columns(S.colmajor(np.zeros((6, 9))), 3)
+    assert empty.indices == [] and empty.truncated
+    got = S.select_rows(S.colmajor(oracle.random_dense(20, 3, 67)), 5)
+    assert len(got.indices) == 3 and got.truncated
+    with pytest.raises(ValueError):
+        S.select_columns(S.colmajor(oracle.random_dense(4, 9, 71)), 5)
+    with pytest.raises(IndexError):
+        S.select_columns(S.colmajor(oracle.random_dense(4, 9, 71)), 2, exclude=[40])
+    m = oracle.random_dense(10, 4, 17)
+    m[:4, :] = 0.0
+    got = S.select_rows(S.colmajor(m), 2, exclude=[0, 1, 2, 3])
+    assert all(i >= 4 for i in got.indices) and len(got.indices) == 2
