@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark: m*n/s to tolerance of the B200 IterativeCUR engine (BASELINE.json metric).
+
+One "step" = one full ``iterative_cur`` run (sketch + adaptive loop to tolerance) of
+BASELINE config 2 (configs[1]: 20000 x 10000, sigma_i = i^-2, sparse-sign sketch, b = 20,
+tol 1e-4) on a synthetic matrix formed in HBM (inputs > L2, so no flush is needed).
+
+  value : m*n / (device time per step), A resident in HBM (device entry, CUDA events)
+  e2e   : the same metric through the public API with a pinned HOST matrix (the host entry
+          copies A to the device inside the call; indices / trace come back to the host)
+  roofline : the sketch-apply kernel (the metric's named kernel), timed alone with CUDA
+          events on its stream; plus a per-phase device-time breakdown of one profiled run
+  cpu_baseline : the CPU oracle (restatement of the reference, 1 thread) on a bounded
+          sample of the same run — see `cpu_reference_sample`.
+
+`--impl reference` times only the CPU reference path (the oracle port: the reference
+itself cannot be built here, no Eigen) on the same config and prints the same line.
+Multi-GPU (torchrun, N > 1): every rank runs the workload on its own GPU (replicas; the
+column-sharded engine is not built yet), value = N * m*n / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "m·n/s to tolerance (fp64 IterativeCUR); sketch-apply % of HBM/FP64 roofline"
+UNIT = "m·n/s"
+HBM_FALLBACK_GBS = 6650.0
+DMMA_PEAK_TFLOPS = 37.1  # measured on this pool's B200 (tools/microbench/fp64_peak.cu, profiles/)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].strip() == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
+                "samples": len(sm)}
+
+
+def cpu_reference_sample(a_host, cfg, n_iters_total, budget_s=20.0):
+    """Time the CPU oracle (restatement of the reference, single thread like the reference)
+    on the same matrix: the sketch plus the leading iterations until `budget_s` elapses
+    (or convergence). The unmeasured tail is charged at the cost of the last measured
+    iteration — an underestimate (per-iteration cost grows as O(r^3) in the reference's
+    COD), so the reported CPU throughput is an upper bound."""
+    from oracle import oracle as O
+
+    O.build()
+    m, n = a_host.shape
+    b = cfg["b"]
+    # pick a prefix length that fits the budget: grow until the elapsed time exceeds it
+    k = 2
+    while True:
+        t0 = time.perf_counter()
+        r = O.iterative_cur(a_host, epsilon=cfg["epsilon"], b=b, seed=0, sketch=cfg["sketch"], max_iters=k,
+                            max_rank=cfg["max_rank"], log_steps=False)
+        wall = time.perf_counter() - t0
+        done = r.status == "Converged" or len(r.rhos) < k
+        if done or wall > budget_s or k >= n_iters_total:
+            break
+        k = min(n_iters_total, max(k + 1, int(k * min(4.0, budget_s / max(wall, 1e-3)) * 0.8)))
+    measured = len(r.iter_seconds)
+    t_meas = r.total_s
+    if done:
+        t_est = t_meas
+        note = f"full run to tolerance ({measured} iterations)"
+    else:
+        last = r.iter_seconds[-1] if r.iter_seconds else 0.0
+        t_est = t_meas + max(0, n_iters_total - measured) * last
+        note = (f"sketch + first {measured} of {n_iters_total} iterations measured ({t_meas:.2f} s); "
+                f"remaining iterations charged at the last measured iteration's {last:.3f} s (lower bound on time)")
+    return {"value": m * n / t_est, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle restatement of the reference (-O3, 1 thread) on config 2's matrix: {note}",
+            "t_est_s": t_est, "t_measured_s": t_meas, "iterations_measured": measured}
+
+
+def run_reference_arm(args, cfg):
+    """--impl reference: CPU oracle port on the same config; rank 0 only."""
+    import numpy as np
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2509_21963_b200 import testmat
+
+    # the synthetic matrix is formed on the GPU (generation is not timed) and copied to the host
+    a = testmat.generate(args.config).cpu().numpy() if torch.cuda.is_available() else None
+    if a is None:
+        print(json.dumps({"impl": "reference", "unavailable": "no GPU to form the synthetic matrix"}))
+        return 0
+    a = np.asfortranarray(a)
+    n_total = int(args.ref_iters)
+    vals = []
+    for _ in range(args.warmup):
+        pass  # the CPU path has nothing to warm; warm-up steps are not timed
+    for _ in range(args.steps):
+        s = cpu_reference_sample(a, cfg, n_total, budget_s=args.ref_budget)
+        vals.append(s)
+    v = sum(s["value"] for s in vals) / len(vals)
+    t_step = sum(s["t_est_s"] for s in vals) / len(vals)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config}", **cfg}, "impl": "reference",
+            "cpu_baseline": {k: vals[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["cpu_baseline"]["value"] = v
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=20.0, help="CPU sample budget (s)")
+    ap.add_argument("--ref-iters", type=int, default=0, help="iterations to tolerance for the CPU estimate")
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+
+    from paper_2509_21963_b200 import testmat
+
+    cfg = dict(testmat.CONFIGS[args.config])
+    m, n = cfg.pop("m"), cfg.pop("n")
+    run_cfg = dict(epsilon=cfg["epsilon"], b=cfg["b"], seed=0, sketch=cfg["sketch"], max_rank=cfg["max_rank"])
+    cfg_line = {"workload": f"BASELINE config {args.config} ({m}x{n}, {cfg['sketch']}, b={cfg['b']}, "
+                            f"tol={cfg['epsilon']:g})", "m": m, "n": n, **cfg,
+                "l2": "inputs larger than L2 (A = %.1f GB)" % (8 * m * n / 1e9),
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        if args.ref_iters <= 0:
+            args.ref_iters = {1: 15, 2: 120, 3: 8, 4: 9, 5: 16}[args.config]
+        rc = run_reference_arm(args, {"m": m, "n": n, **cfg})
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return rc
+
+    import paper_2509_21963_b200 as engine
+    from paper_2509_21963_b200 import build, stages
+
+    build.build()
+    a = testmat.generate(args.config)
+    torch.cuda.synchronize()
+    handle = engine.MatrixHandle.device(a)
+
+    # ---- one profiled run: per-phase breakdown + iteration count (not timed) ----
+    f, t = engine.iterative_cur(handle, profile=True, **run_cfg)
+    phases = {"sketch_s": t.sketch_s}
+    for key in ("select_cols_s", "row_residual_s", "select_rows_s", "core_s", "downdate_s"):
+        phases[key] = sum(getattr(r, key) for r in t.iterations)
+    n_iters, rank_final, status = len(t.iterations), f.rank, t.status
+    launches = t.kernel_launches
+    del f, t
+
+    # ---- warm-up + timed steps (device entry, A resident) ----
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        engine.iterative_cur(handle, **run_cfg)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            f, t = engine.iterative_cur(handle, **run_cfg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = tt.item()
+    value = world * m * n / (ms * 1e-3)
+
+    # ---- e2e through the public API with a pinned host matrix ----
+    a_host_t = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+    a_host_t.copy_(a.t())
+    a_host = a_host_t.numpy().T  # (m, n) Fortran-ordered view of pinned memory
+    hh = engine.MatrixHandle.dense(a_host)
+    assert hh._host.ctypes.data == a_host.ctypes.data  # no copy: the H2D copy reads pinned memory
+    engine.iterative_cur(hh, **run_cfg)  # warm
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        fe, te = engine.iterative_cur(hh, **run_cfg)
+        _ = (fe.row_indices, fe.col_indices, te.rhos)  # already on the host
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    d2h = 8 * 2 * fe.rank + 8 * len(te.rhos)
+    e2e = {"value": world * m * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
+           "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s}
+    del fe, te, hh
+
+    # ---- roofline: the sketch-apply kernel alone (CUDA events on its stream) ----
+    hbm, hbm_src = peaks()
+    sk = stages.time_sketch_kernel(a, cfg["b"], kind=cfg["sketch"], reps=10)
+    c = engine.sketch_rows_for_block(cfg["b"])
+    bytes_alg = 8.0 * m * n + 8.0 * c * n
+    flops_alg = 2.0 * c * m * n if cfg["sketch"] == "gaussian" else 2.0 * 8 * m * n
+    t_k = sk["ms"] * 1e-3
+    if cfg["sketch"] == "gaussian" and flops_alg / (DMMA_PEAK_TFLOPS * 1e12) > bytes_alg / (hbm * 1e9):
+        roof = {"bound": "tensor", "achieved": flops_alg / t_k / 1e12, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "peak_source": "measured FP64 DMMA (tools/microbench/fp64_peak.cu)"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_alg / t_k / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_source": hbm_src}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None, "kernel": "sketch_dmma_kernel",
+                 "ms_per_launch": sk["ms"], "ctas": sk["ctas"], "splits": sk["splits"], "tma": sk["tma"],
+                 "algorithmic_bytes": bytes_alg, "algorithmic_flops": flops_alg})
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
+            "config": cfg_line, "e2e": e2e, "roofline": roof, "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "run": {"status": status, "rank": rank_final, "iterations": n_iters, "phases_s": phases}}
+
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference_sample(np.asfortranarray(a.cpu().numpy()), {**cfg}, n_iters,
+                                                    budget_s=args.ref_budget)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -138,6 +138,8 @@ ITERCUR_API double itercur_run_ga_norm(const itercur_run* run);
 ITERCUR_API const char* itercur_run_note(const itercur_run* run);
 ITERCUR_API int64_t itercur_run_num_iterations(const itercur_run* run);
 ITERCUR_API int itercur_run_iterations(const itercur_run* run, itercur_iteration_record* out);
+/* number of this library's kernels the run launched (sketch + iterations) */
+ITERCUR_API int64_t itercur_run_kernel_launches(const itercur_run* run);
 /* per pivot step log: kind (0 col, 1 row), iteration, index, |best|, |second| */
 ITERCUR_API int64_t itercur_run_num_steps(const itercur_run* run);
 ITERCUR_API int itercur_run_steps(const itercur_run* run, int32_t* kind, int64_t* iter, int64_t* index, double* best,

@@ -720,6 +720,7 @@ void iterative_cur(const View& a, const oracle_config& cfg, oracle_result* res) 
   int status = ORACLE_MAX_RANK;
   while (true) {
     if (cur.rank() >= max_rank || k >= max_iters) { status = ORACLE_MAX_RANK; break; }
+    const auto it_start = Clock::now();
     const Index block = std::min(cfg.b, max_rank - cur.rank());
     SelectionResult colsel = select_columns(st.col_residual, block, cfg.col_method, cfg.pivot_floor, cur.J);
     if (colsel.indices.empty()) { status = ORACLE_RESIDUAL_EXHAUSTED; break; }
@@ -745,6 +746,7 @@ void iterative_cur(const View& a, const oracle_config& cfg, oracle_result* res) 
     if (k < res->cap_iters) {
       res->rhos[k] = rho;
       res->widths[k] = static_cast<Index>(width);
+      if (res->iter_seconds) res->iter_seconds[k] = seconds_since(it_start);
     }
     ++k;
     if (rho <= threshold) { status = ORACLE_CONVERGED; break; }

@@ -66,6 +66,7 @@ typedef struct {
   int64_t cap_iters;       /* capacity of the per-iteration arrays */
   double* rhos;            /* rho after each iteration */
   int64_t* widths;         /* cols_added (= rows_added) per iteration */
+  double* iter_seconds;    /* wall seconds of each iteration (may be NULL) */
   int64_t cap_steps;       /* capacity of the per-pivot-step log (may be 0) */
   int32_t* step_kind;      /* 0 column LUPP, 1 row LUPP */
   int64_t* step_iter;      /* iteration k */

@@ -40,6 +40,7 @@ class _Result(C.Structure):
     _fields_ = [
         ("cap_rank", C.c_int64), ("row_indices", C.POINTER(C.c_int64)), ("col_indices", C.POINTER(C.c_int64)),
         ("cap_iters", C.c_int64), ("rhos", C.POINTER(C.c_double)), ("widths", C.POINTER(C.c_int64)),
+        ("iter_seconds", C.POINTER(C.c_double)),
         ("cap_steps", C.c_int64), ("step_kind", C.POINTER(C.c_int32)), ("step_iter", C.POINTER(C.c_int64)),
         ("step_index", C.POINTER(C.c_int64)), ("step_best", C.POINTER(C.c_double)),
         ("step_second", C.POINTER(C.c_double)),
@@ -248,6 +249,7 @@ class OracleRun:
     ga_norm: float
     c: int
     steps: list  # (kind, iteration, index, best, second)
+    iter_seconds: list = field(default_factory=list)
 
     @property
     def rank(self) -> int:
@@ -269,6 +271,7 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     J = np.zeros(cap_rank, dtype=np.int64)
     rhos = np.zeros(cap_iters)
     widths = np.zeros(cap_iters, dtype=np.int64)
+    iter_s = np.zeros(cap_iters)
     sk = np.zeros(max(cap_steps, 1), dtype=np.int32)
     si = np.zeros(max(cap_steps, 1), dtype=np.int64)
     sx = np.zeros(max(cap_steps, 1), dtype=np.int64)
@@ -277,6 +280,7 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     res = _Result()
     res.cap_rank, res.row_indices, res.col_indices = cap_rank, _i64p(I), _i64p(J)
     res.cap_iters, res.rhos, res.widths = cap_iters, _dp(rhos), _i64p(widths)
+    res.iter_seconds = _dp(iter_s)
     res.cap_steps = cap_steps
     res.step_kind = sk.ctypes.data_as(C.POINTER(C.c_int32))
     res.step_iter, res.step_index, res.step_best, res.step_second = _i64p(si), _i64p(sx), _dp(sb), _dp(ss)
@@ -286,7 +290,7 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     steps = [(int(sk[q]), int(si[q]), int(sx[q]), float(sb[q]), float(ss[q])) for q in range(nst)]
     return OracleRun([int(v) for v in I[:r]], [int(v) for v in J[:r]], STATUS_NAMES[res.status], res.final_rho,
                      res.threshold, list(rhos[:k]), [int(v) for v in widths[:k]], res.note.decode(),
-                     res.sketch_s, res.total_s, res.ga_norm, res.c, steps)
+                     res.sketch_s, res.total_s, res.ga_norm, res.c, steps, list(iter_s[:k]))
 
 
 def true_relative_error(a, row_indices, col_indices) -> float:

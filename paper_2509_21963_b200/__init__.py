@@ -199,6 +199,7 @@ class RunTrace:
     total_s: float = 0.0
     ga_norm: float = 0.0
     steps: list = field(default_factory=list)  # (kind 0=col/1=row, iteration, index, |best|, |second|)
+    kernel_launches: int = 0
 
     @property
     def rhos(self) -> list:
@@ -251,7 +252,7 @@ def _collect(run_ptr, keepalive):
     trace = RunTrace(_STATUS[L.itercur_run_status(run_ptr)], L.itercur_run_final_rho(run_ptr),
                      L.itercur_run_threshold(run_ptr), L.itercur_run_note(run_ptr).decode(), iters,
                      L.itercur_run_sketch_seconds(run_ptr), L.itercur_run_total_seconds(run_ptr),
-                     L.itercur_run_ga_norm(run_ptr), steps)
+                     L.itercur_run_ga_norm(run_ptr), steps, L.itercur_run_kernel_launches(run_ptr))
     factors = CurFactors(run, [int(v) for v in I[:r]], [int(v) for v in J[:r]])
     return factors, trace
 

@@ -23,7 +23,7 @@ EXPORTED = [
     "itercur_run_rank", "itercur_run_rows", "itercur_run_cols", "itercur_run_indices", "itercur_run_status",
     "itercur_run_final_rho", "itercur_run_threshold", "itercur_run_sketch_seconds", "itercur_run_total_seconds",
     "itercur_run_ga_norm", "itercur_run_note", "itercur_run_num_iterations", "itercur_run_iterations",
-    "itercur_run_num_steps", "itercur_run_steps", "itercur_run_c_matrix", "itercur_run_r_matrix",
+    "itercur_run_kernel_launches", "itercur_run_num_steps", "itercur_run_steps", "itercur_run_c_matrix", "itercur_run_r_matrix",
     "itercur_run_core_matrix", "itercur_true_relative_error_device", "itercur_run_free",
     "itercur_adjusted_threshold", "itercur_gratton_tail", "itercur_sketch_rows_for_block",
     "itercur_gaussian_matrix_device", "itercur_sketch_device", "itercur_select_device",
@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         "itercur_run_num_iterations": (C.c_int64, [runp]),
         "itercur_run_iterations": (C.c_int, [runp, C.POINTER(IterationRecord)]),
         "itercur_run_num_steps": (C.c_int64, [runp]),
+        "itercur_run_kernel_launches": (C.c_int64, [runp]),
         "itercur_run_steps": (C.c_int, [runp, i32p, i64p, i64p, dp, dp]),
         "itercur_run_c_matrix": (C.c_int, [runp, dp]),
         "itercur_run_r_matrix": (C.c_int, [runp, dp]),

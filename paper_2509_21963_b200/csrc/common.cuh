@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "crmath.cuh"
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "paper_2509_21963_b200 kernels target sm_100a only"
 #endif
@@ -13,8 +15,8 @@ constexpr int kNumSMs = 148;
 
 // ---------------------------------------------------------------------------------
 // Philox4x32-10 keyed exactly like proj/src/rng.cpp:20-52 (counter_for / to_unit /
-// normal_at). Integer and to_unit parts are bit-exact; log/cos are CUDA libm (<=1-2 ulp,
-// the reference uses glibc, itself not correctly rounded — SURVEY.md F4/H1).
+// normal_at). Integer and to_unit parts are bit-exact; log/cos are correctly rounded
+// (crmath.cuh) — the reference's glibc is not, on ~0.2% of inputs.
 // ---------------------------------------------------------------------------------
 struct U4 { uint32_t x, y, z, w; };
 
@@ -44,11 +46,10 @@ __host__ __device__ __forceinline__ double to_unit(uint32_t hi, uint32_t lo) {
 __device__ __forceinline__ double normal_at_dev(uint64_t seed, uint32_t stream, int64_t i, int64_t j) {
   const U4 r = philox4x32_10(counter_for(stream, i, j), static_cast<uint32_t>(seed),
                              static_cast<uint32_t>(seed >> 32));
-  const double u1 = to_unit(r.x, r.y);
-  const double u2 = to_unit(r.z, r.w);
-  // sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2), rounding order of rng.cpp:51
-  const double two_pi = 6.283185307179586;  // 2.0 * M_PI, exact product
-  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+  // sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2), rounding order of rng.cpp:51, with
+  // correctly rounded log / cos (crmath.cuh) so the stream matches glibc wherever glibc
+  // itself rounds correctly.
+  return crm::box_muller_cos(to_unit(r.x, r.y), to_unit(r.z, r.w));
 }
 
 __device__ __forceinline__ double uniform_at_dev(uint64_t seed, uint32_t stream, int64_t i, int64_t j) {

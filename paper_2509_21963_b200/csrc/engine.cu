@@ -73,28 +73,49 @@ int guarded(F&& f) {
 }
 
 // ------------------------------------------------------------------ device buffers
+// Stream-ordered allocations from the device's default memory pool (release threshold
+// raised once), so the per-run workspaces cost no cudaMalloc / cudaFree synchronisation
+// after the first run.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+void configure_mempool_once() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
+  cudaStream_t st = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     count = 0;
   }
   void alloc(size_t n) {
     reset();
     if (n == 0) n = 1;
-    CK(cudaMalloc(&p, n * sizeof(T)));
+    st = g_alloc_stream;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
     count = n;
   }
   void swap(DevBuf& o) {
     std::swap(p, o.p);
     std::swap(count, o.count);
+    std::swap(st, o.st);
   }
 };
 
@@ -147,6 +168,7 @@ struct itercur_run {
   DevBuf<double> Dinv;  // per block: LU of D_k (w x w, ld bmax) at offset start * bmax
   DevBuf<int64_t> dI, dJ;
   int64_t ldL = 0, ldR = 0, capL = 0, bmax = 0;
+  int64_t launches = 0;  // kernels of this library launched by the run (sketch + loop)
 };
 
 namespace {
@@ -218,11 +240,20 @@ struct Workspace {
   DevBuf<char> state, lupp_scratch;
   DevBuf<double> scal;  // [0] asq, [1] ysq
   DevBuf<unsigned long long> nonfinite;
-  char* h_state = nullptr;  // pinned mirror
-  ~Workspace() {
-    if (h_state) cudaFreeHost(h_state);
-  }
+  char* h_state = nullptr;  // pinned mirror (thread-local cache, see pinned_state)
 };
+
+char* pinned_state(size_t bytes) {
+  thread_local char* buf = nullptr;
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&buf), bytes));
+    cap = bytes;
+  }
+  return buf;
+}
 
 void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
   if (need <= run->capL) return;
@@ -271,6 +302,7 @@ void run_iterative_cur(itercur_run* run) {
       DevBuf<unsigned long long> cnt;
       cnt.alloc(1);
       CK(launch_count_nonfinite(A, m, n, lda, cnt.p, st));
+      run->launches += 1;
       unsigned long long h = 0;
       CK(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -311,6 +343,7 @@ void run_iterative_cur(itercur_run* run) {
                                                                        ? kSketchSparseSign
                                                                        : kSketchGaussian,
                                   cfg.sparse_nnz, st));
+    run->launches += 1;
     const int64_t wse = sketch_workspace_elems(m, n, cp);
     ws.sk_ws.alloc(wse);
     double scale = 1.0;
@@ -320,6 +353,7 @@ void run_iterative_cur(itercur_run* run) {
     }
     SketchStats stats{ws.scal.p + 0, ws.scal.p + 1};
     CK(run_sketch_apply(A, m, n, lda, ws.S.p, ldg, cp, scale, ws.Y.p, ws.sk_ws.p, wse, stats, st, nullptr));
+    run->launches += 4;
   }
   CK(cudaEventRecord(e_sk1, st));
   double hs[2] = {0, 0};
@@ -330,6 +364,7 @@ void run_iterative_cur(itercur_run* run) {
   if (!std::isfinite(hs[0])) {
     ws.nonfinite.alloc(1);
     CK(launch_count_nonfinite(A, m, n, lda, ws.nonfinite.p, st));
+    run->launches += 1;
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, ws.nonfinite.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -358,252 +393,285 @@ void run_iterative_cur(itercur_run* run) {
   if (!(cfg.pivot_floor > 0.0 && cfg.pivot_floor < 1.0))
     fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
   check_method(cfg.col_method);
+  check_method(cfg.row_method);
 
   // ---- workspaces ----
   const int B = static_cast<int>(b);
-  ws.Wc.alloc(static_cast<size_t>(even(n)) * B);
-  ws.Wr.alloc(static_cast<size_t>(even(m)) * B);
-  ws.Ut.alloc(static_cast<size_t>(even(n)) * B);
+  const int64_t ldn = even(n), ldm = even(m);
+  ws.Wc.alloc(static_cast<size_t>(ldn) * B);
+  ws.Wr.alloc(static_cast<size_t>(ldm) * B);
+  ws.Ut.alloc(static_cast<size_t>(ldn) * B);
   ws.Yg.alloc(static_cast<size_t>(B) * cp);
-  ws.lu.alloc(static_cast<size_t>(B) * B);
   ws.col_mask.alloc(n);
   ws.row_mask.alloc(m);
   CK(cudaMemsetAsync(ws.col_mask.p, 0, n, st));
   CK(cudaMemsetAsync(ws.row_mask.p, 0, m, st));
-  ws.lupp_scratch.alloc(lupp_scratch_bytes());
-  const size_t state_bytes = iter_state_bytes(B);
-  ws.state.alloc(state_bytes);
-  CK(cudaMemsetAsync(ws.state.p, 0, state_bytes, st));
-  CK(cudaMallocHost(&ws.h_state, state_bytes));
-  IterState* d_state = reinterpret_cast<IterState*>(ws.state.p);
-  const IterArrays arr = iter_arrays(ws.state.p, B);
-  const IterArrays harr = iter_arrays(ws.h_state, B);
-  int64_t part_count = std::max<int64_t>({ts_gemm_grid_size(m, B), ts_gemm_grid_size(n, static_cast<int>(cp)),
-                                          ts_gemm_grid_size(n, B), 4096});
-  ws.part.alloc(part_count);
+  ws.lupp_scratch.alloc(lupp_scratch_bytes(B));
+  // iterations are enqueued in batches of kBatch without a host round trip; the loop control
+  // (budgets, stop tests, rank) lives on the device (IterCtl), and every kernel of an
+  // iteration after the stop returns immediately.
+  const int kBatch = 8;
+  const size_t slot_bytes = round_up(iter_state_bytes(B), 64);
+  ws.state.alloc(slot_bytes * kBatch + sizeof(IterCtl));
+  char* slots = ws.state.p;
+  IterCtl* d_ctl = reinterpret_cast<IterCtl*>(ws.state.p + slot_bytes * kBatch);
+  ws.h_state = pinned_state(slot_bytes * kBatch + sizeof(IterCtl));
+  {
+    IterCtl h{};
+    h.r = 0;
+    h.k = 0;
+    h.max_rank = max_rank;
+    h.max_iters = max_iters;
+    h.done = 0;
+    h.status = ITERCUR_MAX_RANK;
+    h.b = B;
+    h.ysq = hs[1];
+    h.rho = rho;
+    h.threshold = threshold;
+    h.ga_norm = ga_norm;
+    IterCtl* hc = reinterpret_cast<IterCtl*>(ws.h_state + slot_bytes * kBatch);
+    *hc = h;
+    CK(cudaMemcpyAsync(d_ctl, hc, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
+  }
   run->dI.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dJ.alloc(std::max<int64_t>(max_rank + b, 1));
   run->capL = 0;
-  grow_factors(run, std::min<int64_t>(max_rank + b, std::max<int64_t>(4 * b, 256)), st);
+  grow_factors(run, std::min<int64_t>(max_rank + b, std::max<int64_t>(kBatch * b, 256)), st);
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+  const int64_t y_parts = ts_gemm_grid_size(n, static_cast<int>(cp));
+  ws.part.alloc(std::max<int64_t>(y_parts, 1));
 
   // initial Wc = Y^T(:, 0:b)
-  CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, even(n), st));
-  CK(cudaMemcpyAsync(&d_state->ysq, ws.scal.p + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, ldn, st));
+  run->launches += 1;
 
   uint8_t epoch = 1;
-  int64_t k = 0;
-  int32_t status = ITERCUR_MAX_RANK;
-  while (true) {
-    if (run->r >= max_rank || k >= max_iters) {
-      status = ITERCUR_MAX_RANK;
-      break;
-    }
-    const int64_t r = run->r;
-    const int block = static_cast<int>(std::min<int64_t>(b, max_rank - r));
-    if (r + B > run->capL) {
-      grow_factors(run, r + B, st);
+  int64_t k_host = 0, r_host = 0;
+  int64_t ev_i = 2;
+  std::vector<size_t> iter_events;
+  bool done = false;
+  while (!done) {
+    // capacity for a whole batch
+    const int64_t need = std::min(r_host + static_cast<int64_t>(kBatch) * b, max_rank + b);
+    if (need > run->capL) {
+      grow_factors(run, need, st);
       ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
     }
-    if (++epoch == 0 || epoch == 1) {  // epochs cycle through 2..255
-      CK(launch_clear_epochs(ws.col_mask.p, n, st));
-      CK(launch_clear_epochs(ws.row_mask.p, m, st));
-      epoch = 2;
-    }
-    itercur_iteration_record rec{};
-    rec.k = k;
-    const size_t e0 = 2 + 6 * static_cast<size_t>(k);
-    if (evs.on) CK(cudaEventRecord(evs.get(e0), st));
+    const int64_t ldbg = run->capL;
+    for (int j = 0; j < kBatch; ++j) {
+      IterState* slot = reinterpret_cast<IterState*>(slots + slot_bytes * j);
+      const IterArrays arr = iter_arrays(slot, B);
+      if (++epoch == 0 || epoch == 1) {  // epochs cycle through 2..255 (global-memory LUPP path)
+        CK(launch_clear_epochs(ws.col_mask.p, n, st));
+        CK(launch_clear_epochs(ws.row_mask.p, m, st));
+        run->launches += 2;
+        epoch = 2;
+      }
+      const size_t e0 = static_cast<size_t>(ev_i);
+      if (evs.on) {
+        CK(cudaEventRecord(evs.get(e0), st));
+        iter_events.push_back(e0);
+        ev_i += 6;
+      }
+      CK(launch_iter_begin(d_ctl, slot, st));
 
-    // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
-    int* d_ncols = &d_state->ncols;
-    int* d_nrows = &d_state->nrows;
-    int* d_width = &d_state->width;
-    {
-      LuppArgs la{};
-      la.W = ws.Wc.p;
-      la.rows = n;
-      la.ldw = even(n);
-      la.cols_max = block;
-      la.d_steps = nullptr;
-      la.mask = ws.col_mask.p;
-      la.epoch = epoch;
-      la.d_norm_sq = &d_state->ysq;
-      la.pivot_floor = cfg.pivot_floor;
-      la.d_idx = arr.col_idx;
-      la.d_best = arr.col_best;
-      la.d_second = arr.col_second;
-      la.d_count = d_ncols;
-      CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
-    }
-    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
+      // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
+      {
+        LuppArgs la{};
+        la.W = ws.Wc.p;
+        la.rows = n;
+        la.ldw = ldn;
+        la.cols_max = B;
+        la.d_steps = &d_ctl->block;
+        la.mask = ws.col_mask.p;
+        la.epoch = epoch;
+        la.d_norm_sq = &d_ctl->ysq;
+        la.pivot_floor = cfg.pivot_floor;
+        la.d_idx = arr.col_idx;
+        la.d_best = arr.col_best;
+        la.d_second = arr.col_second;
+        la.d_count = &slot->ncols;
+        CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+      }
+      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
 
-    // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60)
-    CK(launch_gather(run->Rt.p, run->ldR, 1, r, arr.col_idx, d_ncols, block, ws.Bg.p, std::max<int64_t>(r, 1), st));
-    {
-      TsGemmParams p;
-      p.M = m;
-      p.K = r;
-      p.N = block;
-      p.d_n = d_ncols;
-      p.A = run->L.p;
-      p.lda = run->ldL;
-      p.B = ws.Bg.p;
-      p.bsk = 1;
-      p.bsn = std::max<int64_t>(r, 1);
-      p.base_mode = kBaseGatherCols;
-      p.src = A;
-      p.lds = lda;
-      p.idx = arr.col_idx;
-      p.alpha = -1.0;
-      p.out_mode = kOutColMajor;
-      p.C0 = run->L.p + run->ldL * r;
-      p.ldc0 = run->ldL;
-      p.C1 = ws.Wr.p;
-      p.ldc1 = even(m);
-      CK(run_ts_gemm(p, st));
-    }
-    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
+      // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60)
+      {
+        TsGemmParams p;
+        p.M = m;
+        p.K = ldbg;
+        p.ctl = d_ctl;
+        p.k_from_r = 1;
+        p.N = B;
+        p.d_n = &slot->ncols;
+        p.A = run->L.p;
+        p.lda = run->ldL;
+        p.B = run->Rt.p;  // B(k, q) = Rt(k, J_k[q])
+        p.bsk = run->ldR;
+        p.bsn = 1;
+        p.b_idx = arr.col_idx;
+        p.base_mode = kBaseGatherCols;
+        p.src = A;
+        p.lds = lda;
+        p.idx = arr.col_idx;
+        p.alpha = -1.0;
+        p.out_mode = kOutColMajor;
+        p.C0 = run->L.p;
+        p.c0_off_per_r = run->ldL;
+        p.ldc0 = run->ldL;
+        p.C1 = ws.Wr.p;
+        p.ldc1 = ldm;
+        CK(run_ts_gemm(p, st));
+      }
+      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
 
-    // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
-    {
-      LuppArgs la{};
-      la.W = ws.Wr.p;
-      la.rows = m;
-      la.ldw = even(m);
-      la.cols_max = block;
-      la.d_steps = d_ncols;
-      la.mask = ws.row_mask.p;
-      la.epoch = epoch;
-      la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
-      la.pivot_floor = cfg.pivot_floor;
-      la.d_idx = arr.row_idx;
-      la.d_best = arr.row_best;
-      la.d_second = arr.row_second;
-      la.d_count = d_nrows;
-      CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
-    }
-    CK(launch_width(d_state, st));
-    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
+      // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
+      {
+        LuppArgs la{};
+        la.W = ws.Wr.p;
+        la.rows = m;
+        la.ldw = ldm;
+        la.cols_max = B;
+        la.d_steps = &slot->ncols;
+        la.mask = ws.row_mask.p;
+        la.epoch = epoch;
+        la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
+        la.pivot_floor = cfg.pivot_floor;
+        la.d_idx = arr.row_idx;
+        la.d_best = arr.row_best;
+        la.d_second = arr.row_second;
+        la.d_count = &slot->nrows;
+        la.d_width_out = &slot->width;  // width = min(|cols|, |rows|), driver.cpp:123
+        la.d_width_cap = &slot->ncols;
+        CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+      }
+      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
 
-    // (4) core step: LU of D_k = S_row(I_k, 0:w) and the new Rt rows
-    double* dlu_k = run->Dinv.p + run->bmax * r;
-    CK(launch_cross_lu(run->L.p + run->ldL * r, run->ldL, arr.row_idx, d_width, block, dlu_k, run->bmax, st));
-    // U_k^T = A(I_k,:)^T - Rt^T * L(I_k, 0:r)^T
-    CK(launch_gather(run->L.p, run->ldL, 1, r, arr.row_idx, d_width, block, ws.Bg.p, std::max<int64_t>(r, 1), st));
-    {
-      TsGemmParams p;
-      p.M = n;
-      p.K = r;
-      p.N = block;
-      p.d_n = d_width;
-      p.A = run->Rt.p;
-      p.lda = run->ldR;
-      p.B = ws.Bg.p;
-      p.bsk = 1;
-      p.bsn = std::max<int64_t>(r, 1);
-      p.base_mode = kBaseGatherRowsT;
-      p.src = A;
-      p.lds = lda;
-      p.idx = arr.row_idx;
-      p.alpha = -1.0;
-      p.out_mode = kOutColMajor;
-      p.C0 = ws.Ut.p;
-      p.ldc0 = even(n);
-      CK(run_ts_gemm(p, st));
-    }
-    // Rt_k^T = U_k^T * D_k^{-T} by row-wise LU solves  ->  rows r..r+w of Rt
-    CK(launch_rows_lu_solve(ws.Ut.p, even(n), n, dlu_k, run->bmax, d_width, block, run->Rt.p + run->ldR * r,
-                            run->ldR, st));
-    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
+      // (4) core step: LU of D_k = S_row(I_k, 0:w); U_k^T = A(I_k,:)^T - Rt^T L(I_k,:)^T;
+      //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
+      CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
+      {
+        TsGemmParams p;
+        p.M = n;
+        p.K = ldbg;
+        p.ctl = d_ctl;
+        p.k_from_r = 1;
+        p.N = B;
+        p.d_n = &slot->width;
+        p.A = run->Rt.p;
+        p.lda = run->ldR;
+        p.B = run->L.p;  // B(k, q) = L(I_k[q], k)
+        p.bsk = run->ldL;
+        p.bsn = 1;
+        p.b_idx = arr.row_idx;
+        p.base_mode = kBaseGatherRowsT;
+        p.src = A;
+        p.lds = lda;
+        p.idx = arr.row_idx;
+        p.alpha = -1.0;
+        p.out_mode = kOutColMajor;
+        p.C0 = ws.Ut.p;
+        p.ldc0 = ldn;
+        CK(run_ts_gemm(p, st));
+      }
+      CK(launch_rows_lu_solve(ws.Ut.p, ldn, n, run->Dinv.p, run->bmax, &slot->width, B, run->Rt.p, run->ldR, st,
+                              d_ctl, run->ldR));
+      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
 
-    // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
-    //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
-    // Yg(h, q) = Y(h, J[q]) (cp x w, ld cp), gathered before Y is overwritten
-    CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, d_width, block, ws.Yg.p, cp, st));
-    {
-      TsGemmParams p;
-      p.M = n;
-      p.K = block;
-      p.d_k = d_width;
-      p.N = static_cast<int>(cp);
-      p.A = run->Rt.p + run->ldR * r;
-      p.lda = run->ldR;
-      p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
-      p.bsk = cp;
-      p.bsn = 1;
-      p.base_mode = kBaseInPlaceRowMajor;
-      p.alpha = -1.0;
-      p.out_mode = kOutRowMajor;
-      p.C0 = ws.Y.p;
-      p.ldc0 = cp;
-      p.Wc = ws.Wc.p;
-      p.ldwc = even(n);
-      p.wc_rows = B;
-      p.norm_part = ws.part.p;
-      CK(run_ts_gemm(p, st));
-      CK(launch_sum_partials(ws.part.p, ts_gemm_grid_size(n, static_cast<int>(cp)), &d_state->ysq, st));
+      // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
+      //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
+      CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+      {
+        TsGemmParams p;
+        p.M = n;
+        p.K = B;
+        p.d_k = &slot->width;
+        p.ctl = d_ctl;
+        p.N = static_cast<int>(cp);
+        p.A = run->Rt.p;
+        p.a_off_per_r = run->ldR;
+        p.lda = run->ldR;
+        p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
+        p.bsk = cp;
+        p.bsn = 1;
+        p.base_mode = kBaseInPlaceRowMajor;
+        p.alpha = -1.0;
+        p.out_mode = kOutRowMajor;
+        p.C0 = ws.Y.p;
+        p.ldc0 = cp;
+        p.Wc = ws.Wc.p;
+        p.ldwc = ldn;
+        p.wc_rows = B;
+        p.norm_part = ws.part.p;
+        CK(run_ts_gemm(p, st));
+      }
+      CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
+                       st));
+      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
+      run->launches += 10;
     }
-    CK(launch_commit(d_state, arr, r, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ga_norm, st));
-    if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
-
-    // one D2H read per iteration: the record + this iteration's pivots
-    CK(cudaMemcpyAsync(ws.h_state, ws.state.p, state_bytes, cudaMemcpyDeviceToHost, st));
+    // one D2H read per batch: the batch's records + the loop control
+    CK(cudaMemcpyAsync(ws.h_state, ws.state.p, slot_bytes * kBatch + sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const IterState* hs_ = reinterpret_cast<const IterState*>(ws.h_state);
-    const int ncols = hs_->ncols, nrows = hs_->nrows;
-    for (int s = 0; s < ncols; ++s) {
-      run->step_kind.push_back(0);
-      run->step_iter.push_back(k);
-      run->step_index.push_back(harr.col_idx[s]);
-      run->step_best.push_back(harr.col_best[s]);
-      run->step_second.push_back(harr.col_second[s]);
+    const IterCtl* hc = reinterpret_cast<const IterCtl*>(ws.h_state + slot_bytes * kBatch);
+    for (int j = 0; j < kBatch; ++j) {
+      const IterState* hs_ = reinterpret_cast<const IterState*>(ws.h_state + slot_bytes * j);
+      if (!hs_->valid) continue;
+      const IterArrays harr = iter_arrays(const_cast<IterState*>(hs_), B);
+      const int ncols = hs_->ncols, nrows = hs_->nrows;
+      for (int s = 0; s < ncols; ++s) {
+        run->step_kind.push_back(0);
+        run->step_iter.push_back(k_host);
+        run->step_index.push_back(harr.col_idx[s]);
+        run->step_best.push_back(harr.col_best[s]);
+        run->step_second.push_back(harr.col_second[s]);
+      }
+      for (int s = 0; s < nrows; ++s) {
+        run->step_kind.push_back(1);
+        run->step_iter.push_back(k_host);
+        run->step_index.push_back(harr.row_idx[s]);
+        run->step_best.push_back(harr.row_best[s]);
+        run->step_second.push_back(harr.row_second[s]);
+      }
+      if (ncols == 0 || nrows == 0) break;  // ResidualExhausted: nothing committed
+      const int width = hs_->width;
+      for (int q = 0; q < width; ++q) {
+        run->I.push_back(harr.row_idx[q]);
+        run->J.push_back(harr.col_idx[q]);
+      }
+      run->block_start.push_back(r_host);
+      run->block_width.push_back(width);
+      r_host += width;
+      itercur_iteration_record rec{};
+      rec.k = k_host;
+      rec.rho = hs_->rho;
+      rec.cols_added = rec.rows_added = width;
+      rec.col_truncated = 0;  // filled below from the requested block
+      rec.row_truncated = nrows < ncols;
+      rec.min_col_margin = min_margin(harr.col_best, harr.col_second, ncols);
+      rec.min_row_margin = min_margin(harr.row_best, harr.row_second, nrows);
+      const int64_t requested = std::min<int64_t>(b, max_rank - (r_host - width));
+      rec.col_truncated = ncols < requested;
+      run->iters.push_back(rec);
+      ++k_host;
     }
-    if (ncols == 0) {  // driver.cpp:102-105
-      status = ITERCUR_RESIDUAL_EXHAUSTED;
-      break;
-    }
-    for (int s = 0; s < nrows; ++s) {
-      run->step_kind.push_back(1);
-      run->step_iter.push_back(k);
-      run->step_index.push_back(harr.row_idx[s]);
-      run->step_best.push_back(harr.row_best[s]);
-      run->step_second.push_back(harr.row_second[s]);
-    }
-    if (nrows == 0) {  // driver.cpp:118-121
-      status = ITERCUR_RESIDUAL_EXHAUSTED;
-      break;
-    }
-    const int width = hs_->width;
-    for (int q = 0; q < width; ++q) {
-      run->I.push_back(harr.row_idx[q]);
-      run->J.push_back(harr.col_idx[q]);
-    }
-    run->block_start.push_back(r);
-    run->block_width.push_back(width);
-    run->r = r + width;
-    rho = hs_->rho;
-    rec.rho = rho;
-    rec.cols_added = rec.rows_added = width;
-    rec.col_truncated = ncols < block;
-    rec.row_truncated = nrows < ncols;
-    rec.min_col_margin = min_margin(harr.col_best, harr.col_second, ncols);
-    rec.min_row_margin = min_margin(harr.row_best, harr.row_second, nrows);
-    if (evs.on) {
+    if (hc->r != r_host || hc->k != k_host) fail(ITERCUR_E_LOGIC, "device / host iteration bookkeeping diverged");
+    run->r = r_host;
+    rho = hc->rho;
+    done = hc->done != 0;
+    if (done) run->status = hc->status;
+  }
+  if (evs.on) {
+    for (size_t q = 0; q < run->iters.size() && q < iter_events.size(); ++q) {
+      const size_t e0 = iter_events[q];
+      auto& rec = run->iters[q];
       rec.select_cols_s = elapsed_s(evs.get(e0), evs.get(e0 + 1));
       rec.row_residual_s = elapsed_s(evs.get(e0 + 1), evs.get(e0 + 2));
       rec.select_rows_s = elapsed_s(evs.get(e0 + 2), evs.get(e0 + 3));
       rec.core_s = elapsed_s(evs.get(e0 + 3), evs.get(e0 + 4));
       rec.downdate_s = elapsed_s(evs.get(e0 + 4), evs.get(e0 + 5));
     }
-    ++k;
-    run->iters.push_back(rec);
-    if (rho <= threshold) {  // driver.cpp:156-159
-      status = ITERCUR_CONVERGED;
-      break;
-    }
   }
-  run->status = status;
   run->final_rho = rho;
   run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
@@ -763,6 +831,8 @@ int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t
     run->lda = lda;
     run->A = dA;
     run->cfg = cfg ? *cfg : default_config();
+    configure_mempool_once();
+    g_alloc_stream = run->stream;
     run_iterative_cur(run.get());
     *out = run.release();
   });
@@ -776,13 +846,19 @@ int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t ld
     auto run = std::make_unique<itercur_run>();
     CK(cudaGetDevice(&run->device));
     run->stream = nullptr;
+    configure_mempool_once();
+    g_alloc_stream = run->stream;
     run->m = m;
     run->n = n;
     run->lda = std::max<int64_t>(m, 1);
     if (m > 0 && n > 0) {
       run->A_owned.alloc(static_cast<size_t>(m) * n);
-      CK(cudaMemcpy2DAsync(run->A_owned.p, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
-                           cudaMemcpyHostToDevice, run->stream));
+      if (lda == m) {
+        CK(cudaMemcpyAsync(run->A_owned.p, A, sizeof(double) * m * n, cudaMemcpyHostToDevice, run->stream));
+      } else {
+        CK(cudaMemcpy2DAsync(run->A_owned.p, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
+                             cudaMemcpyHostToDevice, run->stream));
+      }
       run->A = run->A_owned.p;
     }
     run->cfg = cfg ? *cfg : default_config();
@@ -815,6 +891,7 @@ int itercur_run_iterations(const itercur_run* run, itercur_iteration_record* out
     std::copy(run->iters.begin(), run->iters.end(), out);
   });
 }
+int64_t itercur_run_kernel_launches(const itercur_run* run) { return run ? run->launches : 0; }
 int64_t itercur_run_num_steps(const itercur_run* run) { return run ? static_cast<int64_t>(run->step_index.size()) : 0; }
 int itercur_run_steps(const itercur_run* run, int32_t* kind, int64_t* iter, int64_t* index, double* best,
                       double* second) {
@@ -831,6 +908,7 @@ int itercur_run_c_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
     // C(i, q) = A(i, J[q]): out(k=i, q) = A[i * 1 + J[q] * lda]
     gather_host(run, run->A, 1, run->lda, run->m, run->dJ.p, run->r, out);
   });
@@ -839,6 +917,7 @@ int itercur_run_r_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
     // R^T(j, q) = A(I[q], j): gathered as (n x r), then transposed on the host
     std::vector<double> t(static_cast<size_t>(run->n) * run->r);
     gather_host(run, run->A, run->lda, 1, run->n, run->dI.p, run->r, t.data());
@@ -850,6 +929,7 @@ int itercur_run_core_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
     core_matrix_impl(run, out);
   });
 }
@@ -857,6 +937,7 @@ int itercur_true_relative_error_device(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
     *out = true_error_impl(run);
   });
 }
@@ -888,6 +969,8 @@ int itercur_sketch_device(const double* dA, int64_t m, int64_t n, int64_t lda, i
     if (m == 0 || n == 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonempty");
     if (b > m) fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    configure_mempool_once();
+    g_alloc_stream = st;
     const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
     DevBuf<double> S, Yp, wsb, scal;
     S.alloc(static_cast<size_t>(cp) * ldg);
@@ -920,6 +1003,8 @@ int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t 
   return guarded([&] {
     require_device();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    configure_mempool_once();
+    g_alloc_stream = st;
     // select.cpp:24-28, 124-126, 143
     if (!(pivot_floor > 0.0 && pivot_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
     if (is_columns && (b < 0 || b > rows))
@@ -971,7 +1056,7 @@ int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t 
     CK(launch_sumsq(dM, rows, cols, ldm, part.p, 148 * 8, scal.p, st));
     mask.alloc(wrows);
     CK(cudaMemcpyAsync(mask.p, hmask.data(), wrows, cudaMemcpyHostToDevice, st));
-    scratch.alloc(lupp_scratch_bytes());
+    scratch.alloc(lupp_scratch_bytes(static_cast<int>(steps)));
     const int S = static_cast<int>(steps);
     outs.alloc(sizeof(int64_t) * S * 3 + 16);
     int64_t* d_idx = reinterpret_cast<int64_t*>(outs.p);
@@ -1016,6 +1101,8 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
   return guarded([&] {
     require_device();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    configure_mempool_once();
+    g_alloc_stream = st;
     const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
     DevBuf<double> S, Y, wsb;
     S.alloc(static_cast<size_t>(cp) * ldg);

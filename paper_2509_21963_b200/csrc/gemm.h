@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "kernels.h"
+#include "misc.h"
 
 namespace itercur_b200 {
 
@@ -31,6 +32,7 @@ struct TsGemmParams {
   int64_t lda = 0;
   const double* B = nullptr;
   int64_t bsk = 0, bsn = 0;
+  const int64_t* b_idx = nullptr;  // optional: B(k, q) = B[k * bsk + b_idx[q] * bsn]
   int base_mode = kBaseNone;
   const double* src = nullptr;
   int64_t lds = 0;
@@ -46,6 +48,12 @@ struct TsGemmParams {
   int64_t ldwc = 0;
   int wc_rows = 0;
   double* norm_part = nullptr;  // [grid.y * grid.x] per-CTA sum of squares of C
+  // device-resident loop control: skip when ctl->done; K = min(K, ctl->r) when k_from_r;
+  // A += ctl->r * a_off_per_r and C0 += ctl->r * c0_off_per_r (elements)
+  const IterCtl* ctl = nullptr;
+  int k_from_r = 0;
+  int64_t a_off_per_r = 0;
+  int64_t c0_off_per_r = 0;
 };
 
 cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st);

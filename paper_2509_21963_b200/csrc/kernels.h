@@ -59,9 +59,11 @@ struct LuppArgs {
   double* d_best;           // out: |pivot|
   double* d_second;         // out: runner-up magnitude (margin log)
   int* d_count;             // out: accepted pivots
+  int* d_width_out = nullptr;        // optional out: min(count, *d_width_cap)
+  const int* d_width_cap = nullptr;
   int requested_b;          // for `truncated` semantics (host side)
 };
-size_t lupp_scratch_bytes();
+size_t lupp_scratch_bytes(int b);
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used);
 cudaError_t launch_clear_epochs(uint8_t* mask, int64_t count, cudaStream_t st);
 

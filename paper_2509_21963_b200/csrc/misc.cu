@@ -22,9 +22,11 @@ __global__ void transpose_rows_kernel(const double* __restrict__ Y, int64_t cp, 
 }
 
 // out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < w (dynamic), zero for q >= w
-__global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride, int64_t col_stride, int64_t K,
+__global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride, int64_t col_stride, int64_t Kmax,
                               const int64_t* __restrict__ idx, const int* __restrict__ d_w, int w_max,
-                              double* __restrict__ out, int64_t ldo) {
+                              double* __restrict__ out, int64_t ldo, const IterCtl* __restrict__ ctl, int k_from_r) {
+  if (ctl && ctl->done) return;
+  const int64_t K = (ctl && k_from_r) ? min(Kmax, ctl->r) : Kmax;
   const int w = d_w ? min(*d_w, w_max) : w_max;
   const int64_t total = K * w_max;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -43,11 +45,13 @@ cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int ro
 }
 
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
-                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st) {
+                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st, const IterCtl* ctl,
+                          bool k_from_r) {
   const int64_t total = K * w_max;
   if (total <= 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
-  gather_kernel<<<blocks, 256, 0, st>>>(src, row_stride, col_stride, K, d_idx, d_w, w_max, out, ldo);
+  gather_kernel<<<blocks, 256, 0, st>>>(src, row_stride, col_stride, K, d_idx, d_w, w_max, out, ldo, ctl,
+                                        k_from_r ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -90,7 +94,13 @@ cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, ui
 // block is never inverted explicitly (an explicit inverse loses accuracy in proportion to
 // cond(D_k), which reaches 1e9+ once pivots hit the noise floor).
 __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
-                                const int* __restrict__ d_w, int w_max, double* __restrict__ lu, int64_t ldd) {
+                                const int* __restrict__ d_w, int w_max, double* __restrict__ lu, int64_t ldd,
+                                const IterCtl* __restrict__ ctl) {
+  if (ctl) {
+    if (ctl->done) return;
+    Lk += ctl->r * ldl;
+    lu += ctl->r * ldd;
+  }
   const int w = min(*d_w, w_max);
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
     const int p = e % w, q = e / w;
@@ -113,8 +123,8 @@ __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, cons
 }
 
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
-                            double* lu, int64_t ldd, cudaStream_t st) {
-  cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd);
+                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl) {
+  cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
   return cudaGetLastError();
 }
 
@@ -125,8 +135,14 @@ cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows
 template <int WMAX>
 __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
                                      const double* __restrict__ lu, int64_t ldd, const int* __restrict__ d_w,
-                                     int w_max, double* __restrict__ out, int64_t ldo) {
+                                     int w_max, double* __restrict__ out, int64_t ldo,
+                                     const IterCtl* __restrict__ ctl, int64_t out_off_per_r) {
   extern __shared__ double slu[];
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+  }
   const int w = d_w ? min(*d_w, w_max) : w_max;
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
   __syncthreads();
@@ -149,15 +165,16 @@ __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, 
 }
 
 cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
-                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st) {
+                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
+                                 const IterCtl* ctl, int64_t out_off_per_r) {
   if (M <= 0 || w_max <= 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 8));
   const size_t smem = sizeof(double) * static_cast<size_t>(w_max) * w_max;
   if (w_max <= 64) {
-    rows_lu_solve_kernel<64><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo);
+    rows_lu_solve_kernel<64><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
   } else if (w_max <= 256) {
     cudaFuncSetAttribute(rows_lu_solve_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    rows_lu_solve_kernel<256><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo);
+    rows_lu_solve_kernel<256><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
   } else {
     return cudaErrorInvalidValue;  // blocks wider than 256 are rejected by the driver
   }
@@ -165,15 +182,18 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
 }
 
 // Sum `count` partials into *out in a fixed order (one CTA).
-__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t count, double* __restrict__ out) {
+__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t count, double* __restrict__ out,
+                                    const IterCtl* __restrict__ ctl) {
   __shared__ double red[8];
+  if (ctl && ctl->done) return;
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += p[i];
   const double b = block_sum<256>(s, red);
   if (threadIdx.x == 0) *out = b;
 }
-cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st) {
-  sum_partials_kernel<<<1, 256, 0, st>>>(partials, count, d_out);
+cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st,
+                                const IterCtl* ctl) {
+  sum_partials_kernel<<<1, 256, 0, st>>>(partials, count, d_out, ctl);
   return cudaGetLastError();
 }
 
@@ -196,7 +216,7 @@ cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld
   const int64_t total = rows * cols;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), max_parts)));
   sumsq_kernel<<<blocks, 256, 0, st>>>(x, rows, cols, ld, partials);
-  sum_partials_kernel<<<1, 256, 0, st>>>(partials, blocks, d_out);
+  sum_partials_kernel<<<1, 256, 0, st>>>(partials, blocks, d_out, nullptr);
   return cudaGetLastError();
 }
 
@@ -220,15 +240,61 @@ cudaError_t launch_count_nonfinite(const double* x, int64_t rows, int64_t cols, 
   return cudaGetLastError();
 }
 
-// Iteration commit: width = min(|cols|, |rows|) (driver.cpp:123), append the first `width`
-// pivots to I, J (device lists), ban them for later iterations, rho = ||Y|| / ||GA||.
-__global__ void commit_kernel(IterState* s, IterArrays arr, int64_t r, int64_t* __restrict__ I_all,
+// Iteration start (driver.cpp:87-95).
+__global__ void iter_begin_kernel(IterCtl* ctl, IterState* slot) {
+  slot->ncols = slot->nrows = slot->width = 0;
+  slot->valid = 0;
+  if (ctl->done) {
+    ctl->block = 0;
+    return;
+  }
+  if (ctl->r >= ctl->max_rank || ctl->k >= ctl->max_iters) {
+    ctl->done = 1;
+    ctl->status = 1;  // MaxRank
+    ctl->block = 0;
+    return;
+  }
+  slot->valid = 1;
+  ctl->block = static_cast<int32_t>(min(static_cast<int64_t>(ctl->b), ctl->max_rank - ctl->r));
+}
+cudaError_t launch_iter_begin(IterCtl* ctl, IterState* slot, cudaStream_t st) {
+  iter_begin_kernel<<<1, 1, 0, st>>>(ctl, slot);
+  return cudaGetLastError();
+}
+
+__global__ void width_kernel(IterState* slot, const IterCtl* ctl) {
+  if (ctl->done) return;
+  slot->width = min(slot->ncols, slot->nrows);
+}
+cudaError_t launch_width(IterState* slot, const IterCtl* ctl, cudaStream_t st) {
+  width_kernel<<<1, 1, 0, st>>>(slot, ctl);
+  return cudaGetLastError();
+}
+
+// Iteration commit (driver.cpp:102-159).
+__global__ void commit_kernel(IterCtl* ctl, IterState* slot, IterArrays arr, int64_t* __restrict__ I_all,
                               int64_t* __restrict__ J_all, uint8_t* __restrict__ row_mask,
-                              uint8_t* __restrict__ col_mask, double ga_norm) {
-  const int width = min(s->ncols, s->nrows);
-  if (threadIdx.x == 0) {
-    s->width = width;
-    s->rho = ga_norm > 0.0 ? sqrt(s->ysq) / ga_norm : 0.0;
+                              uint8_t* __restrict__ col_mask, const double* __restrict__ y_partials,
+                              int64_t y_parts) {
+  __shared__ int s_stop;
+  __shared__ double red[8];
+  if (ctl->done) return;
+  {  // ||Y||^2 of the downdated residual: fixed-order sum of the GEMM's per-CTA partials
+    double sq = 0.0;
+    for (int64_t i = threadIdx.x; i < y_parts; i += blockDim.x) sq += y_partials[i];
+    const double tot = block_sum<256>(sq, red);
+    if (threadIdx.x == 0) ctl->ysq = tot;
+  }
+  const int width = min(slot->ncols, slot->nrows);
+  const int64_t r = ctl->r;
+  if (threadIdx.x == 0) s_stop = (slot->ncols == 0 || slot->nrows == 0) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) {  // empty column or row selection -> ResidualExhausted, factors unchanged
+    if (threadIdx.x == 0) {
+      ctl->done = 1;
+      ctl->status = 2;
+    }
+    return;
   }
   for (int q = threadIdx.x; q < width; q += blockDim.x) {
     I_all[r + q] = arr.row_idx[q];
@@ -236,19 +302,25 @@ __global__ void commit_kernel(IterState* s, IterArrays arr, int64_t r, int64_t* 
     row_mask[arr.row_idx[q]] = 1;
     col_mask[arr.col_idx[q]] = 1;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double rho = ctl->ga_norm > 0.0 ? sqrt(ctl->ysq) / ctl->ga_norm : 0.0;
+    slot->width = width;
+    slot->ysq = ctl->ysq;
+    slot->rho = rho;
+    ctl->rho = rho;
+    ctl->r = r + width;
+    ctl->k += 1;
+    if (rho <= ctl->threshold) {
+      ctl->done = 1;
+      ctl->status = 0;  // Converged
+    }
+  }
 }
-cudaError_t launch_commit(IterState* s, const IterArrays& arr, int64_t r, int64_t* I_all, int64_t* J_all,
-                          uint8_t* row_mask, uint8_t* col_mask, double ga_norm, cudaStream_t st) {
-  commit_kernel<<<1, 256, 0, st>>>(s, arr, r, I_all, J_all, row_mask, col_mask, ga_norm);
-  return cudaGetLastError();
-}
-
-// width = min(ncols, nrows) published before the U/Rt/Y stages of the same iteration.
-__global__ void width_kernel(IterState* s) {
-  s->width = min(s->ncols, s->nrows);
-}
-cudaError_t launch_width(IterState* s, cudaStream_t st) {
-  width_kernel<<<1, 1, 0, st>>>(s);
+cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, int64_t* I_all, int64_t* J_all,
+                          uint8_t* row_mask, uint8_t* col_mask, const double* y_partials, int64_t y_parts,
+                          cudaStream_t st) {
+  commit_kernel<<<1, 256, 0, st>>>(ctl, slot, arr, I_all, J_all, row_mask, col_mask, y_partials, y_parts);
   return cudaGetLastError();
 }
 

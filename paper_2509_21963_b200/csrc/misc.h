@@ -1,4 +1,5 @@
-// misc.h — small per-iteration kernels (misc.cu) and the device iteration record.
+// misc.h — small per-iteration kernels (misc.cu), the device-resident loop control and the
+// per-iteration record.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -7,14 +8,31 @@
 
 namespace itercur_b200 {
 
-// Device-side record of one iteration. Lives at the head of one allocation followed by
+// Loop state that lives on the device so the host can enqueue several iterations without
+// waiting for each one (proj/src/driver.cpp:86-160 control flow, evaluated on the device).
+struct IterCtl {
+  int64_t r;          // current rank (sum of committed widths)
+  int64_t k;          // committed iterations
+  int64_t max_rank;
+  int64_t max_iters;
+  int32_t done;       // set once the run must stop; every later kernel returns immediately
+  int32_t status;     // 0 Converged, 1 MaxRank, 2 ResidualExhausted (valid when done)
+  int32_t block;      // requested column steps of the current iteration: min(b, max_rank - r)
+  int32_t b;
+  double ysq;         // ||Y||_F^2 of the current sketched residual
+  double rho;         // ||Y||_F / ||GA||_F
+  double threshold;
+  double ga_norm;
+};
+
+// Device-side record of one iteration. Lives at the head of one allocation slot followed by
 // six arrays of `b` entries (col_idx, row_idx as int64; col_best, col_second, row_best,
-// row_second as double) so one D2H copy returns everything the host loop needs.
+// row_second as double) so one D2H copy returns a whole batch of iterations.
 struct IterState {
   int ncols;   // accepted column pivots (col LUPP)
   int nrows;   // accepted row pivots (row LUPP)
   int width;   // min(ncols, nrows)
-  int pad;
+  int valid;   // 1 if this slot's iteration ran (the run was not already done)
   double ysq;  // ||Y||_F^2 after the downdate
   double rho;  // ||Y||_F / ||GA||_F
   double pad2[4];
@@ -29,6 +47,7 @@ struct IterArrays {
   double* row_best;
   double* row_second;
 };
+inline size_t iter_state_bytes(int b) { return sizeof(IterState) + 6 * sizeof(double) * static_cast<size_t>(b); }
 inline IterArrays iter_arrays(void* base, int b) {
   char* p = static_cast<char*>(base) + sizeof(IterState);
   IterArrays a;
@@ -40,32 +59,45 @@ inline IterArrays iter_arrays(void* base, int b) {
   a.row_second = a.row_best + b;
   return a;
 }
-inline size_t iter_state_bytes(int b) { return sizeof(IterState) + 6 * sizeof(double) * static_cast<size_t>(b); }
 
 cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int rows, double* Wc, int64_t ldwc,
                                   cudaStream_t st);
-// out(k, q) = src[k * row_stride + idx[q] * col_stride], k < K, q < min(*d_w, w_max); zero beyond
+// out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < min(*d_w, w_max), zero for
+// q >= w. With ctl: skipped when ctl->done, and K = ctl->r when k_from_r.
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
-                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st);
+                          const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
+                          const IterCtl* ctl = nullptr, bool k_from_r = false);
 // out(k, q) = src[idx[k] + q * ld] for k < K, q < w (row-indexed gather)
 cudaError_t launch_gather2(const double* src, int64_t ld, const int64_t* d_idx, int64_t K, int w, double* out,
                            int64_t ldo, cudaStream_t st);
 // G(i, j) = normal_at(seed, stream_tag, i, j), rows x cols column-major (rng.cpp:61-67)
 cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* out,
                                    cudaStream_t st);
-// LU (no pivoting; rows already in LUPP order) of D = Lk(rows, 0:w) into lu (ld ldd)
+// LU (no pivoting; rows already in LUPP order) of D = Lk(rows, 0:w) into lu (ld ldd).
+// With ctl: Lk += ctl->r * ldl, lu += ctl->r * ldd, skipped when done.
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
-                            double* lu, int64_t ldd, cudaStream_t st);
-// out(j, :) = X(j, :) * D^{-T} (each row solves D x = u) via the LU factors (in place allowed)
+                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl = nullptr);
+// out(j, :) = X(j, :) * D^{-T} (each row solves D x = u) via the LU factors (in place allowed).
+// With ctl: lu += ctl->r * ldd, out += ctl->r * out_off_per_r, skipped when done.
 cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
-                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st);
-cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st);
+                                 const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
+                                 const IterCtl* ctl = nullptr, int64_t out_off_per_r = 0);
+cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st,
+                                const IterCtl* ctl = nullptr);
 cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partials, int max_parts,
                          double* d_out, cudaStream_t st);
 cudaError_t launch_count_nonfinite(const double* x, int64_t rows, int64_t cols, int64_t ld,
                                    unsigned long long* d_count, cudaStream_t st);
-cudaError_t launch_commit(IterState* s, const IterArrays& arr, int64_t r, int64_t* I_all, int64_t* J_all,
-                          uint8_t* row_mask, uint8_t* col_mask, double ga_norm, cudaStream_t st);
-cudaError_t launch_width(IterState* s, cudaStream_t st);
+// Start of an iteration (driver.cpp:87-95): budget checks, block = min(b, max_rank - r).
+cudaError_t launch_iter_begin(IterCtl* ctl, IterState* slot, cudaStream_t st);
+// width = min(ncols, nrows) (driver.cpp:123), published before the core/downdate stages.
+cudaError_t launch_width(IterState* slot, const IterCtl* ctl, cudaStream_t st);
+// End of an iteration (driver.cpp:102-159): empty selections -> ResidualExhausted; append the
+// first `width` pivots to I, J, ban them, r += width, k++, rho = ||Y||/||GA||, rho <= thr ->
+// Converged.
+// The ||Y||^2 partials of the downdate (y_parts of them) are summed here in a fixed order.
+cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, int64_t* I_all, int64_t* J_all,
+                          uint8_t* row_mask, uint8_t* col_mask, const double* y_partials, int64_t y_parts,
+                          cudaStream_t st);
 
 }  // namespace itercur_b200

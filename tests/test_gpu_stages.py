@@ -22,15 +22,16 @@ def _ulp_diff(a, b):
 
 
 def test_device_normals_vs_reference_stream(engine):
-    """Philox + to_unit are bit-exact; CUDA log/cos vs glibc differ by <= 2 ulp on a few entries (F4)."""
+    """Philox + to_unit are bit-exact and log/cos are correctly rounded on the device, so the
+    sketch entries equal the reference's except where glibc itself misrounds."""
     S = _stages()
     with open(os.path.join(GOLD, "rng_kat.json")) as f:
         g = json.load(f)
     block = np.array([[float.fromhex(h) for h in row] for row in g["sketch_block_seed0_11x512"]])
     dev = S.gaussian_matrix(11, 512, 0, 1).cpu().numpy()
     d = _ulp_diff(dev, block)
-    assert d.max() <= 4, d.max()
-    assert (d == 0).mean() >= 0.98, (d != 0).sum()
+    assert d.max() <= 2, d.max()
+    assert (d == 0).mean() >= 0.99, (d != 0).sum()
     for seed, stream, i, j, hx in g["normal_at"][:200]:
         if i > 100000 or j > 250000:
             continue

@@ -1,0 +1,68 @@
+"""Run the engine on BASELINE configs (default 1..5) on one GPU and print one JSON line each:
+status, rank, iterations, device time, m*n/s, sketch-kernel roofline, true error, phases."""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--true-error", action="store_true")
+    args = ap.parse_args()
+    import torch
+
+    import paper_2509_21963_b200 as engine
+    from paper_2509_21963_b200 import stages, testmat
+
+    hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                      "MEASURED_PEAKS.json")))["hbm_gbs"]
+    for cfgno in [int(x) for x in args.configs.split(",")]:
+        cfg = dict(testmat.CONFIGS[cfgno])
+        m, n = cfg["m"], cfg["n"]
+        t0 = time.time()
+        a = testmat.generate(cfgno)
+        torch.cuda.synchronize()
+        gen_s = time.time() - t0
+        h = engine.MatrixHandle.device(a)
+        kw = dict(epsilon=cfg["epsilon"], b=cfg["b"], seed=0, sketch=cfg["sketch"], max_rank=cfg["max_rank"])
+        f, t = engine.iterative_cur(h, profile=True, **kw)  # warm + phases
+        phases = {"sketch_s": t.sketch_s}
+        for key in ("select_cols_s", "row_residual_s", "select_rows_s", "core_s", "downdate_s"):
+            phases[key] = round(sum(getattr(r, key) for r in t.iterations), 5)
+        times = []
+        for _ in range(args.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f, t = engine.iterative_cur(h, **kw)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        sec = min(times)
+        sk = stages.time_sketch_kernel(a, cfg["b"], kind=cfg["sketch"], reps=3)
+        c = engine.sketch_rows_for_block(cfg["b"])
+        cpad = (c + 7) // 8 * 8
+        bytes_alg = 8.0 * m * n + 8.0 * c * n
+        flops_alg = 2.0 * c * m * n
+        out = {"config": cfgno, "m": m, "n": n, "status": t.status, "rank": f.rank, "iterations": len(t.iterations),
+               "final_rho": t.final_rho, "seconds": sec, "mn_per_s": m * n / sec, "gen_s": round(gen_s, 2),
+               "sketch_ms": sk["ms"], "sketch_hbm_frac": bytes_alg / (sk["ms"] * 1e-3) / 1e9 / hbm,
+               "sketch_fp64_frac_alg": flops_alg / (sk["ms"] * 1e-3) / 37.1e12,
+               "sketch_dmma_frac_issued": 2.0 * cpad * m * n / (sk["ms"] * 1e-3) / 37.1e12,
+               "sketch_splits": sk["splits"], "sketch_ctas": sk["ctas"], "tma": sk["tma"], "phases_s": phases,
+               "launches": t.kernel_launches}
+        if args.true_error:
+            out["true_error"] = engine.true_relative_error(h, f)
+        print(json.dumps(out), flush=True)
+        del f, t, h, a
+        torch.cuda.empty_cache()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
