@@ -178,6 +178,16 @@ ITERCUR_API int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t 
                                int32_t reps, void* stream, double* ms_per_launch, int32_t* ctas, int32_t* splits,
                                int32_t* uses_tma);
 
+/* Time the LUPP selection kernel alone on a random rows x steps column-major W (CUDA
+   events, `reps` launches after one warm-up). path_used: -CL for the cluster kernel,
+   G for the grid shared-memory kernel, 1000000 + G for the global-memory kernel. */
+ITERCUR_API int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_path, void* stream,
+                                  double* us_per_launch, int32_t* path_used);
+
+/* Time the tall-skinny DMMA GEMM C = A(:,idx) - L * B (the row-residual shape) on random
+   data: M x K times K x N, `reps` launches; returns microseconds per launch. */
+ITERCUR_API int itercur_time_gemm(int64_t M, int32_t N, int64_t K, int32_t reps, void* stream, double* us_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

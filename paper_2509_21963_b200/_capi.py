@@ -27,7 +27,7 @@ EXPORTED = [
     "itercur_run_core_matrix", "itercur_true_relative_error_device", "itercur_run_free",
     "itercur_adjusted_threshold", "itercur_gratton_tail", "itercur_sketch_rows_for_block",
     "itercur_gaussian_matrix_device", "itercur_sketch_device", "itercur_select_device",
-    "itercur_time_sketch_kernel",
+    "itercur_time_sketch_kernel", "itercur_time_lupp", "itercur_time_gemm",
 ]
 
 
@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
                                             i64p, C.c_int64, i64p, i64p, i32p, dp, dp, dp, vp]),
         "itercur_time_sketch_kernel": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                                  C.c_int32, vp, dp, i32p, i32p, i32p]),
+        "itercur_time_lupp": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, dp, i32p]),
+        "itercur_time_gemm": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int32, vp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -21,6 +21,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -77,6 +78,14 @@ int guarded(F&& f) {
 // raised once), so the per-run workspaces cost no cudaMalloc / cudaFree synchronisation
 // after the first run.
 thread_local cudaStream_t g_alloc_stream = nullptr;
+
+// The engine's own non-blocking work stream (one per host thread, never destroyed): the
+// iteration batches are captured into CUDA graphs, which the legacy default stream cannot do.
+cudaStream_t work_stream() {
+  thread_local cudaStream_t s = nullptr;
+  if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
 
 void configure_mempool_once() {
   static bool done = false;
@@ -146,7 +155,8 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 // ====================================================================== the run handle
 struct itercur_run {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // the caller's stream (accessors run on it)
+  cudaStream_t wstream = nullptr;  // the engine's work stream for iterative_cur (capturable)
   int64_t m = 0, n = 0, lda = 0;
   const double* A = nullptr;
   DevBuf<double> A_owned;  // host entry: device copy of A
@@ -287,7 +297,7 @@ double min_margin(const double* best, const double* second, int count) {
 // The driver: proj/src/driver.cpp:48-167 over device state.
 void run_iterative_cur(itercur_run* run) {
   const itercur_config& cfg = run->cfg;
-  cudaStream_t st = run->stream;
+  cudaStream_t st = run->wstream;
   const int64_t m = run->m, n = run->n, lda = run->lda;
   const double* A = run->A;
   const auto t_start = std::chrono::steady_clock::now();
@@ -313,7 +323,7 @@ void run_iterative_cur(itercur_run* run) {
     if (cfg.b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
     fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
   }
-  if (cfg.b > 2048) fail(ITERCUR_E_INVALID_ARGUMENT, "block size above 2048 is not supported by the B200 engine");
+  if (cfg.b > 180) fail(ITERCUR_E_INVALID_ARGUMENT, "block size above 180 is not supported by the B200 engine yet");
 
   const int64_t b = cfg.b;
   const int64_t min_dim = std::min(m, n);
@@ -445,7 +455,18 @@ void run_iterative_cur(itercur_run* run) {
   CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, ldn, st));
   run->launches += 1;
 
-  uint8_t epoch = 1;
+  const uint8_t epoch = 2;  // the global-memory LUPP clears its in-call marks, so one epoch suffices
+  static uint32_t run_counter = 0;
+  const uint32_t gen_base = ((++run_counter) & 0x3FFu) << 21;  // LUPP slot-tag generations
+  const bool use_graph = !evs.on && getenv("ITERCUR_NO_GRAPH") == nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_cap = -1;
+  struct ExecGuard {
+    cudaGraphExec_t* e;
+    ~ExecGuard() {
+      if (*e) cudaGraphExecDestroy(*e);
+    }
+  } exec_guard{&graph_exec};
   int64_t k_host = 0, r_host = 0;
   int64_t ev_i = 2;
   std::vector<size_t> iter_events;
@@ -458,158 +479,187 @@ void run_iterative_cur(itercur_run* run) {
       ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
     }
     const int64_t ldbg = run->capL;
-    for (int j = 0; j < kBatch; ++j) {
-      IterState* slot = reinterpret_cast<IterState*>(slots + slot_bytes * j);
-      const IterArrays arr = iter_arrays(slot, B);
-      if (++epoch == 0 || epoch == 1) {  // epochs cycle through 2..255 (global-memory LUPP path)
-        CK(launch_clear_epochs(ws.col_mask.p, n, st));
-        CK(launch_clear_epochs(ws.row_mask.p, m, st));
-        run->launches += 2;
-        epoch = 2;
-      }
-      const size_t e0 = static_cast<size_t>(ev_i);
-      if (evs.on) {
-        CK(cudaEventRecord(evs.get(e0), st));
-        iter_events.push_back(e0);
-        ev_i += 6;
-      }
-      CK(launch_iter_begin(d_ctl, slot, st));
+    // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
+    // when the factor buffers grow) and replayed, so a batch costs one graph launch
+    auto enqueue_batch = [&]() {
+      for (int j = 0; j < kBatch; ++j) {
+        IterState* slot = reinterpret_cast<IterState*>(slots + slot_bytes * j);
+        const IterArrays arr = iter_arrays(slot, B);
+        const size_t e0 = static_cast<size_t>(ev_i);
+        if (evs.on) {
+          CK(cudaEventRecord(evs.get(e0), st));
+          iter_events.push_back(e0);
+          ev_i += 6;
+        }
+        CK(launch_iter_begin(d_ctl, slot, st));
 
-      // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
-      {
-        LuppArgs la{};
-        la.W = ws.Wc.p;
-        la.rows = n;
-        la.ldw = ldn;
-        la.cols_max = B;
-        la.d_steps = &d_ctl->block;
-        la.mask = ws.col_mask.p;
-        la.epoch = epoch;
-        la.d_norm_sq = &d_ctl->ysq;
-        la.pivot_floor = cfg.pivot_floor;
-        la.d_idx = arr.col_idx;
-        la.d_best = arr.col_best;
-        la.d_second = arr.col_second;
-        la.d_count = &slot->ncols;
-        CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
-      }
-      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
+        // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
+        {
+          LuppArgs la{};
+          la.W = ws.Wc.p;
+          la.rows = n;
+          la.ldw = ldn;
+          la.cols_max = B;
+          la.d_steps = &d_ctl->block;
+          la.mask = ws.col_mask.p;
+          la.epoch = epoch;
+          la.d_norm_sq = &d_ctl->ysq;
+          la.pivot_floor = cfg.pivot_floor;
+          la.d_idx = arr.col_idx;
+          la.d_best = arr.col_best;
+          la.d_second = arr.col_second;
+          la.d_count = &slot->ncols;
+          la.d_gen_k = &d_ctl->k;
+          la.gen_base = gen_base;
+          la.gen_which = 0;
+          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+        }
+        if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
 
-      // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60)
-      {
-        TsGemmParams p;
-        p.M = m;
-        p.K = ldbg;
-        p.ctl = d_ctl;
-        p.k_from_r = 1;
-        p.N = B;
-        p.d_n = &slot->ncols;
-        p.A = run->L.p;
-        p.lda = run->ldL;
-        p.B = run->Rt.p;  // B(k, q) = Rt(k, J_k[q])
-        p.bsk = run->ldR;
-        p.bsn = 1;
-        p.b_idx = arr.col_idx;
-        p.base_mode = kBaseGatherCols;
-        p.src = A;
-        p.lds = lda;
-        p.idx = arr.col_idx;
-        p.alpha = -1.0;
-        p.out_mode = kOutColMajor;
-        p.C0 = run->L.p;
-        p.c0_off_per_r = run->ldL;
-        p.ldc0 = run->ldL;
-        p.C1 = ws.Wr.p;
-        p.ldc1 = ldm;
-        CK(run_ts_gemm(p, st));
-      }
-      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
+        // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60);
+        //     Rt(:,J_k) is gathered once into a contiguous K x w block (a strided gather inside
+        //     the GEMM loader would re-fetch one 32-B sector per element in every CTA)
+        CK(launch_gather(run->Rt.p, run->ldR, 1, ldbg, arr.col_idx, &slot->ncols, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        {
+          TsGemmParams p;
+          p.M = m;
+          p.K = ldbg;
+          p.ctl = d_ctl;
+          p.k_from_r = 1;
+          p.N = B;
+          p.d_n = &slot->ncols;
+          p.A = run->L.p;
+          p.lda = run->ldL;
+          p.B = ws.Bg.p;  // B(k, q) = Rt(k, J_k[q])
+          p.bsk = 1;
+          p.bsn = ldbg;
+          p.base_mode = kBaseGatherCols;
+          p.src = A;
+          p.lds = lda;
+          p.idx = arr.col_idx;
+          p.alpha = -1.0;
+          p.out_mode = kOutColMajor;
+          p.C0 = run->L.p;
+          p.c0_off_per_r = run->ldL;
+          p.ldc0 = run->ldL;
+          p.C1 = ws.Wr.p;
+          p.ldc1 = ldm;
+          CK(run_ts_gemm(p, st));
+        }
+        if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
 
-      // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
-      {
-        LuppArgs la{};
-        la.W = ws.Wr.p;
-        la.rows = m;
-        la.ldw = ldm;
-        la.cols_max = B;
-        la.d_steps = &slot->ncols;
-        la.mask = ws.row_mask.p;
-        la.epoch = epoch;
-        la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
-        la.pivot_floor = cfg.pivot_floor;
-        la.d_idx = arr.row_idx;
-        la.d_best = arr.row_best;
-        la.d_second = arr.row_second;
-        la.d_count = &slot->nrows;
-        la.d_width_out = &slot->width;  // width = min(|cols|, |rows|), driver.cpp:123
-        la.d_width_cap = &slot->ncols;
-        CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
-      }
-      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
+        // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
+        {
+          LuppArgs la{};
+          la.W = ws.Wr.p;
+          la.rows = m;
+          la.ldw = ldm;
+          la.cols_max = B;
+          la.d_steps = &slot->ncols;
+          la.mask = ws.row_mask.p;
+          la.epoch = epoch;
+          la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
+          la.pivot_floor = cfg.pivot_floor;
+          la.d_idx = arr.row_idx;
+          la.d_best = arr.row_best;
+          la.d_second = arr.row_second;
+          la.d_count = &slot->nrows;
+          la.d_width_out = &slot->width;  // width = min(|cols|, |rows|), driver.cpp:123
+          la.d_width_cap = &slot->ncols;
+          la.d_gen_k = &d_ctl->k;
+          la.gen_base = gen_base;
+          la.gen_which = 1;
+          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+        }
+        if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
 
-      // (4) core step: LU of D_k = S_row(I_k, 0:w); U_k^T = A(I_k,:)^T - Rt^T L(I_k,:)^T;
-      //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
-      CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
-      {
-        TsGemmParams p;
-        p.M = n;
-        p.K = ldbg;
-        p.ctl = d_ctl;
-        p.k_from_r = 1;
-        p.N = B;
-        p.d_n = &slot->width;
-        p.A = run->Rt.p;
-        p.lda = run->ldR;
-        p.B = run->L.p;  // B(k, q) = L(I_k[q], k)
-        p.bsk = run->ldL;
-        p.bsn = 1;
-        p.b_idx = arr.row_idx;
-        p.base_mode = kBaseGatherRowsT;
-        p.src = A;
-        p.lds = lda;
-        p.idx = arr.row_idx;
-        p.alpha = -1.0;
-        p.out_mode = kOutColMajor;
-        p.C0 = ws.Ut.p;
-        p.ldc0 = ldn;
-        CK(run_ts_gemm(p, st));
-      }
-      CK(launch_rows_lu_solve(ws.Ut.p, ldn, n, run->Dinv.p, run->bmax, &slot->width, B, run->Rt.p, run->ldR, st,
-                              d_ctl, run->ldR));
-      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
+        // (4) core step: LU of D_k = S_row(I_k, 0:w); U_k^T = A(I_k,:)^T - Rt^T L(I_k,:)^T;
+        //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
+        CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
+        CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        {
+          TsGemmParams p;
+          p.M = n;
+          p.K = ldbg;
+          p.ctl = d_ctl;
+          p.k_from_r = 1;
+          p.N = B;
+          p.d_n = &slot->width;
+          p.A = run->Rt.p;
+          p.lda = run->ldR;
+          p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
+          p.bsk = 1;
+          p.bsn = ldbg;
+          p.base_mode = kBaseGatherRowsT;
+          p.src = A;
+          p.lds = lda;
+          p.idx = arr.row_idx;
+          p.alpha = -1.0;
+          p.out_mode = kOutColMajor;
+          p.C0 = ws.Ut.p;
+          p.ldc0 = ldn;
+          CK(run_ts_gemm(p, st));
+        }
+        CK(launch_rows_lu_solve(ws.Ut.p, ldn, n, run->Dinv.p, run->bmax, &slot->width, B, run->Rt.p, run->ldR, st,
+                                d_ctl, run->ldR));
+        if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
 
-      // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
-      //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
-      CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
-      {
-        TsGemmParams p;
-        p.M = n;
-        p.K = B;
-        p.d_k = &slot->width;
-        p.ctl = d_ctl;
-        p.N = static_cast<int>(cp);
-        p.A = run->Rt.p;
-        p.a_off_per_r = run->ldR;
-        p.lda = run->ldR;
-        p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
-        p.bsk = cp;
-        p.bsn = 1;
-        p.base_mode = kBaseInPlaceRowMajor;
-        p.alpha = -1.0;
-        p.out_mode = kOutRowMajor;
-        p.C0 = ws.Y.p;
-        p.ldc0 = cp;
-        p.Wc = ws.Wc.p;
-        p.ldwc = ldn;
-        p.wc_rows = B;
-        p.norm_part = ws.part.p;
-        CK(run_ts_gemm(p, st));
+        // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
+        //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
+        CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+        {
+          TsGemmParams p;
+          p.M = n;
+          p.K = B;
+          p.d_k = &slot->width;
+          p.ctl = d_ctl;
+          p.N = static_cast<int>(cp);
+          p.A = run->Rt.p;
+          p.a_off_per_r = run->ldR;
+          p.lda = run->ldR;
+          p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
+          p.bsk = cp;
+          p.bsn = 1;
+          p.base_mode = kBaseInPlaceRowMajor;
+          p.alpha = -1.0;
+          p.out_mode = kOutRowMajor;
+          p.C0 = ws.Y.p;
+          p.ldc0 = cp;
+          p.Wc = ws.Wc.p;
+          p.ldwc = ldn;
+          p.wc_rows = B;
+          p.norm_part = ws.part.p;
+          CK(run_ts_gemm(p, st));
+        }
+        CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
+                         st));
+        if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
       }
-      CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
-                       st));
-      if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
-      run->launches += 10;
+    };
+    if (use_graph) {
+      if (!graph_exec || graph_cap != run->capL) {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue_batch();
+        } catch (...) {
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        CK(cudaStreamEndCapture(st, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        graph_cap = run->capL;
+      }
+      CK(cudaGraphLaunch(graph_exec, st));
+    } else {
+      enqueue_batch();
     }
+    run->launches += 12 * kBatch;
     // one D2H read per batch: the batch's records + the loop control
     CK(cudaMemcpyAsync(ws.h_state, ws.state.p, slot_bytes * kBatch + sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -826,13 +876,21 @@ int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t
     auto run = std::make_unique<itercur_run>();
     CK(cudaGetDevice(&run->device));
     run->stream = static_cast<cudaStream_t>(stream);
+    run->wstream = work_stream();
+    {  // the work stream starts after everything already queued on the caller's stream
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, run->stream));
+      CK(cudaStreamWaitEvent(run->wstream, ev, 0));
+      cudaEventDestroy(ev);
+    }
     run->m = m;
     run->n = n;
     run->lda = lda;
     run->A = dA;
     run->cfg = cfg ? *cfg : default_config();
     configure_mempool_once();
-    g_alloc_stream = run->stream;
+    g_alloc_stream = run->wstream;
     run_iterative_cur(run.get());
     *out = run.release();
   });
@@ -846,18 +904,19 @@ int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t ld
     auto run = std::make_unique<itercur_run>();
     CK(cudaGetDevice(&run->device));
     run->stream = nullptr;
+    run->wstream = work_stream();
     configure_mempool_once();
-    g_alloc_stream = run->stream;
+    g_alloc_stream = run->wstream;
     run->m = m;
     run->n = n;
     run->lda = std::max<int64_t>(m, 1);
     if (m > 0 && n > 0) {
       run->A_owned.alloc(static_cast<size_t>(m) * n);
       if (lda == m) {
-        CK(cudaMemcpyAsync(run->A_owned.p, A, sizeof(double) * m * n, cudaMemcpyHostToDevice, run->stream));
+        CK(cudaMemcpyAsync(run->A_owned.p, A, sizeof(double) * m * n, cudaMemcpyHostToDevice, run->wstream));
       } else {
         CK(cudaMemcpy2DAsync(run->A_owned.p, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
-                             cudaMemcpyHostToDevice, run->stream));
+                             cudaMemcpyHostToDevice, run->wstream));
       }
       run->A = run->A_owned.p;
     }
@@ -1129,6 +1188,139 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     if (ctas) *ctas = info.ctas;
     if (splits) *splits = info.splits;
     if (uses_tma) *uses_tma = info.tma ? 1 : 0;
+  });
+}
+
+int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_path, void* stream,
+                      double* us_per_launch, int32_t* path_used) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    configure_mempool_once();
+    g_alloc_stream = st;
+    if (rows < 1 || steps < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "rows and steps must be positive");
+    const int64_t ldw = even(rows);
+    DevBuf<double> W0, W;
+    W0.alloc(static_cast<size_t>(ldw) * steps);
+    W.alloc(static_cast<size_t>(ldw) * steps);
+    CK(launch_gaussian_matrix(ldw, steps, 12345, 3, W0.p, st));
+    DevBuf<uint8_t> mask;
+    mask.alloc(rows);
+    CK(cudaMemsetAsync(mask.p, 0, rows, st));
+    DevBuf<char> scratch, outs;
+    scratch.alloc(lupp_scratch_bytes(steps));
+    outs.alloc(sizeof(int64_t) * steps * 3 + 16);
+    LuppArgs la{};
+    la.W = W.p;
+    la.rows = rows;
+    la.ldw = ldw;
+    la.cols_max = steps;
+    la.mask = mask.p;
+    la.epoch = 2;
+    la.d_norm_sq = nullptr;
+    la.pivot_floor = 1e-13;
+    la.d_idx = reinterpret_cast<int64_t*>(outs.p);
+    la.d_best = reinterpret_cast<double*>(la.d_idx + steps);
+    la.d_second = la.d_best + steps;
+    la.d_count = reinterpret_cast<int*>(la.d_second + steps);
+    set_lupp_force_path(force_path);
+    int used = 0;
+    CK(cudaMemcpyAsync(W.p, W0.p, sizeof(double) * ldw * steps, cudaMemcpyDeviceToDevice, st));
+    CK(run_lupp_with_scratch(la, scratch.p, st, &used));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float total = 0.f;
+    for (int q = 0; q < reps; ++q) {
+      CK(cudaMemcpyAsync(W.p, W0.p, sizeof(double) * ldw * steps, cudaMemcpyDeviceToDevice, st));
+      CK(cudaEventRecord(e0, st));
+      CK(run_lupp_with_scratch(la, scratch.p, st, &used));
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    set_lupp_force_path(0);
+    if (getenv("ITERCUR_LUPP_TRACE")) {  // one traced launch: per-step phase cycles of CTA 0
+      DevBuf<long long> tr;
+      tr.alloc(static_cast<size_t>(steps) * 8);
+      CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * 8, st));
+      set_lupp_force_path(force_path);
+      set_lupp_debug_trace(tr.p);
+      CK(cudaMemcpyAsync(W.p, W0.p, sizeof(double) * ldw * steps, cudaMemcpyDeviceToDevice, st));
+      CK(run_lupp_with_scratch(la, scratch.p, st, &used));
+      set_lupp_debug_trace(nullptr);
+      set_lupp_force_path(0);
+      std::vector<long long> h(static_cast<size_t>(steps) * 8);
+      CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int q = 0; q + 1 < steps; ++q) {
+        const long long* v = h.data() + q * 8;
+        fprintf(stderr,
+                "lupp trace step %d: col1 %lld wcand %lld B2 %lld publish %lld exchange %lld deferred %lld "
+                "B1(after exch) %lld step %lld\n",
+                q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[4] - v[3], v[5] - v[4], v[6] - v[2], v[7] - v[5],
+                v[8] - v[0]);
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *us_per_launch = 1e3 * total / std::max(reps, 1);
+    if (path_used) *path_used = used;
+  });
+}
+
+int itercur_time_gemm(int64_t M, int32_t N, int64_t K, int32_t reps, void* stream, double* us_per_launch) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    configure_mempool_once();
+    g_alloc_stream = st;
+    const int64_t ldl = even(M);
+    DevBuf<double> Lm, Bm, Cm, Asrc;
+    DevBuf<int64_t> idx;
+    Lm.alloc(static_cast<size_t>(ldl) * std::max<int64_t>(K, 1));
+    Bm.alloc(static_cast<size_t>(std::max<int64_t>(K, 1)) * N);
+    Cm.alloc(static_cast<size_t>(ldl) * N);
+    Asrc.alloc(static_cast<size_t>(ldl) * N);
+    idx.alloc(N);
+    CK(launch_gaussian_matrix(ldl, std::max<int64_t>(K, 1), 1, 3, Lm.p, st));
+    CK(launch_gaussian_matrix(std::max<int64_t>(K, 1), N, 2, 3, Bm.p, st));
+    CK(launch_gaussian_matrix(ldl, N, 3, 3, Asrc.p, st));
+    std::vector<int64_t> h(N);
+    for (int q = 0; q < N; ++q) h[q] = q;
+    CK(cudaMemcpyAsync(idx.p, h.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
+    TsGemmParams p;
+    p.M = M;
+    p.K = K;
+    p.N = N;
+    p.A = Lm.p;
+    p.lda = ldl;
+    p.B = Bm.p;
+    p.bsk = 1;
+    p.bsn = std::max<int64_t>(K, 1);
+    p.base_mode = kBaseGatherCols;
+    p.src = Asrc.p;
+    p.lds = ldl;
+    p.idx = idx.p;
+    p.alpha = -1.0;
+    p.out_mode = kOutColMajor;
+    p.C0 = Cm.p;
+    p.ldc0 = ldl;
+    CK(run_ts_gemm(p, st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    for (int q = 0; q < reps; ++q) CK(run_ts_gemm(p, st));
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *us_per_launch = 1e3 * ms / std::max(reps, 1);
   });
 }
 

@@ -17,6 +17,7 @@
 // call so that every launch spreads over several CTAs per SM (these GEMMs are HBM-bound:
 // intensity 2N/8 flop/B ~ the FP64 ridge), keeping all SMs streaming.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.h"
@@ -69,6 +70,22 @@ __device__ __forceinline__ void gemm_load_stage(const TsGemmParams& p, double* s
     cp_async_16(sA + kl * Cfg::BM + il, src, bytes);
   }
   // B tile: [NT*8][kBPitch], element (k, q) -> sB[q * kBPitch + k]
+  if (p.bsk == 1 && !p.b_idx && (p.bsn & 1) == 0 && (reinterpret_cast<uintptr_t>(p.B) & 15) == 0) {
+    // k-contiguous B: 16-byte copies of (k, k+1) pairs (k0 is a multiple of 16)
+    constexpr int B_PAIRS = NT * 8 * kGemmKT / 2;
+    for (int e = threadIdx.x; e < B_PAIRS; e += Cfg::THREADS) {
+      const int ql = e / (kGemmKT / 2), kl = (e % (kGemmKT / 2)) * 2;
+      const int64_t k = k0 + kl;
+      int bytes = 0;
+      const double* src = p.B;
+      if (k < K && ql < nvalid) {
+        bytes = (k + 1 < K) ? 16 : 8;
+        src = p.B + k + (q0 + ql) * p.bsn;
+      }
+      cp_async_16(sB + ql * kBPitch + kl, src, bytes);
+    }
+    return;
+  }
   constexpr int B_ELEMS = NT * 8 * kGemmKT;
   for (int e = threadIdx.x; e < B_ELEMS; e += Cfg::THREADS) {
     const int ql = e / kGemmKT, kl = e % kGemmKT;
@@ -198,6 +215,12 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
 
 // CTA height: the largest of {128, 64, 32} rows that still gives >= 4 CTAs per SM.
 static int gemm_warps(int64_t M) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("ITERCUR_GEMM_WARPS");  // tuning override: 2, 4 or 8
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 2 || forced == 4 || forced == 8) return forced;
   if (ceil_div(M, 128) >= 4 * kNumSMs) return 8;
   if (ceil_div(M, 64) >= 4 * kNumSMs) return 4;
   return 2;

@@ -62,9 +62,17 @@ struct LuppArgs {
   int* d_width_out = nullptr;        // optional out: min(count, *d_width_cap)
   const int* d_width_cap = nullptr;
   int requested_b;          // for `truncated` semantics (host side)
+  // slot-tag generation for the tagged exchange: when d_gen_k is set the generation is
+  // derived on the device, gen_base | (k << 1) | gen_which, so captured graphs replay safely
+  const int64_t* d_gen_k = nullptr;
+  uint32_t gen_base = 0;
+  int gen_which = 0;
 };
 size_t lupp_scratch_bytes(int b);
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used);
 cudaError_t launch_clear_epochs(uint8_t* mask, int64_t count, cudaStream_t st);
+// benchmarking: 0 automatic, 1 cluster only, 2 grid shared-memory only, 3 global only
+void set_lupp_force_path(int path);
+void set_lupp_debug_trace(long long* dbg);  // per-step clock64() trace of CTA 0 (grid path)
 
 }  // namespace itercur_b200

@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -39,6 +40,55 @@ __device__ __forceinline__ Cand block_reduce_cand(Cand c, Cand* sc) {
   Cand r = sc[kLuppThreads / 32];
   __syncthreads();
   return r;
+}
+
+// Warp-level exact argmax with the reference's tie rule, built on redux.sync: a candidate
+// is key = bits(|w|) + 1 (0 = none; non-negative doubles order like their bit patterns),
+// the winner is the largest key, ties -> lowest row index. `second` is the largest
+// magnitude among all other candidates (runner-up, for the margin log).
+struct WCand {
+  uint64_t key;
+  int32_t idx;     // row index (< 2^31 on this path)
+  double second;   // -1 if none
+};
+__device__ __forceinline__ uint64_t mag_key(double mag) {
+  return static_cast<uint64_t>(__double_as_longlong(mag)) + 1ull;
+}
+__device__ __forceinline__ double key_mag(uint64_t key) {
+  return key ? __longlong_as_double(static_cast<long long>(key - 1ull)) : -1.0;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32), lo = static_cast<unsigned>(v);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return (static_cast<uint64_t>(mhi) << 32) | mlo;
+}
+__device__ __forceinline__ WCand warp_argmax(const WCand& c) {
+  const uint64_t best = warp_max_u64(c.key);
+  const int32_t tie_idx = (c.key == best && best != 0) ? c.idx : 0x7fffffff;
+  const int32_t widx = __reduce_min_sync(0xffffffffu, tie_idx);
+  const bool winner = best != 0 && c.key == best && c.idx == widx;
+  // runner-up: the winner lane offers its own second, every other lane its best
+  const double offer = winner ? c.second : key_mag(c.key);
+  const uint64_t okey = offer >= 0.0 ? mag_key(offer) : 0ull;
+  const uint64_t sec = warp_max_u64(okey);
+  WCand r;
+  r.key = best;
+  r.idx = best ? widx : -1;
+  r.second = key_mag(sec);
+  return r;
+}
+__device__ __forceinline__ WCand wcand_merge_row(WCand c, double mag, int32_t idx) {
+  // sequential scan in ascending row order: strict '>' keeps the lowest index on ties
+  const uint64_t k = mag_key(mag);
+  if (k > c.key) {
+    c.second = key_mag(c.key);
+    c.key = k;
+    c.idx = idx;
+  } else if (mag > c.second) {
+    c.second = mag;
+  }
+  return c;
 }
 
 struct LuppKernelArgs {
@@ -134,10 +184,20 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_kernel(LuppKernelArgs ka) {
       if (mk == 1 || mk == ep) continue;
       const double f = __ddiv_rn(W[i + s * ldw], pivot);
       double nxt = 0.0;
-      for (int t = s + 1; t < steps; ++t) {
-        const double v = __dsub_rn(W[i + t * ldw], __dmul_rn(f, prow[t]));
-        W[i + t * ldw] = v;
-        if (t == s + 1) nxt = v;
+      // columns in chunks of 8: all loads of a chunk are issued before its stores, so the
+      // L2 round trips overlap instead of serialising on the possible aliasing
+      for (int t0 = s + 1; t0 < steps; t0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (t0 + u < steps) ? W[i + (t0 + u) * ldw] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (t0 + u < steps) {
+            v[u] = __dsub_rn(v[u], __dmul_rn(f, prow[t0 + u]));
+            W[i + (t0 + u) * ldw] = v[u];
+          }
+        }
+        if (t0 == s + 1) nxt = v[0];
       }
       local = cand_merge(local, Cand{fabs(nxt), -1.0, i});
     }
@@ -145,9 +205,18 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_kernel(LuppKernelArgs ka) {
     if (threadIdx.x == 0) ka.cand[((s + 1) & 1) * G + blockIdx.x] = bc;
     grid.sync();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *a.d_count = count;
-    if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+  if (blockIdx.x == 0) {
+    // drop this call's in-call ban marks (pivots) so the next call may reuse the same epoch;
+    // no CTA reads the mask after the final pivot decision
+    __syncthreads();  // d_idx was written by thread 0
+    for (int q = threadIdx.x; q < count; q += kLuppThreads) {
+      const int64_t i = a.d_idx[q];
+      if (a.mask[i] == ep) a.mask[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      *a.d_count = count;
+      if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+    }
   }
 }
 
@@ -161,20 +230,49 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_kernel(LuppKernelArgs ka) {
 // ---------------------------------------------------------------------------------
 struct LuppSmemArgs {
   LuppArgs a;
-  double* pub;        // [2][G][pub_stride]: mag, second, idx, then the row tail
+  double* pub;        // [2][G][pub_stride]: tag, mag, second, idx, then the row tail
   int pub_stride;
   double* norm_part;  // [G]
   int rows_per_cta;
+  uint32_t gen;       // per-call generation: slot tags are (gen << 32) | (step + 1)
 };
+
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Pipelined per-CTA schedule. Warp 0 is the communication warp (owns no rows); warps 1..7
+// own the CTA's rows. Per pivot step s:
+//   compute warps: read the pivot (s_best / prow of step s), eliminate only column s+1 of
+//     their rows (factor = W(i,s)/pivot, kept for later), take the candidate on column s+1,
+//     and each warp materialises its own winner row's tail (columns >= s+2) from the
+//     not-yet-updated values; [B2]; then apply the deferred updates of columns >= s+2 —
+//     overlapped with the exchange below.
+//   warp 0: [B2]; block argmax over the warps; write the CTA slot (header + tail) and
+//     release it with a (generation, step) tag; poll the G tags with acquire loads — the
+//     arrivals are the barrier; read the headers, reduce them in the same order as every
+//     other CTA, fetch the winner's tail; publish s_best / prow of step s+1 (double-buffered).
+//   [B1] all threads.
+// The arithmetic per element is the reference's (factor = W(i,s)/pivot, W(i,t) -= factor *
+// W(best,t), separate roundings), so the pivot sequence is identical to select.cpp:40-70.
+constexpr int kCompWarps = kLuppThreads / 32 - 1;
 
 __global__ void __launch_bounds__(kLuppThreads) lupp_smem_kernel(LuppSmemArgs ka) {
   cg::grid_group grid = cg::this_grid();
   const LuppArgs& a = ka.a;
   extern __shared__ double sm[];
-  __shared__ Cand sc[kLuppThreads / 32 + 1];
+  __shared__ WCand wc[kLuppThreads / 32];
   __shared__ double sred[kLuppThreads / 32];
-  __shared__ int s_winner;
+  __shared__ WCand s_best[2];
   const int G = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ctid = threadIdx.x - 32;  // compute-thread id (warps 1..7)
+  constexpr int kComp = kCompWarps * 32;
   const int Rb = ka.rows_per_cta;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * Rb;
   int64_t nr64 = a.rows - r0;
@@ -189,15 +287,17 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_smem_kernel(LuppSmemArgs ka
     }
     return;
   }
-  double* Ws = sm;                                   // [steps][Rb]
-  double* F = Ws + static_cast<size_t>(steps) * Rb;  // [Rb] elimination factors
-  double* prow = F + Rb;                             // [steps]
-  uint8_t* banned = reinterpret_cast<uint8_t*>(prow + steps);  // [Rb]
+  const int smax = a.cols_max;
+  const int stride = ka.pub_stride;
+  double* Ws = sm;                                       // [smax][Rb]
+  double* prow = Ws + static_cast<size_t>(smax) * Rb;    // [2][smax] pivot rows (by step parity)
+  double* wtail = prow + 2 * smax;                       // [kLuppThreads/32][smax] warp winner tails
+  double* F = wtail + (kLuppThreads / 32) * smax;        // [Rb] factors of the current step
+  uint8_t* banned = reinterpret_cast<uint8_t*>(F + Rb);  // [Rb]
 
-  for (int e = threadIdx.x; e < steps * nr; e += kLuppThreads) {
-    const int t = e / nr, r = e - t * nr;
-    Ws[t * Rb + r] = a.W[(r0 + r) + t * a.ldw];
-  }
+#pragma unroll 4
+  for (int t = 0; t < steps; ++t)
+    for (int r = threadIdx.x; r < nr; r += kLuppThreads) Ws[t * Rb + r] = a.W[(r0 + r) + t * a.ldw];
   for (int r = threadIdx.x; r < nr; r += kLuppThreads) {
     const uint8_t mk = a.mask[r0 + r];
     banned[r] = (mk == 1 || mk == a.epoch) ? 1 : 0;
@@ -209,11 +309,11 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_smem_kernel(LuppSmemArgs ka
     nsq = *a.d_norm_sq;
   } else {
     double sq = 0.0;
-    for (int e = threadIdx.x; e < steps * nr; e += kLuppThreads) {
-      const int t = e / nr, r = e - t * nr;
-      const double v = Ws[t * Rb + r];
-      sq = fma(v, v, sq);
-    }
+    for (int t = 0; t < steps; ++t)
+      for (int r = threadIdx.x; r < nr; r += kLuppThreads) {
+        const double v = Ws[t * Rb + r];
+        sq = fma(v, v, sq);
+      }
     const double b = block_sum<kLuppThreads>(sq, sred);
     if (threadIdx.x == 0) ka.norm_part[blockIdx.x] = b;
     grid.sync();
@@ -221,73 +321,500 @@ __global__ void __launch_bounds__(kLuppThreads) lupp_smem_kernel(LuppSmemArgs ka
     for (int q = 0; q < G; ++q) nsq += ka.norm_part[q];
   }
   const double abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(nsq);
+  const uint32_t gen = a.d_gen_k ? (a.gen_base | (static_cast<uint32_t>(*a.d_gen_k & 0x1FFFFF) << 1) |
+                                     static_cast<uint32_t>(a.gen_which))
+                                  : ka.gen;
+  const uint64_t gen_hi = static_cast<uint64_t>(gen) << 32;
 
-  // publish this CTA's candidate on column `col` (and its row tail from `col`)
-  auto publish = [&](int col, int parity) {
-    Cand local = cand_empty();
-    for (int r = threadIdx.x; r < nr; r += kLuppThreads)
-      if (!banned[r]) local = cand_merge(local, Cand{fabs(Ws[col * Rb + r]), -1.0, r0 + r});
-    const Cand bc = block_reduce_cand(local, sc);
-    double* slot = ka.pub + (static_cast<size_t>(parity) * G + blockIdx.x) * ka.pub_stride;
-    if (threadIdx.x == 0) {
-      slot[0] = bc.mag;
-      slot[1] = bc.second;
-      slot[2] = __longlong_as_double(bc.idx);
+  // compute warps: warp candidate on column `col` + that row's tail (columns > col) into
+  // wtail[warp]; `upd` = (factor lane value, pivot row) when the tail is an update
+  auto warp_candidate = [&](WCand mine, int col, bool upd, const double* P) {
+    const WCand w = warp_argmax(mine);
+    if (w.key) {
+      const int lr = w.idx - static_cast<int>(r0);
+      const double f = upd ? F[lr] : 0.0;
+      for (int t = col + 1 + lane; t < steps; t += 32)
+        wtail[warp * smax + t] = upd ? __dsub_rn(Ws[t * Rb + lr], __dmul_rn(f, P[t])) : Ws[t * Rb + lr];
     }
-    if (bc.idx >= 0) {
-      const int lr = static_cast<int>(bc.idx - r0);
-      for (int t = col + threadIdx.x; t < steps; t += kLuppThreads) slot[3 + t] = Ws[t * Rb + lr];
+    if (lane == 0) wc[warp] = w;
+  };
+  // warp 0: CTA candidate -> slot (parity of col), released with tag (gen, col + 1)
+  auto publish = [&](int col) {
+    const WCand c = (lane >= 1 && lane <= kCompWarps) ? wc[lane] : WCand{0ull, -1, -1.0};
+    const WCand bc = warp_argmax(c);
+    double* slot = ka.pub + (static_cast<size_t>(col & 1) * G + blockIdx.x) * stride;
+    if (lane == 0) {
+      slot[1] = key_mag(bc.key);
+      slot[2] = bc.second;
+      slot[3] = __longlong_as_double(bc.key ? static_cast<long long>(bc.idx) : -1ll);
     }
+    if (bc.key) {
+      const int lr = bc.idx - static_cast<int>(r0);
+      const int ow = 1 + (lr % kComp) / 32;  // owning compute warp
+      if (lane == 0) slot[4 + col] = Ws[col * Rb + lr];
+      for (int t = col + 1 + lane; t < steps; t += 32) slot[4 + t] = wtail[ow * smax + t];
+    }
+    // __syncwarp orders the lanes' slot writes before lane 0's release store (cumulative)
+    __syncwarp();
+    if (lane == 0) st_release_u64(reinterpret_cast<uint64_t*>(slot), gen_hi | static_cast<uint64_t>(col + 1));
+  };
+  // warp 0: wait for every CTA's slot of step s, reduce, fetch the winner row
+  auto exchange = [&](int s) {
+    const double* pubs = ka.pub + static_cast<size_t>(s & 1) * G * stride;
+    const uint64_t want = gen_hi | static_cast<uint64_t>(s + 1);
+    WCand c{0ull, -1, -1.0};
+    for (int q = lane; q < G; q += 32) {  // ascending q = ascending row slabs
+      const double* slot = pubs + static_cast<size_t>(q) * stride;
+      while (ld_acquire_u64(reinterpret_cast<const uint64_t*>(slot)) != want) {
+      }
+      const double mag = slot[1];
+      if (mag >= 0.0) {
+        const uint64_t k = mag_key(mag);
+        if (k > c.key) {
+          c.second = fmax(key_mag(c.key), slot[2]);
+          c.key = k;
+          c.idx = static_cast<int32_t>(__double_as_longlong(slot[3]));
+        } else {
+          c.second = fmax(c.second, mag);
+        }
+      }
+    }
+    const WCand best = warp_argmax(c);
+    if (best.key) {
+      const double* ws_ = pubs + static_cast<size_t>(best.idx / Rb) * stride;
+      for (int t = s + lane; t < steps; t += 32) prow[(s & 1) * smax + t] = ws_[4 + t];
+    }
+    if (lane == 0) s_best[s & 1] = best;
   };
 
-  publish(0, 0);
-  grid.sync();
+  // ---- step 0: candidates on column 0 ----
+  if (warp > 0) {
+    WCand mine{0ull, -1, -1.0};
+    for (int r = ctid; r < nr; r += kComp)
+      if (!banned[r]) mine = wcand_merge_row(mine, fabs(Ws[r]), static_cast<int32_t>(r0 + r));
+    warp_candidate(mine, 0, false, nullptr);
+  }
+  __syncthreads();  // B2
+  if (warp == 0) {
+    publish(0);
+    exchange(0);
+  }
+  __syncthreads();  // B1
+
   int count = 0;
   double first = 0.0;
   for (int s = 0; s < steps; ++s) {
-    const double* pubs = ka.pub + static_cast<size_t>(s & 1) * G * ka.pub_stride;
-    Cand r = cand_empty();
-    for (int q = threadIdx.x; q < G; q += kLuppThreads) {
-      const double* slot = pubs + static_cast<size_t>(q) * ka.pub_stride;
-      r = cand_merge(r, Cand{slot[0], slot[1], __double_as_longlong(slot[2])});
-    }
-    const Cand best = block_reduce_cand(r, sc);
-    if (best.idx < 0 || best.mag <= abs_floor) break;
+    const WCand best = s_best[s & 1];
+    const double best_mag = key_mag(best.key);
+    if (best.key == 0 || best_mag <= abs_floor) break;
     if (s == 0)
-      first = best.mag;
-    else if (best.mag < a.pivot_floor * first)
+      first = best_mag;
+    else if (best_mag < a.pivot_floor * first)
       break;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       a.d_idx[s] = best.idx;
-      a.d_best[s] = best.mag;
+      a.d_best[s] = best_mag;
       a.d_second[s] = best.second;
     }
     ++count;
     if (s + 1 >= steps) break;
-    // winner CTA = the one whose published index is best.idx (rows are CTA-contiguous)
-    if (threadIdx.x == 0) s_winner = static_cast<int>(best.idx / Rb);
-    __syncthreads();
-    const double* wslot = pubs + static_cast<size_t>(s_winner) * ka.pub_stride;
-    for (int t = s + threadIdx.x; t < steps; t += kLuppThreads) prow[t] = wslot[3 + t];
-    if (best.idx >= r0 && best.idx < r0 + nr && threadIdx.x == 0) banned[best.idx - r0] = 1;
-    __syncthreads();
-    const double pivot = prow[s];
-    for (int rr = threadIdx.x; rr < nr; rr += kLuppThreads)
-      F[rr] = banned[rr] ? 0.0 : __ddiv_rn(Ws[s * Rb + rr], pivot);
-    __syncthreads();
-    const int ncols = steps - s - 1;
-    for (int e = threadIdx.x; e < ncols * nr; e += kLuppThreads) {
-      const int t = s + 1 + e / nr, rr = e - (e / nr) * nr;
-      if (!banned[rr]) Ws[t * Rb + rr] = __dsub_rn(Ws[t * Rb + rr], __dmul_rn(F[rr], prow[t]));
+    const double* P = prow + (s & 1) * smax;
+    if (warp > 0) {
+      // column s+1 first (critical path), factors kept for the deferred columns
+      const double pivot = P[s];
+      WCand mine{0ull, -1, -1.0};
+      for (int rr = ctid; rr < nr; rr += kComp) {
+        if (banned[rr]) continue;
+        if (r0 + rr == best.idx) {
+          banned[rr] = 1;  // only the owning thread ever reads this flag
+          continue;
+        }
+        const double f = __ddiv_rn(Ws[s * Rb + rr], pivot);
+        F[rr] = f;
+        const double v = __dsub_rn(Ws[(s + 1) * Rb + rr], __dmul_rn(f, P[s + 1]));
+        Ws[(s + 1) * Rb + rr] = v;
+        mine = wcand_merge_row(mine, fabs(v), static_cast<int32_t>(r0 + rr));
+      }
+      __syncwarp();
+      warp_candidate(mine, s + 1, true, P);
     }
-    __syncthreads();
-    publish(s + 1, (s + 1) & 1);
-    grid.sync();
+    __syncthreads();  // B2
+    if (warp == 0) {
+      publish(s + 1);
+      exchange(s + 1);
+    } else {
+      // deferred columns s+2.. (overlaps the exchange)
+      for (int rr = ctid; rr < nr; rr += kComp) {
+        if (banned[rr]) continue;
+        const double f = F[rr];
+        for (int t0 = s + 2; t0 < steps; t0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = (t0 + u < steps) ? Ws[(t0 + u) * Rb + rr] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (t0 + u < steps) Ws[(t0 + u) * Rb + rr] = __dsub_rn(v[u], __dmul_rn(f, P[t0 + u]));
+        }
+      }
+    }
+    __syncthreads();  // B1
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *a.d_count = count;
     if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
   }
+}
+
+// ---------------------------------------------------------------------------------
+// Thread-block-cluster variant for small problems (W fits in the shared memory of one
+// cluster of up to 16 CTAs): the per-step exchange goes through distributed shared memory
+// and a cluster barrier instead of global memory and a grid-wide barrier. Each CTA keeps a
+// contiguous slab of rows; per step it publishes (|best|, runner-up, index, row tail) in
+// its own shared memory (double-buffered by step parity), all CTAs read the CL slots over
+// DSMEM after the cluster barrier and reduce them in the same fixed order. Identical
+// arithmetic to the kernels above.
+// ---------------------------------------------------------------------------------
+constexpr int kClusterThreads = 512;
+constexpr int kClusterComp = kClusterThreads - 32;
+
+struct LuppClusterArgs {
+  LuppArgs a;
+  long long* dbg;   // optional per-step clock64() trace of CTA 0 (benchmarking)
+  int rows_per_cta;
+  int slot_stride;  // doubles per published slot: 4 + steps_max (tag, mag, second, idx, tail)
+};
+
+// st.async: store 16 bytes into another CTA's shared memory and signal that CTA's mbarrier
+// with the byte count (complete_tx); the receiver waits on its own barrier only.
+__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, double a, double b, uint32_t remote_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(remote_addr),
+               "d"(a), "d"(b), "r"(remote_mbar)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t map_cluster_addr(uint32_t local_addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_release_cluster_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.cluster.shared::cta.u64 [%0], %1;\n" ::"r"(smem_u32(p)), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_cluster_u64(const uint64_t* generic_remote) {
+  uint64_t v;
+  asm volatile("ld.acquire.cluster.u64 %0, [%1];\n" : "=l"(v) : "l"(generic_remote) : "memory");
+  return v;
+}
+
+// Same pipelined schedule as lupp_smem_kernel, but the slots live in the publishing CTA's
+// own shared memory and are read over distributed shared memory: the per-step exchange is
+// a few DSMEM round trips inside one thread-block cluster (<= 16 CTAs) instead of L2 round
+// trips across the whole GPU. Used whenever W fits in the cluster's shared memory.
+__global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppClusterArgs ka) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const LuppArgs& a = ka.a;
+  extern __shared__ double sm[];
+  __shared__ WCand wc[kClusterThreads / 32];
+  __shared__ double sred[kClusterThreads / 32];
+  __shared__ double s_norm;
+  __shared__ WCand s_best[2];
+  constexpr int kWarps = kClusterThreads / 32;
+  const int CL = static_cast<int>(cluster.num_blocks());
+  const int me = static_cast<int>(cluster.block_rank());
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ctid = threadIdx.x - 32;
+  const int Rb = ka.rows_per_cta;
+  const int64_t r0 = static_cast<int64_t>(me) * Rb;
+  int64_t nr64 = a.rows - r0;
+  nr64 = nr64 < 0 ? 0 : (nr64 > Rb ? Rb : nr64);
+  const int nr = static_cast<int>(nr64);
+  int steps = a.cols_max;
+  if (a.d_steps) steps = min(steps, *a.d_steps);
+  if (steps <= 0) {
+    if (me == 0 && threadIdx.x == 0) {
+      *a.d_count = 0;
+      if (a.d_width_out) *a.d_width_out = 0;
+    }
+    return;  // uniform across the cluster: no DSMEM traffic happened
+  }
+  const int smax = a.cols_max;
+  const int stride = ka.slot_stride;
+  double* Ws = sm;                                       // [smax][Rb]
+  double* prow = Ws + static_cast<size_t>(smax) * Rb;    // [2][smax]
+  double* wtail = prow + 2 * smax;                       // [kWarps][smax]
+  double* F = wtail + kWarps * smax;                     // [Rb]
+  // [2][CL][stride] every CTA's pushed slot (16-byte aligned: st.async writes pairs)
+  double* inbox = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(F + Rb) + 15) & ~uintptr_t(15));
+  double* stage = inbox + 2 * CL * stride;               // [stride] this CTA's outgoing slot
+  uint8_t* banned = reinterpret_cast<uint8_t*>(stage + stride);  // [Rb]
+  __shared__ __align__(8) uint64_t mbar[2];
+
+  for (int t = 0; t < steps; ++t)
+    for (int r = threadIdx.x; r < nr; r += kClusterThreads) Ws[t * Rb + r] = a.W[(r0 + r) + t * a.ldw];
+  for (int r = threadIdx.x; r < nr; r += kClusterThreads) {
+    const uint8_t mk = a.mask[r0 + r];
+    banned[r] = (mk == 1 || mk == a.epoch) ? 1 : 0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  double nsq;
+  if (a.d_norm_sq) {
+    nsq = *a.d_norm_sq;
+    cluster.sync();  // every CTA's mbarriers are initialised before anyone pushes to them
+  } else {
+    double sq = 0.0;
+    for (int t = 0; t < steps; ++t)
+      for (int r = threadIdx.x; r < nr; r += kClusterThreads) {
+        const double v = Ws[t * Rb + r];
+        sq = fma(v, v, sq);
+      }
+    const double b = block_sum<kClusterThreads>(sq, sred);
+    if (threadIdx.x == 0) s_norm = b;
+    cluster.sync();
+    nsq = 0.0;
+    for (int q = 0; q < CL; ++q) nsq += *cluster.map_shared_rank(&s_norm, q);
+  }
+  const double abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(nsq);
+
+  auto warp_candidate = [&](WCand mine, int col, bool upd, const double* P) {
+    const WCand w = warp_argmax(mine);
+    if (w.key) {
+      const int lr = w.idx - static_cast<int>(r0);
+      const double f = upd ? F[lr] : 0.0;
+      for (int t = col + 1 + lane; t < steps; t += 32)
+        wtail[warp * smax + t] = upd ? __dsub_rn(Ws[t * Rb + lr], __dmul_rn(f, P[t])) : Ws[t * Rb + lr];
+    }
+    if (lane == 0) wc[warp] = w;
+  };
+  // warp 0: CTA candidate (mag, second, idx, row tail from `col`) pushed with st.async into
+  // slot `me` of every CTA's inbox (parity of col); each receiver's mbarrier counts the bytes
+  const uint32_t slot_bytes = static_cast<uint32_t>(stride) * 8u;
+  auto publish = [&](int col) {
+    const WCand c = (lane >= 1 && lane < kWarps) ? wc[lane] : WCand{0ull, -1, -1.0};
+    const WCand bc = warp_argmax(c);
+    const int par = col & 1;
+    if (lane == 0) {
+      stage[0] = key_mag(bc.key);
+      stage[1] = bc.second;
+      stage[2] = __longlong_as_double(bc.key ? static_cast<long long>(bc.idx) : -1ll);
+      stage[3] = 0.0;
+    }
+    if (bc.key) {
+      const int lr = bc.idx - static_cast<int>(r0);
+      const int ow = 1 + (lr % kClusterComp) / 32;
+      if (lane == 0) stage[4 + col] = Ws[col * Rb + lr];
+      for (int t = col + 1 + lane; t < steps; t += 32) stage[4 + t] = wtail[ow * smax + t];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(&mbar[par], static_cast<uint32_t>(CL) * slot_bytes);
+    const uint32_t local_slot = smem_u32(inbox + (static_cast<size_t>(par) * CL + me) * stride);
+    const uint32_t local_bar = smem_u32(&mbar[par]);
+    const int pairs = stride / 2;
+    for (int e = lane; e < CL * pairs; e += 32) {
+      const int dst = e / pairs, pr = e - dst * pairs;
+      const int t0 = 2 * pr;
+      // columns < col of the tail are never read: send zeros instead of stale values
+      const double v0 = (t0 < 4 || t0 - 4 >= col) ? stage[t0] : 0.0;
+      const double v1 = (t0 + 1 < 4 || t0 - 3 >= col) ? stage[t0 + 1] : 0.0;
+      st_async_v2(map_cluster_addr(local_slot + t0 * 8, dst), v0, v1, map_cluster_addr(local_bar, dst));
+    }
+  };
+  // warp 0: wait for the CL pushed slots of step s, reduce them in fixed order, keep the
+  // winner's row (all local reads)
+  auto exchange = [&](int s) {
+    const int par = s & 1;
+    mbar_wait_cluster(&mbar[par], static_cast<uint32_t>((s >> 1) & 1));
+    const double* box = inbox + static_cast<size_t>(par) * CL * stride;
+    WCand c{0ull, -1, -1.0};
+    if (lane < CL) {
+      const double* rs = box + static_cast<size_t>(lane) * stride;
+      const double mag = rs[0];
+      if (mag >= 0.0) {
+        c.key = mag_key(mag);
+        c.idx = static_cast<int32_t>(__double_as_longlong(rs[2]));
+        c.second = rs[1];
+      }
+    }
+    const WCand best = warp_argmax(c);
+    if (best.key) {
+      const double* ws_ = box + static_cast<size_t>(best.idx / Rb) * stride;
+      for (int t = s + lane; t < steps; t += 32) prow[par * smax + t] = ws_[4 + t];
+    }
+    if (lane == 0) s_best[par] = best;
+  };
+
+  if (warp > 0) {
+    WCand mine{0ull, -1, -1.0};
+    for (int r = ctid; r < nr; r += kClusterComp)
+      if (!banned[r]) mine = wcand_merge_row(mine, fabs(Ws[r]), static_cast<int32_t>(r0 + r));
+    warp_candidate(mine, 0, false, nullptr);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    publish(0);
+    exchange(0);
+  }
+  __syncthreads();
+
+  int count = 0;
+  double first = 0.0;
+  long long* dbg = (ka.dbg && me == 0) ? ka.dbg : nullptr;
+  for (int s = 0; s < steps; ++s) {
+    if (dbg && threadIdx.x == 32) dbg[s * 8 + 0] = clock64();
+    const WCand best = s_best[s & 1];
+    const double best_mag = key_mag(best.key);
+    if (best.key == 0 || best_mag <= abs_floor) break;
+    if (s == 0)
+      first = best_mag;
+    else if (best_mag < a.pivot_floor * first)
+      break;
+    if (me == 0 && threadIdx.x == 0) {
+      a.d_idx[s] = best.idx;
+      a.d_best[s] = best_mag;
+      a.d_second[s] = best.second;
+    }
+    ++count;
+    if (s + 1 >= steps) break;
+    const double* P = prow + (s & 1) * smax;
+    if (warp > 0) {
+      const double pivot = P[s];
+      WCand mine{0ull, -1, -1.0};
+      for (int rr = ctid; rr < nr; rr += kClusterComp) {
+        if (banned[rr]) continue;
+        if (r0 + rr == best.idx) {
+          banned[rr] = 1;
+          continue;
+        }
+        const double f = __ddiv_rn(Ws[s * Rb + rr], pivot);
+        F[rr] = f;
+        const double v = __dsub_rn(Ws[(s + 1) * Rb + rr], __dmul_rn(f, P[s + 1]));
+        Ws[(s + 1) * Rb + rr] = v;
+        mine = wcand_merge_row(mine, fabs(v), static_cast<int32_t>(r0 + rr));
+      }
+      __syncwarp();
+      if (dbg && threadIdx.x == 32) dbg[s * 8 + 1] = clock64();
+      warp_candidate(mine, s + 1, true, P);
+      if (dbg && threadIdx.x == 32) dbg[s * 8 + 2] = clock64();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (dbg && threadIdx.x == 0) dbg[s * 8 + 3] = clock64();
+      publish(s + 1);
+      if (dbg && threadIdx.x == 0) dbg[s * 8 + 4] = clock64();
+      exchange(s + 1);
+      if (dbg && threadIdx.x == 0) dbg[s * 8 + 5] = clock64();
+    } else {
+      for (int rr = ctid; rr < nr; rr += kClusterComp) {
+        if (banned[rr]) continue;
+        const double f = F[rr];
+        for (int t0 = s + 2; t0 < steps; t0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = (t0 + u < steps) ? Ws[(t0 + u) * Rb + rr] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (t0 + u < steps) Ws[(t0 + u) * Rb + rr] = __dsub_rn(v[u], __dmul_rn(f, P[t0 + u]));
+        }
+      }
+      if (dbg && threadIdx.x == 32) dbg[s * 8 + 6] = clock64();
+    }
+    __syncthreads();
+    if (dbg && threadIdx.x == 32) dbg[s * 8 + 7] = clock64();
+  }
+  if (me == 0 && threadIdx.x == 0) {
+    *a.d_count = count;
+    if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
+static long long* g_lupp_dbg = nullptr;
+
+static int cluster_capacity_ok(int cl, size_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, lupp_cluster_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters;
+}
+
+// Try the cluster path; returns cudaErrorNotSupported when the problem does not fit.
+static cudaError_t try_lupp_cluster(const LuppArgs& a, cudaStream_t st, int* grid_used) {
+  const int steps = std::max(a.cols_max, 1);
+  static bool attr_done = false;
+  static bool usable = false;
+  static int max_cl = 16;
+  const size_t budget = 220 * 1024;
+  if (!attr_done) {
+    attr_done = true;
+    usable = cudaFuncSetAttribute(lupp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess &&
+             cudaFuncSetAttribute(lupp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(budget)) == cudaSuccess;
+    if (usable && cluster_capacity_ok(16, budget) < 1) max_cl = 8;
+    if (usable && cluster_capacity_ok(max_cl, budget) < 1) usable = false;
+    cudaGetLastError();
+  }
+  static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;  // tuning switch
+  if (disabled || !usable || a.rows >= (1ll << 31) - 1) return cudaErrorNotSupported;
+  // smallest cluster whose slabs fit
+  for (int cl = 1; cl <= max_cl; cl *= 2) {
+    const int Rb = static_cast<int>(ceil_div(a.rows, cl));
+    const int stride = static_cast<int>(round_up(steps + 4, 2));
+    const size_t smem = sizeof(double) * (static_cast<size_t>(steps) * Rb + (2 + kClusterThreads / 32) * steps +
+                                          Rb + 2 + (2 * cl + 1) * stride) + Rb + 16;
+    if (smem > budget) continue;
+    // enough rows per CTA to keep 1024 threads busy; prefer more CTAs for big slabs
+    if (cl < max_cl && Rb > 2 * kClusterComp) continue;  // keep every compute thread to <= 2 rows
+    LuppClusterArgs ka;
+    ka.a = a;
+    ka.dbg = g_lupp_dbg;
+    ka.rows_per_cta = Rb;
+    ka.slot_stride = stride;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (grid_used) *grid_used = -cl;
+    return cudaLaunchKernelEx(&cfg, lupp_cluster_kernel, ka);
+  }
+  return cudaErrorNotSupported;
 }
 
 // Clear in-call ban marks (any value other than 1) when the epoch counter wraps.
@@ -320,6 +847,10 @@ size_t lupp_scratch_bytes(int b) {
          sizeof(double) * 2 * kMaxLuppGrid * static_cast<size_t>(b + 4);
 }
 
+static int g_force_path = 0;
+void set_lupp_force_path(int path) { g_force_path = path; }
+void set_lupp_debug_trace(long long* dbg) { g_lupp_dbg = dbg; }
+
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used) {
   if (a.cols_max > 2048) return cudaErrorInvalidValue;
   char* sp = reinterpret_cast<char*>(scratch);
@@ -327,17 +858,24 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
   double* norm_part = reinterpret_cast<double*>(sp + sizeof(Cand) * 2 * kMaxLuppGrid);
   double* pub = norm_part + kMaxLuppGrid;
   const int steps = std::max(a.cols_max, 1);
+  // cluster path (W fits in one thread-block cluster's shared memory)
+  if (g_force_path == 0 || g_force_path == 1) {
+    const cudaError_t e = try_lupp_cluster(a, st, grid_used);
+    if (e != cudaErrorNotSupported) return e;
+  }
   // shared-memory-resident path: one CTA per SM, slab of rows_per_cta x steps doubles
-  {
+  if (g_force_path == 0 || g_force_path == 2) {
     static int sms = 0;
     if (!sms) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.rows, 32))));
+    // enough rows per CTA to amortise the per-step exchange (~300), at most one CTA per SM
+    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.rows, 300))));
     const int Rb = static_cast<int>(ceil_div(a.rows, G));
-    const size_t smem = sizeof(double) * (static_cast<size_t>(steps) * Rb + Rb + steps) + Rb + 16;
+    const size_t smem =
+        sizeof(double) * (static_cast<size_t>(steps) * Rb + (2 + kLuppThreads / 32) * steps + Rb) + Rb + 16;
     if (smem <= kLuppSmemBudget) {
       static size_t attr = 0;
       if (smem > attr) {
@@ -347,12 +885,14 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
         attr = kLuppSmemBudget;
       }
       if (lupp_max_blocks(reinterpret_cast<const void*>(lupp_smem_kernel), smem) >= G) {
+        static uint32_t gen = 0x80000000u;  // host-side generations (stage entries) keep bit 31 set
         LuppSmemArgs ka;
         ka.a = a;
         ka.pub = pub;
-        ka.pub_stride = steps + 3;
+        ka.pub_stride = steps + 4;
         ka.norm_part = norm_part;
         ka.rows_per_cta = Rb;
+        ka.gen = ++gen | 0x80000000u;
         void* params[] = {&ka};
         if (grid_used) *grid_used = G;
         return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lupp_smem_kernel), dim3(G),
@@ -367,7 +907,7 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
     attr_set = true;
   }
   const size_t smem = sizeof(double) * static_cast<size_t>(steps);
-  const int64_t want = std::max<int64_t>(1, ceil_div(a.rows, kLuppThreads * 4));
+  const int64_t want = std::max<int64_t>(1, ceil_div(a.rows, kLuppThreads));  // one row per thread
   const int maxb = lupp_max_blocks(reinterpret_cast<const void*>(lupp_kernel), smem);
   int grid = static_cast<int>(std::min<int64_t>(want, std::min(maxb, kMaxLuppGrid)));
   LuppKernelArgs ka;
@@ -375,7 +915,7 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
   ka.cand = cand;
   ka.norm_part = norm_part;
   void* params[] = {&ka};
-  if (grid_used) *grid_used = grid;
+  if (grid_used) *grid_used = 1000000 + grid;
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lupp_kernel), dim3(grid), dim3(kLuppThreads),
                                      params, smem, st);
 }

@@ -122,9 +122,49 @@ __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, cons
   }
 }
 
+// One-warp variant for w <= 32: lane p holds row p of D in registers; the pivot row is
+// broadcast with shuffles (same operations and roundings as cross_lu_kernel).
+__global__ void cross_lu_warp_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
+                                     const int* __restrict__ d_w, double* __restrict__ lu, int64_t ldd,
+                                     const IterCtl* __restrict__ ctl) {
+  if (ctl) {
+    if (ctl->done) return;
+    Lk += ctl->r * ldl;
+    lu += ctl->r * ldd;
+  }
+  const int w = min(*d_w, 32);
+  const int lane = threadIdx.x;
+  double d[32];
+  const int64_t row = lane < w ? rows[lane] : 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) d[t] = (lane < w && t < w) ? Lk[row + t * ldl] : 0.0;
+#pragma unroll
+  for (int s = 0; s < 32; ++s) {
+    if (s < w) {
+      const double piv = __shfl_sync(0xffffffffu, d[s], s);
+      const bool below = lane > s && lane < w;
+      const double f = below ? __ddiv_rn(d[s], piv) : 0.0;
+#pragma unroll
+      for (int t = s + 1; t < 32; ++t) {
+        const double pt = __shfl_sync(0xffffffffu, d[t], s);
+        if (below && t < w) d[t] = __dsub_rn(d[t], __dmul_rn(f, pt));
+      }
+      if (below) d[s] = f;
+    }
+  }
+  if (lane < w) {
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      if (t < w) lu[lane + t * ldd] = d[t];
+  }
+}
+
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
                             double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl) {
-  cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
+  if (w_max <= 32)
+    cross_lu_warp_kernel<<<1, 32, 0, st>>>(Lk, ldl, d_rows, d_w, lu, ldd, ctl);
+  else
+    cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
   return cudaGetLastError();
 }
 
@@ -147,20 +187,63 @@ __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, 
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
   __syncthreads();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
-    double x[WMAX];
-#pragma unroll 4
-    for (int q = 0; q < w; ++q) x[q] = X[j + q * ldx];
-    for (int q = 1; q < w; ++q) {  // Lhat y = u
-      double v = x[q];
-      for (int p = 0; p < q; ++p) v = __dsub_rn(v, __dmul_rn(slu[q + p * w], x[p]));
-      x[q] = v;
+    double x[WMAX];  // fully unrolled: stays in registers
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q) x[q] = q < w ? X[j + q * ldx] : 0.0;
+#pragma unroll
+    for (int q = 1; q < WMAX; ++q) {  // Lhat y = u
+      if (q < w) {
+        double v = x[q];
+#pragma unroll
+        for (int p = 0; p < q; ++p) v = fma(-slu[q + p * w], x[p], v);
+        x[q] = v;
+      }
     }
-    for (int q = w - 1; q >= 0; --q) {  // Uhat x = y
-      double v = x[q];
-      for (int p = q + 1; p < w; ++p) v = __dsub_rn(v, __dmul_rn(slu[q + p * w], x[p]));
-      x[q] = __ddiv_rn(v, slu[q + q * w]);
+#pragma unroll
+    for (int q = WMAX - 1; q >= 0; --q) {  // Uhat x = y
+      if (q < w) {
+        double v = x[q];
+#pragma unroll
+        for (int p = q + 1; p < WMAX; ++p)
+          if (p < w) v = fma(-slu[q + p * w], x[p], v);
+        x[q] = v / slu[q + q * w];
+      }
     }
-    for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q];
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q)
+      if (q < w) out[j + q * ldo] = x[q];
+  }
+}
+
+// generic width (w > 64): same solves with x in local memory
+__global__ void rows_lu_solve_wide_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                          const double* __restrict__ lu, int64_t ldd, const int* __restrict__ d_w,
+                                          int w_max, double* __restrict__ out, int64_t ldo,
+                                          const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                          double* __restrict__ scratch) {
+  extern __shared__ double slu[];
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+  }
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+  __syncthreads();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+    double* x = scratch + j;  // column-strided per-row workspace (ld M)
+    for (int q = 0; q < w; ++q) x[q * M] = X[j + q * ldx];
+    for (int q = 1; q < w; ++q) {
+      double v = x[q * M];
+      for (int p = 0; p < q; ++p) v = fma(-slu[q + p * w], x[p * M], v);
+      x[q * M] = v;
+    }
+    for (int q = w - 1; q >= 0; --q) {
+      double v = x[q * M];
+      for (int p = q + 1; p < w; ++p) v = fma(-slu[q + p * w], x[p * M], v);
+      x[q * M] = v / slu[q + q * w];
+    }
+    for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q * M];
   }
 }
 
@@ -168,15 +251,26 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
                                  const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
                                  const IterCtl* ctl, int64_t out_off_per_r) {
   if (M <= 0 || w_max <= 0) return cudaSuccess;
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 8));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 16));
   const size_t smem = sizeof(double) * static_cast<size_t>(w_max) * w_max;
-  if (w_max <= 64) {
+  if (w_max <= 16) {
+    rows_lu_solve_kernel<16><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+  } else if (w_max <= 32) {
+    rows_lu_solve_kernel<32><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+  } else if (w_max <= 64) {
     rows_lu_solve_kernel<64><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
-  } else if (w_max <= 256) {
-    cudaFuncSetAttribute(rows_lu_solve_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    rows_lu_solve_kernel<256><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+  } else if (w_max <= 180) {
+    // X itself serves as the per-row workspace when solving in place is not requested:
+    // use the output buffer (each row's entries are private to its thread)
+    cudaFuncSetAttribute(rows_lu_solve_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    double* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * M * w_max, st);
+    if (e != cudaSuccess) return e;
+    rows_lu_solve_wide_kernel<<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl,
+                                                         out_off_per_r, scratch);
+    cudaFreeAsync(scratch, st);
   } else {
-    return cudaErrorInvalidValue;  // blocks wider than 256 are rejected by the driver
+    return cudaErrorInvalidValue;  // blocks wider than 180 exceed one CTA's shared memory for D
   }
   return cudaGetLastError();
 }

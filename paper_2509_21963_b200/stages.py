@@ -101,3 +101,21 @@ def time_sketch_kernel(a: torch.Tensor, b: int, kind: str = "gaussian", reps: in
                                                   _SKETCHES[kind], int(reps), _stream(a), C.byref(ms),
                                                   C.byref(ctas), C.byref(splits), C.byref(tma)))
     return {"ms": ms.value, "ctas": ctas.value, "splits": splits.value, "tma": bool(tma.value)}
+
+
+def time_lupp(rows: int, steps: int, reps: int = 10, force_path: int = 0):
+    """Mean microseconds per LUPP launch on a random rows x steps W (0 auto, 1 cluster, 2 grid, 3 global)."""
+    us = C.c_double()
+    used = C.c_int32()
+    _check(_capi.lib().itercur_time_lupp(int(rows), int(steps), int(reps), int(force_path),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(us),
+                                         C.byref(used)))
+    return {"us": us.value, "path": used.value}
+
+
+def time_gemm(M: int, N: int, K: int, reps: int = 10) -> float:
+    """Microseconds per launch of the tall-skinny DMMA GEMM (row-residual shape) on random data."""
+    us = C.c_double()
+    _check(_capi.lib().itercur_time_gemm(int(M), int(N), int(K), int(reps),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(us)))
+    return us.value
