@@ -237,6 +237,7 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
+            f = t = None  # release the previous run's factors before the next allocation
             f, t = engine.iterative_cur(handle, **run_cfg)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -257,6 +258,7 @@ def main():
     torch.cuda.synchronize()
     e2e_t = []
     for _ in range(max(1, args.steps)):
+        fe = te = None
         t0 = time.perf_counter()
         fe, te = engine.iterative_cur(hh, **run_cfg)
         _ = (fe.row_indices, fe.col_indices, te.rhos)  # already on the host

@@ -120,7 +120,7 @@ __device__ __forceinline__ double block_sum(double v, double* smem_scratch) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], double a0, double a1, double a2, double a3, double b0,
                                             double b1) {
-  asm volatile(
+  asm(  // not volatile: lets the scheduler interleave independent MMAs with loads
       "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])

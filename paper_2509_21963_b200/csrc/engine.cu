@@ -271,6 +271,7 @@ void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
   const int64_t maxcap = std::min(run->m, run->n) + run->bmax;
   cap = std::min(cap, maxcap);
   if (cap < need) cap = need;
+  cap = (cap + 1) & ~int64_t(1);  // even: 16-byte aligned gathered columns (lean GEMM loads)
   DevBuf<double> L2, R2, D2;
   L2.alloc(static_cast<size_t>(run->ldL) * cap);
   R2.alloc(static_cast<size_t>(run->ldR) * cap);
@@ -446,9 +447,59 @@ void run_iterative_cur(itercur_run* run) {
   run->dI.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dJ.alloc(std::max<int64_t>(max_rank + b, 1));
   run->capL = 0;
-  grow_factors(run, std::min<int64_t>(max_rank + b, std::max<int64_t>(kBatch * b, 256)), st);
+  {
+    // factor capacity: the whole max_rank + b up front when it is a small share of free HBM
+    // (no regrowth copies, one graph capture per run), else grow by doubling
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t full = max_rank + b;
+    const double full_bytes = 8.0 * static_cast<double>(run->ldL + run->ldR + b) * static_cast<double>(full);
+    const int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
+                              ? full
+                              : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
+    grow_factors(run, first, st);
+  }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
-  const int64_t y_parts = ts_gemm_grid_size(n, static_cast<int>(cp));
+  // the fused U-block kernel (GEMM2 + solves + downdate) when the shape qualifies
+  auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
+    TsGemmParams p;
+    p.M = n;
+    p.K = ldbg;
+    p.ctl = d_ctl;
+    p.k_from_r = 1;
+    p.N = B;
+    p.d_n = &slot->width;
+    p.A = run->Rt.p;
+    p.lda = run->ldR;
+    p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
+    p.bsk = 1;
+    p.bsn = ldbg;
+    p.base_mode = kBaseGatherRowsT;
+    p.src = A;
+    p.lds = lda;
+    p.idx = arr.row_idx;
+    p.alpha = -1.0;
+    p.out_mode = kOutNone;
+    p.lu = run->Dinv.p;
+    p.ldd = run->bmax;
+    p.rt = run->Rt.p;
+    p.ldr = run->ldR;
+    p.yg = ws.Yg.p;
+    p.ycp = static_cast<int>(cp);
+    p.y = ws.Y.p;
+    p.Wc = ws.Wc.p;
+    p.ldwc = ldn;
+    p.wc_rows = B;
+    p.norm_part = ws.part.p;
+    return p;
+  };
+  const bool fused_ub = getenv("ITERCUR_NO_FUSED_UBLOCK") == nullptr && [&] {
+    IterState* slot0 = reinterpret_cast<IterState*>(slots);
+    TsGemmParams p = ublock_params(run->capL, slot0, iter_arrays(slot0, B));
+    p.norm_part = reinterpret_cast<double*>(16);  // placeholder: allocated below
+    return ts_gemm_ublock_supported(p) && (run->capL & 1) == 0;
+  }();
+  const int64_t y_parts = fused_ub ? ts_gemm_ublock_parts(n) : ts_gemm_grid_size(n, static_cast<int>(cp));
   ws.part.alloc(std::max<int64_t>(y_parts, 1));
 
   // initial Wc = Y^T(:, 0:b)
@@ -468,20 +519,31 @@ void run_iterative_cur(itercur_run* run) {
     }
   } exec_guard{&graph_exec};
   int64_t k_host = 0, r_host = 0;
+  int64_t graph_batch_launches = 0;  // kernels per replayed batch graph
   int64_t ev_i = 2;
   std::vector<size_t> iter_events;
   bool done = false;
+  static const bool host_trace = getenv("ITERCUR_HOST_TRACE") != nullptr;
+  using hclock = std::chrono::steady_clock;
+  auto us_since = [](hclock::time_point t0) {
+    return std::chrono::duration<double, std::micro>(hclock::now() - t0).count();
+  };
   while (!done) {
+    const auto tb0 = hclock::now();
+    double t_grow = 0, t_capture = 0, t_launch = 0, t_sync = 0;
     // capacity for a whole batch
     const int64_t need = std::min(r_host + static_cast<int64_t>(kBatch) * b, max_rank + b);
     if (need > run->capL) {
       grow_factors(run, need, st);
       ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+      t_grow = us_since(tb0);
     }
     const int64_t ldbg = run->capL;
     // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
+    int64_t batch_launches = 0;
     auto enqueue_batch = [&]() {
+      batch_launches = 0;
       for (int j = 0; j < kBatch; ++j) {
         IterState* slot = reinterpret_cast<IterState*>(slots + slot_bytes * j);
         const IterArrays arr = iter_arrays(slot, B);
@@ -548,6 +610,7 @@ void run_iterative_cur(itercur_run* run) {
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
 
+        int row_lupp_path = 0;
         // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
         {
           LuppArgs la{};
@@ -569,14 +632,31 @@ void run_iterative_cur(itercur_run* run) {
           la.d_gen_k = &d_ctl->k;
           la.gen_base = gen_base;
           la.gen_which = 1;
-          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+          la.lu_out = run->Dinv.p;
+          la.lu_ld = run->bmax;
+          la.d_lu_r = &d_ctl->r;
+          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, &row_lupp_path));
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
 
         // (4) core step: LU of D_k = S_row(I_k, 0:w); U_k^T = A(I_k,:)^T - Rt^T L(I_k,:)^T;
         //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
-        CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
+        if (row_lupp_path >= 0)  // the cluster LUPP emitted the factors of D_k itself
+          CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
         CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        if (fused_ub) {
+          // Y(:, J_k) before the downdate, then one kernel: U_k^T, the solves against D_k,
+          // R~ rows, Y^T -= R~_k^T Y(:, J_k)^T, ||Y||^2 partials and Wc
+          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+          TsGemmParams p = ublock_params(ldbg, slot, arr);
+          CK(run_ts_gemm_ublock(p, st));
+          batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0);
+          if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
+          if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));  // downdate fused into the core step
+          CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p,
+                           y_parts, st));
+          continue;
+        }
         {
           TsGemmParams p;
           p.M = n;
@@ -633,9 +713,11 @@ void run_iterative_cur(itercur_run* run) {
         }
         CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
                          st));
+        batch_launches += 11 + (row_lupp_path >= 0 ? 1 : 0);
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
       }
     };
+    const auto tc0 = hclock::now();
     if (use_graph) {
       if (!graph_exec || graph_cap != run->capL) {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -654,15 +736,21 @@ void run_iterative_cur(itercur_run* run) {
         cudaGraphDestroy(g);
         CK(ie);
         graph_cap = run->capL;
+        t_capture = us_since(tc0);
       }
       CK(cudaGraphLaunch(graph_exec, st));
     } else {
       enqueue_batch();
     }
-    run->launches += 12 * kBatch;
+    t_launch = us_since(tc0) - t_capture;
+    if (use_graph && batch_launches == 0) batch_launches = graph_batch_launches;
+    graph_batch_launches = batch_launches;
+    run->launches += batch_launches;
     // one D2H read per batch: the batch's records + the loop control
     CK(cudaMemcpyAsync(ws.h_state, ws.state.p, slot_bytes * kBatch + sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+    const auto ts0 = hclock::now();
     CK(cudaStreamSynchronize(st));
+    t_sync = us_since(ts0);
     const IterCtl* hc = reinterpret_cast<const IterCtl*>(ws.h_state + slot_bytes * kBatch);
     for (int j = 0; j < kBatch; ++j) {
       const IterState* hs_ = reinterpret_cast<const IterState*>(ws.h_state + slot_bytes * j);
@@ -706,6 +794,10 @@ void run_iterative_cur(itercur_run* run) {
       ++k_host;
     }
     if (hc->r != r_host || hc->k != k_host) fail(ITERCUR_E_LOGIC, "device / host iteration bookkeeping diverged");
+    if (host_trace)
+      fprintf(stderr, "[itercur batch] r=%lld capL=%lld grow=%.0fus capture=%.0fus launch=%.0fus sync=%.0fus total=%.0fus\n",
+              static_cast<long long>(r_host), static_cast<long long>(run->capL), t_grow, t_capture, t_launch, t_sync,
+              us_since(tb0));
     run->r = r_host;
     rho = hc->rho;
     done = hc->done != 0;

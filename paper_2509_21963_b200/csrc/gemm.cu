@@ -16,6 +16,8 @@
 // staged with cp.async in a 4-deep ring. The CTA height (WARPS x 16 rows) is chosen per
 // call so that every launch spreads over several CTAs per SM (these GEMMs are HBM-bound:
 // intensity 2N/8 flop/B ~ the FP64 ridge), keeping all SMs streaming.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -36,6 +38,7 @@ struct GemmCfg {
   static constexpr int B_ELEMS = NT * 8 * kBPitch;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr int BYTES = kGemmStages * STAGE_ELEMS * 8;
+  static_assert(THREADS * NT * 4 <= kGemmStages * STAGE_ELEMS, "split-K reduction buffer must fit the ring");
 };
 
 __device__ __forceinline__ void cp_async_16(void* dst, const void* src, int src_bytes) {
@@ -102,69 +105,48 @@ __device__ __forceinline__ void gemm_load_stage(const TsGemmParams& p, double* s
   }
 }
 
+// Split-K cluster reduction (when gridDim.z > 1) and the fused epilogue: base + alpha * acc
+// written per out_mode, with the per-CTA sum of squares of C.
 template <int NT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
-  using Cfg = GemmCfg<NT, WARPS>;
-  extern __shared__ __align__(16) double gsm[];
+__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
+                                                int w);
+
+template <int NT, int WARPS, bool UB = false>
+__device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
+                                              int64_t q0, int nvalid, int splits) {
+  constexpr int THREADS = WARPS * 32;
   __shared__ double red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  if (p.ctl) {
-    if (p.ctl->done) return;
-    const int64_t r = p.ctl->r;
-    if (p.k_from_r) p.K = min(p.K, r);
-    p.A += r * p.a_off_per_r;
-    p.C0 += r * p.c0_off_per_r;
-  }
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * Cfg::BM;
-  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * (NT * 8);
-  int n_total = p.N;
-  if (p.d_n) n_total = min(n_total, *p.d_n);
-  int64_t nv = static_cast<int64_t>(n_total) - q0;
-  nv = nv < 0 ? 0 : (nv > NT * 8 ? NT * 8 : nv);
-  const int nvalid = static_cast<int>(nv);
-
-  double acc[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
-
-  int64_t K = p.K;
-  if (p.d_k) K = min(K, static_cast<int64_t>(*p.d_k));
-  const int nk = nvalid > 0 ? static_cast<int>(ceil_div(K, kGemmKT)) : 0;
-#pragma unroll
-  for (int s = 0; s < kGemmStages - 1; ++s) {
-    if (s < nk)
-      gemm_load_stage<NT, WARPS>(p, gsm + s * Cfg::STAGE_ELEMS, gsm + s * Cfg::STAGE_ELEMS + Cfg::A_ELEMS, i0,
-                                 static_cast<int64_t>(s) * kGemmKT, q0, nvalid, K);
-    cp_async_commit();
-  }
-  for (int it = 0; it < nk; ++it) {
-    cp_async_wait<kGemmStages - 2>();
+  if (splits > 1) {
+    // fixed-order reduction over the cluster: rank z publishes its fragments in its own
+    // shared memory, rank 0 adds ranks 1..S-1 in order (deterministic for a given S)
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
     __syncthreads();
-    const int nxt = it + kGemmStages - 1;
-    if (nxt < nk) {
-      double* base = gsm + (nxt % kGemmStages) * Cfg::STAGE_ELEMS;
-      gemm_load_stage<NT, WARPS>(p, base, base + Cfg::A_ELEMS, i0, static_cast<int64_t>(nxt) * kGemmKT, q0, nvalid,
-                                 K);
+    if (blockIdx.z != 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) gsm[(nt * 4 + v) * THREADS + threadIdx.x] = acc[nt][v];
     }
-    cp_async_commit();
-    const double* sA = gsm + (it % kGemmStages) * Cfg::STAGE_ELEMS;
-    const double* sB = sA + Cfg::A_ELEMS;
+    cl.sync();
+    if (blockIdx.z == 0) {
+      for (int src = 1; src < splits; ++src) {
+        const double* peer = cl.map_shared_rank(gsm, src);
 #pragma unroll
-    for (int kk = 0; kk < kGemmKT; kk += 8) {
-      const int rb = warp * 16 + 2 * g;
-      const double2 a01 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t) * Cfg::BM + rb);
-      const double2 a23 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t + 1) * Cfg::BM + rb);
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double2 b = *reinterpret_cast<const double2*>(sB + (nt * 8 + g) * kBPitch + kk + 2 * t);
-        dmma_16x8x8(acc[nt], a01.x, a01.y, a23.x, a23.y, b.x, b.y);
+          for (int v = 0; v < 4; ++v) acc[nt][v] += peer[(nt * 4 + v) * THREADS + threadIdx.x];
       }
     }
+    cl.sync();
+    if (blockIdx.z != 0) return;
   }
-  cp_async_wait<0>();
+  if constexpr (UB) {
+    ublock_epilogue<NT, WARPS>(p, acc, gsm, i0, nvalid);
+    return;
+  }
 
   // ---------------- epilogue: physical rows (2g, 2g+1), columns (2t, 2t+1) ----------
   double sq = 0.0;
@@ -213,17 +195,403 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
   }
 }
 
-// CTA height: the largest of {128, 64, 32} rows that still gives >= 4 CTAs per SM.
-static int gemm_warps(int64_t M) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("ITERCUR_GEMM_WARPS");  // tuning override: 2, 4 or 8
-    forced = e ? atoi(e) : 0;
+
+// Fused U-block epilogue (see gemm.h). The C fragment of a warp holds rows (2g, 2g+1) x
+// columns (nt*8 + 2t, +1): one row's w entries live in the 4 lanes of a quad, so the
+// substitutions broadcast x[p] inside the quad with shuffles. The solved fragment is
+// already the A operand of the downdate MMA (same physical k permutation as the main
+// loop: logical k t <-> column 2t, t+4 <-> 2t+1), so Y^T -= X Yg^T runs on DMMA without
+// leaving registers.
+template <int NT, int WARPS>
+__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
+                                                int w) {
+  constexpr int W = NT * 8;          // max block width
+  constexpr int NTY = NT + 1;        // n-tiles of the downdate (ycp <= 8 * (NT + 1))
+  constexpr int YP = ((W + 15) / 16) * 16 + 8;  // Yg^T pitch: 16-byte loads conflict-free
+  __shared__ double red[WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t r = p.ctl ? p.ctl->r : 0;
+  const double* lu = p.lu + r * p.ldd;
+  double* s_lu = gsm;            // [W][W]: s_lu[a + b*W] = LU(a, b)
+  double* s_yg = gsm + W * W;    // [NTY*8][YP]: s_yg[h*YP + q] = Yg(h, q) = Y(h, J_k[q])
+  __syncthreads();               // the ring is drained: reuse it
+  for (int e = threadIdx.x; e < W * W; e += WARPS * 32) {
+    const int a = e % W, b = e / W;
+    s_lu[e] = (a < w && b < w) ? lu[a + b * p.ldd] : 0.0;
   }
+  for (int e = threadIdx.x; e < NTY * 8 * W; e += WARPS * 32) {
+    const int h = e / W, q = e % W;
+    s_yg[h * YP + q] = (q < w && h < p.ycp) ? p.yg[h + q * p.ycp] : 0.0;
+  }
+  __syncthreads();
+
+  // u = base + alpha * acc (base = A(I_k[q], j)), zero outside the block
+  const int64_t r0 = i0 + warp * 16 + 2 * g;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq) {
+      const int q = nt * 8 + 2 * t + dq;
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int64_t j = r0 + dr;
+        double v = 0.0;
+        if (q < w && j < p.M) v = p.src[p.idx[q] + j * p.lds] + p.alpha * acc[nt][dr * 2 + dq];
+        acc[nt][dr * 2 + dq] = v;
+      }
+    }
+  const int qbase = lane & ~3;
+  // forward substitution with the unit-lower factor: x[q] -= L(q, p) x[p], p ascending
+#pragma unroll
+  for (int pp = 0; pp < W; ++pp) {
+    if (pp >= w) break;
+    const int ntp = pp / 8, tp = (pp % 8) / 2, dqp = pp % 2;
+    const double x0 = __shfl_sync(0xffffffffu, acc[ntp][dqp], qbase | tp);
+    const double x1 = __shfl_sync(0xffffffffu, acc[ntp][2 + dqp], qbase | tp);
+#pragma unroll
+    for (int nt = ntp; nt < NT; ++nt)
+#pragma unroll
+      for (int dq = 0; dq < 2; ++dq) {
+        const int q = nt * 8 + 2 * t + dq;
+        if (q > pp && q < w) {
+          const double l = s_lu[q + pp * W];
+          acc[nt][dq] = fma(-l, x0, acc[nt][dq]);
+          acc[nt][2 + dq] = fma(-l, x1, acc[nt][2 + dq]);
+        }
+      }
+  }
+  // back substitution with U: x[p] /= U(p, p), then x[q] -= U(q, p) x[p] for q < p
+#pragma unroll
+  for (int pp = W - 1; pp >= 0; --pp) {
+    if (pp >= w) continue;
+    const int ntp = pp / 8, tp = (pp % 8) / 2, dqp = pp % 2;
+    const double upp = s_lu[pp + pp * W];
+    const double x0 = __shfl_sync(0xffffffffu, acc[ntp][dqp], qbase | tp) / upp;
+    const double x1 = __shfl_sync(0xffffffffu, acc[ntp][2 + dqp], qbase | tp) / upp;
+    if (t == tp) {
+      acc[ntp][dqp] = x0;
+      acc[ntp][2 + dqp] = x1;
+    }
+#pragma unroll
+    for (int nt = 0; nt <= ntp; ++nt)
+#pragma unroll
+      for (int dq = 0; dq < 2; ++dq) {
+        const int q = nt * 8 + 2 * t + dq;
+        if (q < pp) {
+          const double u = s_lu[q + pp * W];
+          acc[nt][dq] = fma(-u, x0, acc[nt][dq]);
+          acc[nt][2 + dq] = fma(-u, x1, acc[nt][2 + dq]);
+        }
+      }
+  }
+  // R~ rows r .. r+w
+  double* rt = p.rt + r * p.ldr;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq) {
+      const int q = nt * 8 + 2 * t + dq;
+      if (q >= w) continue;
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int64_t j = r0 + dr;
+        if (j < p.M) rt[q * p.ldr + j] = acc[nt][dr * 2 + dq];
+      }
+    }
+  // downdate MMA: D(j, h) = sum_q x_j[q] Yg(h, q)
+  double yacc[NTY][4];
+#pragma unroll
+  for (int ny = 0; ny < NTY; ++ny)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) yacc[ny][v] = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+    for (int ny = 0; ny < NTY; ++ny) {
+      const double2 b = *reinterpret_cast<const double2*>(s_yg + (ny * 8 + g) * YP + nt * 8 + 2 * t);
+      dmma_16x8x8(yacc[ny], acc[nt][0], acc[nt][2], acc[nt][1], acc[nt][3], b.x, b.y);
+    }
+  }
+  double sq = 0.0;
+#pragma unroll
+  for (int ny = 0; ny < NTY; ++ny)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq) {
+      const int h = ny * 8 + 2 * t + dq;
+      if (h >= p.ycp) continue;
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int64_t j = r0 + dr;
+        if (j >= p.M) continue;
+        double* yp = p.y + j * p.ycp + h;
+        const double v = *yp + p.alpha * yacc[ny][dr * 2 + dq];
+        *yp = v;
+        sq = fma(v, v, sq);
+        if (h < p.wc_rows) p.Wc[j + h * p.ldwc] = v;
+      }
+    }
+  sq = warp_sum(sq);
+  if (lane == 0) red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < WARPS; ++q) s += red[q];
+    p.norm_part[blockIdx.x] = s;
+  }
+}
+
+static int ts_gemm_nt_host(int n) { return n <= 8 ? 1 : (n <= 16 ? 2 : (n <= 24 ? 3 : (n <= 32 ? 4 : 9))); }
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int NT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
+  using Cfg = GemmCfg<NT, WARPS>;
+  extern __shared__ __align__(16) double gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  if (p.ctl) {
+    if (p.ctl->done) return;
+    const int64_t r = p.ctl->r;
+    if (p.k_from_r) p.K = min(p.K, r);
+    p.A += r * p.a_off_per_r;
+    p.C0 += r * p.c0_off_per_r;
+  }
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * Cfg::BM;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * (NT * 8);
+  int n_total = p.N;
+  if (p.d_n) n_total = min(n_total, *p.d_n);
+  int64_t nv = static_cast<int64_t>(n_total) - q0;
+  nv = nv < 0 ? 0 : (nv > NT * 8 ? NT * 8 : nv);
+  const int nvalid = static_cast<int>(nv);
+
+  double acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
+
+  int64_t K = p.K;
+  if (p.d_k) K = min(K, static_cast<int64_t>(*p.d_k));
+  // split-K: the CTAs of one (1, 1, S) cluster share the output tile and take consecutive
+  // ranges of k-stages; partial accumulators are summed in rank order through DSMEM below.
+  const int nk_all = nvalid > 0 ? static_cast<int>(ceil_div(K, kGemmKT)) : 0;
+  const int splits = static_cast<int>(gridDim.z);
+  const int per_split = (nk_all + splits - 1) / splits;
+  const int kb = static_cast<int>(blockIdx.z) * per_split;
+  const int nk = max(0, min(nk_all - kb, per_split));
+  const int64_t kbase = static_cast<int64_t>(kb) * kGemmKT;
+#pragma unroll
+  for (int s = 0; s < kGemmStages - 1; ++s) {
+    if (s < nk)
+      gemm_load_stage<NT, WARPS>(p, gsm + s * Cfg::STAGE_ELEMS, gsm + s * Cfg::STAGE_ELEMS + Cfg::A_ELEMS, i0,
+                                 kbase + static_cast<int64_t>(s) * kGemmKT, q0, nvalid, K);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<kGemmStages - 2>();
+    __syncthreads();
+    const int nxt = it + kGemmStages - 1;
+    if (nxt < nk) {
+      double* base = gsm + (nxt % kGemmStages) * Cfg::STAGE_ELEMS;
+      gemm_load_stage<NT, WARPS>(p, base, base + Cfg::A_ELEMS, i0, kbase + static_cast<int64_t>(nxt) * kGemmKT, q0,
+                                 nvalid, K);
+    }
+    cp_async_commit();
+    const double* sA = gsm + (it % kGemmStages) * Cfg::STAGE_ELEMS;
+    const double* sB = sA + Cfg::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < kGemmKT; kk += 8) {
+      const int rb = warp * 16 + 2 * g;
+      const double2 a01 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t) * Cfg::BM + rb);
+      const double2 a23 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t + 1) * Cfg::BM + rb);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 b = *reinterpret_cast<const double2*>(sB + (nt * 8 + g) * kBPitch + kk + 2 * t);
+        dmma_16x8x8(acc[nt], a01.x, a01.y, a23.x, a23.y, b.x, b.y);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  gemm_epilogue<NT, WARPS>(p, acc, gsm, i0, q0, nvalid, splits);
+}
+
+
+// ---------------------------------------------------------------------------------
+// Lean main loop for the hot shapes (row residual, U block, verification): Aop 16-byte
+// aligned with even lda, B k-contiguous (bsk == 1, even bsn). Every thread's cp.async
+// sources are fixed offsets from two per-thread base pointers, so a stage costs a handful
+// of instructions per thread (the generic loader spends ~10x more on index math). Padded
+// shared rows make every 16-byte fragment load conflict-free:
+//   A stage [KT][BM + 2]: lane (g, t) reads chunk 2t*(BM+2)/2 + g = t*(BM+2) + g -> 8 banks
+//   B stage [NT*8][KT + 8]: row pitch (KT+8)/2 chunks = 4 (mod 8) separates g from g+1
+// ---------------------------------------------------------------------------------
+template <int NT, int WARPS, int KT, int STAGES>
+struct LeanCfg {
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int BM = WARPS * 16;
+  static constexpr int AP = BM + 2;  // A row pitch (doubles)
+  static constexpr int BP = KT + 8;  // B row pitch (doubles)
+  static constexpr int A_ELEMS = KT * AP;
+  static constexpr int B_ELEMS = NT * 8 * BP;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int BYTES = STAGES * STAGE_ELEMS * 8;
+  static constexpr int A_KSTEP = THREADS / (BM / 2);  // k rows covered per pass (= 4)
+  static constexpr int A_PER = KT / A_KSTEP;
+  static constexpr int B_QSTEP = THREADS / (KT / 2);  // q columns covered per pass
+  static constexpr int B_PER = (NT * 8 + B_QSTEP - 1) / B_QSTEP;
+  static_assert(THREADS % (BM / 2) == 0 && KT % A_KSTEP == 0, "A tiling");
+  static_assert(THREADS % (KT / 2) == 0, "B tiling");
+  static_assert(THREADS * NT * 4 <= STAGES * STAGE_ELEMS, "split-K reduction buffer must fit the ring");
+};
+
+template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
+__global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p) {
+  using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
+  extern __shared__ __align__(16) double gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  if (p.ctl) {
+    if (p.ctl->done) return;
+    const int64_t r = p.ctl->r;
+    if (p.k_from_r) p.K = min(p.K, r);
+    p.A += r * p.a_off_per_r;
+    p.C0 += r * p.c0_off_per_r;
+  }
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * Cfg::BM;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * (NT * 8);
+  int n_total = p.N;
+  if (p.d_n) n_total = min(n_total, *p.d_n);
+  int64_t nv = static_cast<int64_t>(n_total) - q0;
+  nv = nv < 0 ? 0 : (nv > NT * 8 ? NT * 8 : nv);
+  const int nvalid = static_cast<int>(nv);
+  int64_t K = p.K;
+  if (p.d_k) K = min(K, static_cast<int64_t>(*p.d_k));
+
+  const int nk_all = nvalid > 0 ? static_cast<int>(ceil_div(K, KT)) : 0;
+  const int splits = static_cast<int>(gridDim.z);
+  const int per_split = (nk_all + splits - 1) / splits;
+  const int kb = static_cast<int>(blockIdx.z) * per_split;
+  const int nk = max(0, min(nk_all - kb, per_split));
+
+  // per-thread load descriptors
+  const int a_il = (threadIdx.x % (Cfg::BM / 2)) * 2;
+  const int a_kl0 = threadIdx.x / (Cfg::BM / 2);
+  const int64_t a_row = i0 + a_il;
+  const int a_bytes = a_row + 1 < p.M ? 16 : (a_row < p.M ? 8 : 0);
+  const double* a_src = p.A + (a_row < p.M ? a_row : 0) + static_cast<int64_t>(a_kl0) * p.lda;
+  const int64_t a_kstride = static_cast<int64_t>(Cfg::A_KSTEP) * p.lda;
+  const uint32_t a_dst = smem_u32(gsm) + static_cast<uint32_t>((a_kl0 * Cfg::AP + a_il) * 8);
+  const int b_kl = (threadIdx.x % (KT / 2)) * 2;
+  const int b_ql0 = threadIdx.x / (KT / 2);
+  const double* b_src = p.B + b_kl + (q0 + b_ql0) * p.bsn;
+  const int64_t b_qstride = static_cast<int64_t>(Cfg::B_QSTEP) * p.bsn;
+  const uint32_t b_dst = smem_u32(gsm) + static_cast<uint32_t>((Cfg::A_ELEMS + b_ql0 * Cfg::BP + b_kl) * 8);
+
+  auto load = [&](int stage_slot, int kstage) {
+    const int64_t k0 = static_cast<int64_t>(kstage) * KT;
+    const bool full = k0 + KT <= K;
+    const uint32_t so = static_cast<uint32_t>(stage_slot * Cfg::STAGE_ELEMS * 8);
+    const double* as = a_src + k0 * p.lda;
+#pragma unroll
+    for (int j = 0; j < Cfg::A_PER; ++j) {
+      const int kl = a_kl0 + j * Cfg::A_KSTEP;
+      const int bytes = (full || k0 + kl < K) ? a_bytes : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                       a_dst + so + static_cast<uint32_t>(j * Cfg::A_KSTEP * Cfg::AP * 8)),
+                   "l"(as + j * a_kstride), "r"(bytes)
+                   : "memory");
+    }
+    const double* bs = b_src + k0;
+#pragma unroll
+    for (int j = 0; j < Cfg::B_PER; ++j) {
+      const int ql = b_ql0 + j * Cfg::B_QSTEP;
+      if (Cfg::B_PER * Cfg::B_QSTEP == NT * 8 || ql < NT * 8) {
+        const int64_t k = k0 + b_kl;
+        const int bytes = ql < nvalid ? ((full || k + 1 < K) ? 16 : (k < K ? 8 : 0)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                         b_dst + so + static_cast<uint32_t>(j * Cfg::B_QSTEP * Cfg::BP * 8)),
+                     "l"(bytes ? bs + j * b_qstride : p.B), "r"(bytes)
+                     : "memory");
+      }
+    }
+  };
+
+  double acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load(s, kb + s);
+    cp_async_commit();
+  }
+  const int rb = warp * 16 + 2 * g;
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = it + STAGES - 1;
+    if (nxt < nk) load(nxt % STAGES, kb + nxt);
+    cp_async_commit();
+    const double* sA = gsm + (it % STAGES) * Cfg::STAGE_ELEMS;
+    const double* sB = sA + Cfg::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < KT; kk += 8) {
+      const double2 a01 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t) * Cfg::AP + rb);
+      const double2 a23 = *reinterpret_cast<const double2*>(sA + (kk + 2 * t + 1) * Cfg::AP + rb);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 b = *reinterpret_cast<const double2*>(sB + (nt * 8 + g) * Cfg::BP + kk + 2 * t);
+        dmma_16x8x8(acc[nt], a01.x, a01.y, a23.x, a23.y, b.x, b.y);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  gemm_epilogue<NT, WARPS, UB>(p, acc, gsm, i0, q0, nvalid, splits);
+}
+
+// CTA height: 64 rows (4 warps) unless overridden; measured best across the row-residual,
+// U-block and downdate shapes (tools/bench_gemm.py).
+static int gemm_warps(int64_t) {
+  static const int forced = env_int("ITERCUR_GEMM_WARPS", 0);  // tuning override: 2, 4 or 8
   if (forced == 2 || forced == 4 || forced == 8) return forced;
-  if (ceil_div(M, 128) >= 4 * kNumSMs) return 8;
-  if (ceil_div(M, 64) >= 4 * kNumSMs) return 4;
-  return 2;
+  return 4;
+}
+
+// split-K factor: enough CTAs for ~4 resident per SM, each split keeping >= 4 k-stages.
+static int gemm_splits(int64_t tiles, int64_t K, int kt) {
+  static const int forced = env_int("ITERCUR_GEMM_SPLITS", 0);
+  const int64_t stages = ceil_div(K, kt);
+  int s = forced > 0 ? forced : static_cast<int>(ceil_div(4 * kNumSMs, std::max<int64_t>(tiles, 1)));
+  s = static_cast<int>(std::min<int64_t>(s, std::max<int64_t>(1, stages / 4)));
+  return std::max(1, std::min(s, 8));
+}
+
+template <typename Kern>
+static cudaError_t launch_split(Kern kern, dim3 grid, int threads, int bytes, const TsGemmParams& p, cudaStream_t st) {
+  if (grid.z == 1) {
+    kern<<<grid, threads, bytes, st>>>(p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = grid.z;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 template <int NT, int WARPS>
@@ -237,16 +605,77 @@ static cudaError_t launch_cfg(const TsGemmParams& p, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, Cfg::BM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
-  ts_gemm_kernel<NT, WARPS><<<grid, Cfg::THREADS, Cfg::BYTES, st>>>(p);
-  return cudaGetLastError();
+  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.K, kGemmKT));
+  return launch_split(ts_gemm_kernel<NT, WARPS>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
+}
+
+template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
+static cudaError_t launch_lean(const TsGemmParams& p, cudaStream_t st) {
+  using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
+  static_assert(!UB || (NT * 8 * NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
+                        STAGES * Cfg::STAGE_ELEMS), "U-block epilogue buffers must fit the ring");
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(p.M, Cfg::BM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
+  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.K, KT));
+  return launch_split(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
+}
+
+// lean main loop eligibility: 16-byte aligned A rows pairs (even lda and offsets), k-contiguous B
+static bool lean_ok(const TsGemmParams& p) {
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return p.bsk == 1 && !p.b_idx && (p.bsn & 1) == 0 && al16(p.B) && al16(p.A) && (p.lda & 1) == 0 &&
+         (p.a_off_per_r & 1) == 0;
 }
 
 template <int NT>
 static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
+  // 0 off, 1: KT16 x4, 2: KT32 x3, 3: KT32 x4; default by shape (tools/bench_gemm.py on B200:
+  // the lean loop wins for N <= 32, KT32 x3 for the taller M, the generic loop for wide N)
+  static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
+  const int lean = forced >= 0 ? forced : (NT > 4 ? 0 : (p.M >= 16000 ? 2 : 1));
+  if (lean > 0 && lean_ok(p) && gemm_warps(p.M) == 4) {
+    switch (lean) {
+      case 1: return launch_lean<NT, 4, 16, 4>(p, st);
+      case 2: return launch_lean<NT, 4, 32, 3>(p, st);
+      default: return launch_lean<NT, 4, 32, 4>(p, st);
+    }
+  }
   switch (gemm_warps(p.M)) {
     case 8: return launch_cfg<NT, 8>(p, st);
     case 4: return launch_cfg<NT, 4>(p, st);
     default: return launch_cfg<NT, 2>(p, st);
+  }
+}
+
+bool ts_gemm_ublock_supported(const TsGemmParams& p) {
+  return p.N >= 1 && p.N <= 32 && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) && p.base_mode == kBaseGatherRowsT &&
+         p.norm_part && p.y && p.rt && p.lu && p.yg && p.ctl;
+}
+
+int64_t ts_gemm_ublock_parts(int64_t M) { return ceil_div(M, 64); }
+
+template <int NT>
+static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
+  static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
+  const int lean = forced > 0 ? forced : (p.M >= 16000 ? 2 : 1);
+  if (lean == 2) return launch_lean<NT, 4, 32, 3, true>(p, st);
+  return launch_lean<NT, 4, 16, 4, true>(p, st);
+}
+
+cudaError_t run_ts_gemm_ublock(const TsGemmParams& p, cudaStream_t st) {
+  if (!ts_gemm_ublock_supported(p)) return cudaErrorNotSupported;
+  if (p.M <= 0) return cudaSuccess;
+  switch (ts_gemm_nt_host(p.N)) {
+    case 1: return launch_ublock_nt<1>(p, st);
+    case 2: return launch_ublock_nt<2>(p, st);
+    case 3: return launch_ublock_nt<3>(p, st);
+    default: return launch_ublock_nt<4>(p, st);
   }
 }
 

@@ -54,9 +54,26 @@ struct TsGemmParams {
   int k_from_r = 0;
   int64_t a_off_per_r = 0;
   int64_t c0_off_per_r = 0;
+  // fused U-block epilogue (run_ts_gemm_ublock; N = w <= 32): C = U_k^T rows, then per row j
+  //   x_j = D_k^{-1} u_j   (LU solves with the factors at lu + r*ldd, w x w, pitch ldd)
+  //   R~(r+q, j) = x_j[q]  (rt[(r+q)*ldr + j])
+  //   Y^T(j, :) -= x_j^T Y(:, J_k)^T   (y row-major n x ycp, yg[h + q*ycp] = Y(h, J_k[q]))
+  //   Wc(j, h) = Y^T(j, h) for h < wc_rows, norm_part = per-CTA sum of squares of the new Y^T
+  const double* lu = nullptr;
+  int64_t ldd = 0;
+  double* rt = nullptr;
+  int64_t ldr = 0;
+  const double* yg = nullptr;
+  int ycp = 0;
+  double* y = nullptr;
 };
 
 cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st);
 int64_t ts_gemm_grid_size(int64_t M, int N);
+// the fused U-block GEMM: returns cudaErrorNotSupported when the shape / layout does not
+// qualify (the caller then runs GEMM + rows_lu_solve + downdate GEMM separately)
+bool ts_gemm_ublock_supported(const TsGemmParams& p);
+cudaError_t run_ts_gemm_ublock(const TsGemmParams& p, cudaStream_t st);
+int64_t ts_gemm_ublock_parts(int64_t M);
 
 }  // namespace itercur_b200

@@ -67,6 +67,12 @@ struct LuppArgs {
   const int64_t* d_gen_k = nullptr;
   uint32_t gen_base = 0;
   int gen_which = 0;
+  // optional (cluster path): emit the LU factors of the pivot rows, row s of the block =
+  // (multipliers of steps < s, eliminated entries from column s on) — exactly the
+  // factorisation of W(I, 0:count) in pivot order; written at lu_out + (*d_lu_r) * lu_ld
+  double* lu_out = nullptr;
+  int64_t lu_ld = 0;
+  const int64_t* d_lu_r = nullptr;
 };
 size_t lupp_scratch_bytes(int b);
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used);

@@ -675,6 +675,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
   int count = 0;
   double first = 0.0;
   long long* dbg = (ka.dbg && me == 0) ? ka.dbg : nullptr;
+  double* lu_blk = a.lu_out ? a.lu_out + (a.d_lu_r ? *a.d_lu_r : 0) * a.lu_ld : nullptr;
   for (int s = 0; s < steps; ++s) {
     if (dbg && threadIdx.x == 32) dbg[s * 8 + 0] = clock64();
     const WCand best = s_best[s & 1];
@@ -688,6 +689,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
       a.d_idx[s] = best.idx;
       a.d_best[s] = best_mag;
       a.d_second[s] = best.second;
+    }
+    if (lu_blk && best.idx >= r0 && best.idx < r0 + nr) {
+      // the pivot row is fully eliminated through step s-1: (multipliers, U(s, s:)) = LU row s
+      const int lr = static_cast<int>(best.idx - r0);
+      for (int t = threadIdx.x; t < steps; t += kClusterThreads) lu_blk[s + t * a.lu_ld] = Ws[t * Rb + lr];
     }
     ++count;
     if (s + 1 >= steps) break;
@@ -703,6 +709,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
         }
         const double f = __ddiv_rn(Ws[s * Rb + rr], pivot);
         F[rr] = f;
+        if (lu_blk) Ws[s * Rb + rr] = f;  // column s is dead for this row: keep its multiplier
         const double v = __dsub_rn(Ws[(s + 1) * Rb + rr], __dmul_rn(f, P[s + 1]));
         Ws[(s + 1) * Rb + rr] = v;
         mine = wcand_merge_row(mine, fabs(v), static_cast<int32_t>(r0 + rr));
