@@ -524,6 +524,10 @@ void run_iterative_cur(itercur_run* run) {
   std::vector<size_t> iter_events;
   bool done = false;
   static const bool host_trace = getenv("ITERCUR_HOST_TRACE") != nullptr;
+  if (host_trace)
+    fprintf(stderr, "[itercur setup] %.0fus before the iteration loop (sketch %.0fus)\n",
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count(),
+            run->sketch_s * 1e6);
   using hclock = std::chrono::steady_clock;
   auto us_since = [](hclock::time_point t0) {
     return std::chrono::duration<double, std::micro>(hclock::now() - t0).count();
@@ -816,6 +820,7 @@ void run_iterative_cur(itercur_run* run) {
   }
   run->final_rho = rho;
   run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (host_trace) fprintf(stderr, "[itercur done] total %.0fus\n", run->total_s * 1e6);
 }
 
 // ------------------------------------------------------------------ exports
@@ -1336,17 +1341,27 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
     set_lupp_force_path(0);
     if (getenv("ITERCUR_LUPP_TRACE")) {  // one traced launch: per-step phase cycles of CTA 0
       DevBuf<long long> tr;
-      tr.alloc(static_cast<size_t>(steps) * 8);
-      CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * 8, st));
+      tr.alloc(static_cast<size_t>(steps) * 16);
+      CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * 16, st));
       set_lupp_force_path(force_path);
       set_lupp_debug_trace(tr.p);
       CK(cudaMemcpyAsync(W.p, W0.p, sizeof(double) * ldw * steps, cudaMemcpyDeviceToDevice, st));
       CK(run_lupp_with_scratch(la, scratch.p, st, &used));
       set_lupp_debug_trace(nullptr);
       set_lupp_force_path(0);
-      std::vector<long long> h(static_cast<size_t>(steps) * 8);
-      CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 8, cudaMemcpyDeviceToHost, st));
+      std::vector<long long> h(static_cast<size_t>(steps) * 16);
+      CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 16, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      if (used <= -100) {  // cluster v2 layout (16 slots per step)
+        for (int q = 0; q + 1 < steps; ++q) {
+          const long long* v = h.data() + q * 16;
+          fprintf(stderr,
+                  "lupp v2 step %d: [t32] eager %lld wcand %lld | [t0] B1-released %lld read-wc %lld argmax %lld vals "
+                  "%lld st.async %lld wait %lld read-in %lld argmax %lld tail %lld | B2-released(t32) %lld | step %lld\n",
+                  q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[10] - v[3], v[11] - v[10], v[12] - v[11], v[4] - v[12],
+                  v[5] - v[4], v[13] - v[5], v[14] - v[13], v[15] - v[14], v[8] - v[15], v[16] - v[0]);
+        }
+      } else
       for (int q = 0; q + 1 < steps; ++q) {
         const long long* v = h.data() + q * 8;
         fprintf(stderr,

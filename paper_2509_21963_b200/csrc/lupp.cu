@@ -57,16 +57,33 @@ __device__ __forceinline__ uint64_t mag_key(double mag) {
 __device__ __forceinline__ double key_mag(uint64_t key) {
   return key ? __longlong_as_double(static_cast<long long>(key - 1ull)) : -1.0;
 }
+#ifdef ITERCUR_ARGMAX_SHFL
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int warp_min_i32(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+#else
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
   const unsigned hi = static_cast<unsigned>(v >> 32), lo = static_cast<unsigned>(v);
   const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
   const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
   return (static_cast<uint64_t>(mhi) << 32) | mlo;
 }
+__device__ __forceinline__ int warp_min_i32(int v) { return __reduce_min_sync(0xffffffffu, v); }
+#endif
 __device__ __forceinline__ WCand warp_argmax(const WCand& c) {
   const uint64_t best = warp_max_u64(c.key);
   const int32_t tie_idx = (c.key == best && best != 0) ? c.idx : 0x7fffffff;
-  const int32_t widx = __reduce_min_sync(0xffffffffu, tie_idx);
+  const int32_t widx = warp_min_i32(tie_idx);
   const bool winner = best != 0 && c.key == best && c.idx == widx;
   // runner-up: the winner lane offers its own second, every other lane its best
   const double offer = winner ? c.second : key_mag(c.key);
@@ -496,16 +513,19 @@ __device__ __forceinline__ uint32_t map_cluster_addr(uint32_t local_addr, int ra
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAITC_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
 }
 
 __device__ __forceinline__ void st_release_cluster_u64(uint64_t* p, uint64_t v) {
@@ -751,7 +771,475 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
   cluster.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
+
 static long long* g_lupp_dbg = nullptr;
+
+// ---------------------------------------------------------------------------------
+// Cluster LUPP, v2 (the default cluster path). Same pivots and arithmetic as above, with a
+// much shorter per-step critical path:
+//  * division by the pivot through its correctly rounded reciprocal and one FMA correction
+//    (Markstein): q = RN(a*y), r = fma(-q, p, a), RN(q + r*y) equals RN(a/p) when
+//    y = RN(1/p) and nothing under/overflows; outside a safe exponent window it falls back
+//    to IEEE division (tools/microbench/div_check.cu: 7.6e10 pairs, 0 differences). The
+//    reciprocal is formed once per step by the exchange warp, off the row loop;
+//  * a thread's rows (at most RMAX) are handled together; their liveness is a register
+//    bitmask, indices are 32-bit;
+//  * after the CTA barrier every warp w < CL redundantly reduces the CTA's warp candidates
+//    and pushes the CTA slot (|v|, runner-up, row, then the candidate's row tail) into CTA
+//    w's inbox with st.async — 16 pushes in parallel instead of one warp doing all of them —
+//    and the exchange warp reduces its own inbox (all reads local).
+// The inbox is double-buffered by step parity; a CTA writes a parity again only after an
+// exchange that needed every CTA's next push, which each CTA issues after it finished
+// reading the earlier one.
+// ---------------------------------------------------------------------------------
+struct LuppClusterV2Args {
+  LuppArgs a;
+  long long* dbg;  // optional per-step clock64() trace of CTA 0 (16 slots per step)
+  int skeleton;    // benchmarking only: 1 = skip the row eliminations (exchange cost alone)
+  int rows_per_cta;
+  int smax;        // column capacity of the buffers (cols_max)
+  int slot;        // doubles per inbox slot: 4 + smax rounded up to even
+};
+
+// clock64() that issues only after `dep` is available (trace stamps after barriers / loads)
+__device__ __forceinline__ long long clock_after(unsigned long long dep) {
+  long long c;
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.u64 p, %1, 0x5a5a5a5a5a5a5a5a;\n@p mov.u64 %0, %%clock64;\n@!p mov.u64 %0, "
+      "%%clock64;\n}\n"
+      : "=l"(c)
+      : "l"(dep)
+      : "memory");
+  return c;
+}
+
+// out-of-line IEEE division: the rare fallback stays out of the (instruction-cache
+// sensitive) step loop
+__device__ __noinline__ double ieee_div(double a, double p) { return __ddiv_rn(a, p); }
+
+__device__ __forceinline__ double div_by_pivot(double a, double p, double y, bool p_ok) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = __fma_rn(-q0, p, a);
+  const double q = __fma_rn(r, y, q0);
+  const double aq = fabs(q), aa = fabs(a);
+  if (p_ok && aq > 0x1p-968 && aq < 0x1p968 && aa > 0x1p-968 && aa < 0x1p968) return q;
+  return ieee_div(a, p);
+}
+
+template <int THREADS, int RMAX>
+__global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppClusterV2Args ka) {
+  // warp roles by scheduler: warps 0, 4, 8, .. (all on sub-partition 0) are service warps
+  // (exchange pushes; warp 0 also reduces the inbox), the others own rows. Keeping the row
+  // work off sub-partition 0 leaves the latency-critical exchange its issue slots.
+  constexpr int kWarps = THREADS / 32;
+  constexpr int kSvc = kWarps / 4;
+  constexpr int kCompWarps = kWarps - kSvc;
+  constexpr int kComp = kCompWarps * 32;
+  constexpr int kPanel = 4;  // rank-1 updates of later columns are applied kPanel steps at a time
+  cg::cluster_group cluster = cg::this_cluster();
+  const LuppArgs& a = ka.a;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ WCand wc[kCompWarps];
+  __shared__ double sred[kWarps];
+  __shared__ double s_norm;
+  __shared__ WCand s_best[2];
+  __shared__ double s_rcp[2];
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int CL = static_cast<int>(cluster.num_blocks());
+  const int me = static_cast<int>(cluster.block_rank());
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool svc = (warp & 3) == 0;
+  const int cw = warp - (warp >> 2) - 1;  // compute-warp index (valid when !svc)
+  const int ctid = cw * 32 + lane;
+  const int Rb = ka.rows_per_cta;
+  const int smax = ka.smax, SL = ka.slot;
+  const int r0 = me * Rb;
+  const int nr = max(0, min(Rb, static_cast<int>(a.rows) - r0));
+  int steps = a.cols_max;
+  if (a.d_steps) steps = min(steps, *a.d_steps);
+  if (steps <= 0) {
+    if (me == 0 && threadIdx.x == 0) {
+      *a.d_count = 0;
+      if (a.d_width_out) *a.d_width_out = 0;
+    }
+    return;  // uniform across the cluster
+  }
+  double* Ws = sm;                                                     // [smax][Rb]
+  double* U = Ws + static_cast<size_t>(smax) * Rb;                     // [smax][smax] pivot rows
+  double* wtail = U + smax * smax;                                     // [kCompWarps][smax]
+  double* inbox = reinterpret_cast<double*>(                           // [2][16][SL]
+      (reinterpret_cast<uintptr_t>(wtail + kCompWarps * smax) + 15) & ~uintptr_t(15));
+
+  uint32_t live = 0;  // bit k: row ctid + k*kComp is a candidate
+  // slab load: every element an independent 8-byte cp.async, one wait for all of them
+  for (int t = 0; t < steps; ++t)
+    for (int r = threadIdx.x; r < nr; r += THREADS)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(Ws + t * Rb + r)),
+                   "l"(a.W + (r0 + r) + t * a.ldw)
+                   : "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  if (!svc) {
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) {
+      const int rr = ctid + k * kComp;
+      if (rr < nr) {
+        const uint8_t mk = a.mask[r0 + rr];
+        if (!(mk == 1 || mk == a.epoch)) live |= 1u << k;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_barrier_init();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  double nsq;
+  if (a.d_norm_sq) {
+    nsq = *a.d_norm_sq;
+    cluster.sync();  // every CTA's mbarriers are initialised before anyone pushes to them
+  } else {
+    double sq = 0.0;
+    for (int t = 0; t < steps; ++t)
+      for (int r = threadIdx.x; r < nr; r += THREADS) {
+        const double v = Ws[t * Rb + r];
+        sq = fma(v, v, sq);
+      }
+    const double b = block_sum<THREADS>(sq, sred);
+    if (threadIdx.x == 0) s_norm = b;
+    cluster.sync();
+    nsq = 0.0;
+    for (int q = 0; q < CL; ++q) nsq += *cluster.map_shared_rank(&s_norm, q);
+  }
+  const double abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(nsq);
+  double* lu_blk = a.lu_out ? a.lu_out + (a.d_lu_r ? *a.d_lu_r : 0) * a.lu_ld : nullptr;
+  long long* dbg = (ka.dbg && me == 0) ? ka.dbg : nullptr;
+
+  // bytes one CTA pushes per step (header + pair-aligned tail from column col)
+  auto push_pairs = [&](int col) { return 2 + (steps - (col & ~1) + 1) / 2; };
+  // service warp sv: CTA candidate -> slot `me` of the inboxes of CTAs sv, sv + kSvc, ..
+  auto push = [&](int col) {
+    const int par = col & 1;
+    const WCand c = lane < kCompWarps ? wc[lane] : WCand{0ull, -1, -1.0};
+    const long long k10 = dbg ? clock_after(c.key) : 0;
+    const WCand bc = warp_argmax(c);
+    const long long k11 = dbg ? clock_after(bc.key) : 0;
+    if (dbg && threadIdx.x == 0 && col > 0) {
+      dbg[(col - 1) * 16 + 10] = k10;
+      dbg[(col - 1) * 16 + 11] = k11;
+    }
+    const int npairs = push_pairs(col);
+    if (lane < npairs) {
+      double v0 = 0.0, v1 = 0.0;
+      if (lane == 0) {
+        v0 = bc.key ? key_mag(bc.key) : -1.0;
+        v1 = bc.second;
+      } else if (lane == 1) {
+        v0 = __longlong_as_double(bc.key ? static_cast<long long>(bc.idx) : -1ll);
+      } else if (bc.key) {
+        const int lr = bc.idx - r0;
+        const double* wt = wtail + ((lr % kComp) / 32) * smax;
+        const int t0 = (col & ~1) + 2 * (lane - 2);
+        v0 = (t0 >= col && t0 < steps) ? wt[t0] : 0.0;
+        v1 = (t0 + 1 < steps) ? wt[t0 + 1] : 0.0;
+      }
+      const int t0 = (col & ~1) + 2 * (lane - 2);
+      const int off = lane < 2 ? 2 * lane : 4 + t0;
+      const uint32_t slot = smem_u32(inbox + (par * 16 + me) * SL + off);
+      const uint32_t bar = smem_u32(&mbar[par]);
+      if (dbg && threadIdx.x == 0 && col > 0)
+        dbg[(col - 1) * 16 + 12] = clock_after(__double_as_longlong(v0) ^ __double_as_longlong(v1));
+      for (int dst = warp >> 2; dst < CL; dst += kSvc)
+        st_async_v2(map_cluster_addr(slot, dst), v0, v1, map_cluster_addr(bar, dst));
+    }
+  };
+  // warp 0: wait for the CL slots of column col, reduce them in fixed order, copy the
+  // winner's tail, form the next reciprocal
+  auto exchange = [&](int col) {
+    const int par = col & 1;
+    if (lane == 0) mbar_wait_cluster(&mbar[par], static_cast<uint32_t>((col >> 1) & 1));
+    __syncwarp();  // one poller; the warp leaves the wait converged
+    const long long k5 = dbg ? clock64() : 0;
+    WCand g{0ull, -1, -1.0};
+    if (lane < CL) {
+      const double* rs = inbox + (par * 16 + lane) * SL;
+      const double mag = rs[0];
+      if (mag >= 0.0) {
+        g.key = mag_key(mag);
+        g.idx = static_cast<int32_t>(__double_as_longlong(rs[2]));
+        g.second = rs[1];
+      }
+    }
+    const long long k13 = dbg ? clock_after(g.key) : 0;
+    WCand best = warp_argmax(g);
+    const long long k14 = dbg ? clock_after(best.key) : 0;
+    if (dbg && lane == 0 && col > 0) {
+      dbg[(col - 1) * 16 + 5] = k5;
+      dbg[(col - 1) * 16 + 13] = k13;
+      dbg[(col - 1) * 16 + 14] = k14;
+    }
+    if (best.key) {
+      const double* ws_ = inbox + (par * 16 + best.idx / Rb) * SL + 4;
+      for (int t = col + lane; t < steps; t += 32) U[col * smax + t] = ws_[t];
+      if (lane == 0) s_rcp[par] = __drcp_rn(ws_[col]);
+    }
+    if (lane == 0) s_best[par] = best;
+    if (dbg && lane == 0 && col > 0) dbg[(col - 1) * 16 + 15] = clock_after(__double_as_longlong(U[col * smax + steps - 1]));
+  };
+
+  // step-0 candidates: column 0 as loaded
+  double cur[RMAX];      // this row's value in column s, eliminated through step s-1
+  double fp[RMAX][kPanel];  // multipliers of the current panel's steps
+#pragma unroll
+  for (int k = 0; k < RMAX; ++k) {
+    cur[k] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPanel; ++j) fp[k][j] = 0.0;
+  }
+  if (!svc) {
+    WCand mine{0ull, -1, -1.0};
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) {
+      const int rr = ctid + k * kComp;
+      if (live >> k & 1) {
+        cur[k] = Ws[rr];
+        mine = wcand_merge_row(mine, fabs(cur[k]), r0 + rr);
+      }
+    }
+    const WCand w = warp_argmax(mine);
+    if (w.key) {
+      const int lr = w.idx - r0;
+      for (int t = lane; t < steps; t += 32) wtail[cw * smax + t] = Ws[t * Rb + lr];
+    }
+    if (lane == 0) wc[cw] = w;
+  }
+  __syncthreads();
+  if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&mbar[0], static_cast<uint32_t>(CL * push_pairs(0) * 16));
+  if (svc) push(0);
+  if (warp == 0) exchange(0);
+  __syncthreads();
+
+  int count = 0;
+  double first = 0.0;
+  for (int s = 0; s < steps; ++s) {
+    if (dbg && threadIdx.x == 32) dbg[s * 16 + 0] = clock64();
+    const WCand best = s_best[s & 1];
+    const double best_mag = key_mag(best.key);
+    if (best.key == 0 || best_mag <= abs_floor) break;
+    if (s == 0)
+      first = best_mag;
+    else if (best_mag < a.pivot_floor * first)
+      break;
+    ++count;
+    const bool last = s + 1 >= steps;
+    const int jp = s % kPanel, s0 = s - jp;  // position in the current panel
+    const double* P = U + s * smax;
+    if (svc) {
+      if (warp == 0) {
+        // bookkeeping and the LU row of D_k (owner CTA) while the compute warps eliminate
+        if (me == 0 && lane == 0) {
+          a.d_idx[s] = best.idx;
+          a.d_best[s] = best_mag;
+          a.d_second[s] = best.second;
+        }
+        if (lu_blk && best.idx >= r0 && best.idx < r0 + nr) {
+          const int lr = best.idx - r0;
+          for (int t = lane; t < steps; t += 32) lu_blk[s + t * a.lu_ld] = t < s ? Ws[t * Rb + lr] : P[t];
+        }
+        if (!last && lane == 0)
+          mbar_arrive_expect_tx(&mbar[(s + 1) & 1], static_cast<uint32_t>(CL * push_pairs(s + 1) * 16));
+      }
+    } else if (!last) {
+      const double pivot = P[s];
+      const double y = s_rcp[s & 1];
+      const bool p_ok = fabs(pivot) > 0x1p-968 && fabs(pivot) < 0x1p968;
+      // the pivot row leaves the candidate set
+      const int pk = best.idx - r0 - ctid;
+      if (pk >= 0 && pk % kComp == 0 && pk / kComp < RMAX) live &= ~(1u << (pk / kComp));
+      double ucol[kPanel];  // U(s0 + j, s + 1): the panel's pivot-row entries in column s+1
+#pragma unroll
+      for (int j = 0; j < kPanel; ++j) ucol[j] = j <= jp ? U[(s0 + j) * smax + s + 1] : 0.0;
+      WCand mine{0ull, -1, -1.0};
+      if (ka.skeleton) mine = wcand_merge_row(mine, 1.0 + 1e-3 * ((ctid * 7 + s * 13) % 97), r0 + ctid);
+#pragma unroll
+      for (int k = 0; k < RMAX; ++k) {
+        const int rr = ctid + k * kComp;
+        if (!ka.skeleton && (live >> k & 1)) {
+          const double f = div_by_pivot(cur[k], pivot, y, p_ok);
+#pragma unroll
+          for (int j = 0; j < kPanel; ++j)
+            if (j == jp) fp[k][j] = f;
+          if (lu_blk) Ws[s * Rb + rr] = f;  // column s is dead for this row: keep its multiplier
+          // column s+1: eliminated through the previous panel in shared memory; apply this
+          // panel's steps s0..s in order (the same operation sequence as right-looking)
+          double v = Ws[(s + 1) * Rb + rr];
+#pragma unroll
+          for (int j = 0; j < kPanel; ++j)
+            if (j <= jp) v = __dsub_rn(v, __dmul_rn(fp[k][j], ucol[j]));
+          cur[k] = v;
+          mine = wcand_merge_row(mine, fabs(v), r0 + rr);
+        }
+      }
+      if (dbg && threadIdx.x == 32) dbg[s * 16 + 1] = clock64();
+      const WCand w = warp_argmax(mine);
+      if (w.key) {
+        // the warp winner's full row tail (columns s+1..), pending panel updates applied
+        const int lr = w.idx - r0;
+        const int kw = lr / kComp, wl = lr & 31;
+        double fw[kPanel];
+        double vsel = cur[0];
+#pragma unroll
+        for (int k = 1; k < RMAX; ++k)
+          if (k == kw) vsel = cur[k];
+#pragma unroll
+        for (int j = 0; j < kPanel; ++j) {
+          double fsel = fp[0][j];
+#pragma unroll
+          for (int k = 1; k < RMAX; ++k)
+            if (k == kw) fsel = fp[k][j];
+          fw[j] = __shfl_sync(0xffffffffu, fsel, wl);
+        }
+        const double vw = __shfl_sync(0xffffffffu, vsel, wl);
+        double* wt = wtail + cw * smax;
+        for (int t = s + 1 + lane; t < steps; t += 32) {
+          double x = vw;
+          if (t > s + 1) {
+            x = Ws[t * Rb + lr];
+#pragma unroll
+            for (int j = 0; j < kPanel; ++j)
+              if (j <= jp) x = __dsub_rn(x, __dmul_rn(fw[j], U[(s0 + j) * smax + t]));
+          }
+          wt[t] = x;
+        }
+      }
+      if (lane == 0) wc[cw] = w;
+      if (dbg && threadIdx.x == 32) dbg[s * 16 + 2] = clock64();
+    }
+    if (last) break;
+    __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[s * 16 + 3] = clock_after(wc[0].key);
+    if (svc) {
+      push(s + 1);
+      if (dbg && threadIdx.x == 0) dbg[s * 16 + 4] = clock64();
+      if (warp == 0) {
+        exchange(s + 1);
+        if (dbg && lane == 0) dbg[s * 16 + 6] = clock64();
+      }
+    } else if (jp == kPanel - 1 && !ka.skeleton) {
+      // panel end: apply the panel's kPanel rank-1 updates to columns s+2.. in one pass
+      // (each element read and written once per panel instead of once per step)
+      const double* Up = U + s0 * smax;
+#pragma unroll
+      for (int k = 0; k < RMAX; ++k) {
+        if (!(live >> k & 1)) continue;
+        const int rr = ctid + k * kComp;
+        for (int t = s + 2; t < steps; ++t) {
+          double x = Ws[t * Rb + rr];
+#pragma unroll
+          for (int j = 0; j < kPanel; ++j) x = __dsub_rn(x, __dmul_rn(fp[k][j], Up[j * smax + t]));
+          Ws[t * Rb + rr] = x;
+        }
+      }
+      if (dbg && threadIdx.x == 32) dbg[s * 16 + 7] = clock64();
+    }
+    __syncthreads();
+    if (dbg && threadIdx.x == 32) dbg[s * 16 + 8] = clock_after(s_best[(s + 1) & 1].key);
+  }
+  if (me == 0 && threadIdx.x == 0) {
+    *a.d_count = count;
+    if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+  }
+  cluster.sync();  // no CTA leaves while a peer may still push into it
+}
+
+static size_t v2_smem_bytes(int threads, int smax, int Rb, int slot) {
+  const int comp_warps = threads / 32 - threads / 128;
+  return sizeof(double) * (static_cast<size_t>(smax) * Rb + static_cast<size_t>(smax) * smax + comp_warps * smax + 2 +
+                           2 * 16 * static_cast<size_t>(slot)) +
+         16;
+}
+
+template <int THREADS, int RMAX>
+static cudaError_t launch_cluster_v2(const LuppClusterV2Args& ka, int cl, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, lupp_cluster_v2_kernel<THREADS, RMAX>, ka);
+}
+
+template <int THREADS, int RMAX>
+static bool prepare_cluster_v2(size_t budget) {
+  auto k = lupp_cluster_v2_kernel<THREADS, RMAX>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = budget;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return clusters >= 1;
+}
+
+static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* grid_used) {
+  const int smax = std::max(a.cols_max, 1);
+  const size_t budget = 225 * 1024;
+  static int ready = -1;  // bit 0: 512-thread kernel usable, bit 1: 1024-thread kernel usable
+  if (ready < 0) ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) | (prepare_cluster_v2<1024, 2>(budget) ? 2 : 0);
+  static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;
+  static const bool v1 = getenv("ITERCUR_LUPP_CLUSTER_V1") != nullptr;  // A/B switch
+  static const int force_threads = [] {
+    const char* e = getenv("ITERCUR_LUPP_THREADS");
+    return e ? atoi(e) : 0;
+  }();
+  if (disabled || v1 || !ready || a.rows >= (1ll << 31) - 1 || smax > 56) return cudaErrorNotSupported;
+  const int slot = static_cast<int>(round_up(4 + smax + 1, 2));
+  for (int cl = 1; cl <= 16; cl *= 2) {
+    const int Rb = static_cast<int>(ceil_div(a.rows, cl));
+    // 512 threads (12 row warps, <= 4 rows each) measured faster than 1024 on B200 at every
+    // slab size that fits; the 1024-thread build is kept for A/B runs (ITERCUR_LUPP_THREADS)
+    const bool big = force_threads == 1024 && (ready & 2) && Rb <= 2 * 768;
+    const int threads = big ? 1024 : 512;
+    if (!big && (!(ready & 1) || Rb > 4 * 384)) continue;
+    const size_t smem = v2_smem_bytes(threads, smax, Rb, slot);
+    if (smem > budget) continue;
+    if (cl < 16 && Rb > 2 * (threads * 3 / 4)) continue;  // spread big slabs over more SMs
+    LuppClusterV2Args ka;
+    ka.a = a;
+    ka.dbg = g_lupp_dbg;
+    ka.skeleton = getenv("ITERCUR_LUPP_SKELETON") ? atoi(getenv("ITERCUR_LUPP_SKELETON")) : 0;
+    ka.rows_per_cta = Rb;
+    ka.smax = smax;
+    ka.slot = slot;
+    if (grid_used) *grid_used = -100 - cl;
+    return big ? launch_cluster_v2<1024, 2>(ka, cl, smem, st) : launch_cluster_v2<512, 4>(ka, cl, smem, st);
+  }
+  return cudaErrorNotSupported;
+}
+
 
 static int cluster_capacity_ok(int cl, size_t smem) {
   cudaLaunchConfig_t cfg = {};
@@ -867,7 +1355,9 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
   const int steps = std::max(a.cols_max, 1);
   // cluster path (W fits in one thread-block cluster's shared memory)
   if (g_force_path == 0 || g_force_path == 1) {
-    const cudaError_t e = try_lupp_cluster(a, st, grid_used);
+    cudaError_t e = try_lupp_cluster_v2(a, st, grid_used);
+    if (e != cudaErrorNotSupported) return e;
+    e = try_lupp_cluster(a, st, grid_used);
     if (e != cudaErrorNotSupported) return e;
   }
   // shared-memory-resident path: one CTA per SM, slab of rows_per_cta x steps doubles
