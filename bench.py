@@ -89,6 +89,47 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(kernel_substr, profile="profiles/ncu_full_r01_cfg2.txt"):
+    """DRAM bytes (read + write) per launch of a kernel from the committed `ncu --set full`
+    summary (tools/summarize_ncu.py), or None when no capture is on file."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), profile)
+    if not os.path.exists(path):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total, inside = 0.0, False
+    for line in open(path):
+        if line.startswith("=="):
+            if inside:
+                break
+            inside = kernel_substr in line
+        elif inside and ("DRAM read" in line or "DRAM write" in line):
+            parts = line.split()
+            unit = parts[-1] if parts[-1] in scale else "byte"
+            total += float(parts[-2] if parts[-1] in scale else parts[-1]) * scale[unit]
+    return total if inside or total else None
+
+
+def kernel_rooflines(engine, stages, cfg, rank_final, n_iters, hbm):
+    """Live CUDA-event timings of the per-iteration kernels at the run's mean shapes: the two
+    tall-skinny GEMMs (row residual on L: M = m; U block on R~: M = n, K = mean rank) against
+    max(bytes/BW, flops/FP64 peak), and the LUPP (latency-bound: microseconds per pivot step)."""
+    m, n, b = cfg["m"], cfg["n"], cfg["b"]
+    k_mean = max(8, int(rank_final / 2))
+    out = {}
+    for name, M in (("row_residual_gemm", m), ("u_block_gemm", n)):
+        us = stages.time_gemm(M, b, k_mean, reps=10)
+        byts = 8.0 * M * k_mean
+        fl = 2.0 * M * ((b + 7) // 8 * 8) * k_mean
+        bound_s = max(byts / (hbm * 1e9), fl / (DMMA_PEAK_TFLOPS * 1e12))
+        out[name] = {"shape_MNK": [M, b, k_mean], "us": us, "bound_us": bound_s * 1e6, "frac": bound_s * 1e6 / us,
+                     "bound": "hbm" if byts / (hbm * 1e9) >= fl / (DMMA_PEAK_TFLOPS * 1e12) else "tensor"}
+    for name, rows in (("col_lupp", n), ("row_lupp", m)):
+        r = stages.time_lupp(rows, b, reps=10)
+        out[name] = {"rows": rows, "steps": b, "us_per_call": r["us"], "us_per_step": r["us"] / b,
+                     "bound": "latency (one cluster-wide exchange per pivot step)"}
+    return out
+
+
 def cpu_reference_sample(a_host, cfg, n_iters_total, budget_s=20.0):
     """Time the CPU oracle (restatement of the reference, single thread like the reference)
     on the same matrix: the sketch plus the leading iterations until `budget_s` elapses
@@ -282,7 +323,9 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": bytes_alg / t_k / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": hbm_src}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None, "kernel": "sketch_dmma_kernel",
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": ncu_traffic("sketch_dmma_kernel"),
+                 "traffic_source": "profiles/ncu_full_r01_cfg2.txt (dram__bytes_read + dram__bytes_write, one launch)",
+                 "kernel": "sketch_dmma_kernel",
                  "ms_per_launch": sk["ms"], "ctas": sk["ctas"], "splits": sk["splits"], "tma": sk["tma"],
                  "algorithmic_bytes": bytes_alg, "algorithmic_flops": flops_alg})
 
@@ -291,6 +334,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
             "config": cfg_line, "e2e": e2e, "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
+            "kernels": kernel_rooflines(engine, stages, cfg, rank_final, n_iters, hbm),
             "run": {"status": status, "rank": rank_final, "iterations": n_iters, "phases_s": phases}}
 
     if rank == 0 and not args.no_cpu_baseline:
