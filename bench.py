@@ -15,8 +15,10 @@ tol 1e-4) on a synthetic matrix formed in HBM (inputs > L2, so no flush is neede
 
 `--impl reference` times only the CPU reference path (the oracle port: the reference
 itself cannot be built here, no Eigen) on the same config and prints the same line.
-Multi-GPU (torchrun, N > 1): every rank runs the workload on its own GPU (replicas; the
-column-sharded engine is not built yet), value = N * m*n / max-over-ranks time.
+Multi-GPU (torchrun, N > 1): by default every rank runs the workload on its own GPU (replicas,
+weak scaling), value = N * m*n / max-over-ranks time. With --sharded one matrix is
+column-sharded over the ranks (paper_2509_21963_b200/sharded.py; strong scaling),
+value = m*n / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -203,6 +205,69 @@ def run_reference_arm(args, cfg):
     return 0
 
 
+def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
+    """--sharded: one matrix column-sharded over the ranks (paper_2509_21963_b200/sharded.py,
+    SURVEY §8(e)); strong scaling: value = m*n / max-over-ranks time of one run."""
+    import numpy as np
+    import torch
+
+    import paper_2509_21963_b200 as engine  # noqa: F401  (loads the engine)
+    from paper_2509_21963_b200 import build, testmat
+    from paper_2509_21963_b200.sharded import iterative_cur_sharded
+
+    build.build()
+    a = testmat.generate(args.config)
+    lo, hi = round(rank * n / world), round((rank + 1) * n / world)
+    shard = a[:, lo:hi].t().contiguous().t()
+    del a
+    torch.cuda.synchronize()
+    run = dict(run_cfg)
+    res = None
+    for _ in range(args.warmup):
+        res = iterative_cur_sharded(shard, lo, n, **run)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = iterative_cur_sharded(shard, lo, n, **run)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    # e2e: each rank's shard from pinned host memory, H2D inside the timed region
+    host = torch.empty(shard.shape[1], shard.shape[0], dtype=torch.float64, pin_memory=True)
+    host.copy_(shard.t())
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        dshard = host.to("cuda", non_blocking=True).t()
+        r2 = iterative_cur_sharded(dshard, lo, n, **run)
+        _ = (r2.row_indices, r2.col_indices)
+    torch.cuda.synchronize()
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / max(1, args.steps)
+    if world > 1:
+        tt = torch.tensor([ms, e2e_ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, e2e_ms = float(tt[0]), float(tt[1])
+    if rank == 0:
+        line = {"metric": METRIC, "value": m * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
+                "config": {**cfg_line, "parallelism": f"column-sharded x{world}"},
+                "e2e": {"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
+                        "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms},
+                "clocks": clk.summary(),
+                "run": {"status": res.status, "rank": res.rank, "iterations": len(res.rhos),
+                        "exchanges_per_run": res.exchanges}}
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -213,6 +278,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="CPU sample budget (s)")
     ap.add_argument("--ref-iters", type=int, default=0, help="iterations to tolerance for the CPU estimate")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N > 1: one matrix column-sharded over the GPUs (strong scaling) instead of N replicas")
     args = ap.parse_args()
 
     import numpy as np
@@ -248,6 +315,9 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
         return rc
+
+    if args.sharded:
+        return run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local)
 
     import paper_2509_21963_b200 as engine
     from paper_2509_21963_b200 import build, stages

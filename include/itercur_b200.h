@@ -186,6 +186,27 @@ ITERCUR_API int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int
 
 /* Time the tall-skinny DMMA GEMM C = A(:,idx) - L * B (the row-residual shape) on random
    data: M x K times K x N, `reps` launches; returns microseconds per launch. */
+/* ---- column-sharded engine building blocks (paper_2509_21963_b200/sharded.py) ----
+ * One pivot step of the distributed column LUPP on this rank's rows of W = Y^T (select.cpp:34-74):
+ * eliminate the live rows with the previous step's pivot row dPivotRow (NULL at s == 0; the pivot's
+ * local row, if owned, is retired first), then write this rank's candidate for column s to dCand:
+ * [|best| (-1 if none), runner-up, global row index, 0, row tail W(best, 0..steps-1) (entries < s are 0)]. */
+ITERCUR_API int itercur_lupp_dist_step(double* dW, int64_t rows, int64_t ldw, int32_t steps, int32_t s,
+                                       const double* dPivotRow, int64_t pivot_local_row, uint8_t* dLive,
+                                       int64_t row_offset, double* dCand, void* stream);
+/* C(:, q) = base(:, q) + alpha * A * B(:, q), column-major (M x K, K x N), on the engine's DMMA GEMM
+ * (row residual sketch.cpp:56-58 / U block pinv.cpp:94-111 shapes). dBase may be NULL (base = 0);
+ * lda must be even and dA 16-byte aligned. */
+ITERCUR_API int itercur_gemm_device(int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda, const double* dB,
+                                    int64_t ldb, const double* dBase, int64_t ldbase, double alpha, double* dC,
+                                    int64_t ldc, void* stream);
+/* In-place LU without pivoting of the w x w cross block (rows already in LUPP order). */
+ITERCUR_API int itercur_block_lu_device(double* dD, int64_t w, int64_t ldd, void* stream);
+/* out(j, :) = D^{-1} x_j for every row j of X (M x w): forward then back substitution with the
+ * factors of itercur_block_lu_device (never an explicit inverse). */
+ITERCUR_API int itercur_rows_lu_solve_device(const double* dX, int64_t ldx, int64_t M, const double* dLU, int64_t ldd,
+                                             int64_t w, double* dOut, int64_t ldo, void* stream);
+
 ITERCUR_API int itercur_time_gemm(int64_t M, int32_t N, int64_t K, int32_t reps, void* stream, double* us_per_launch);
 
 #ifdef __cplusplus

@@ -28,6 +28,7 @@ EXPORTED = [
     "itercur_adjusted_threshold", "itercur_gratton_tail", "itercur_sketch_rows_for_block",
     "itercur_gaussian_matrix_device", "itercur_sketch_device", "itercur_select_device",
     "itercur_time_sketch_kernel", "itercur_time_lupp", "itercur_time_gemm",
+    "itercur_lupp_dist_step", "itercur_gemm_device", "itercur_block_lu_device", "itercur_rows_lu_solve_device",
 ]
 
 
@@ -105,6 +106,13 @@ def lib() -> C.CDLL:
                                                  C.c_int32, vp, dp, i32p, i32p, i32p]),
         "itercur_time_lupp": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, dp, i32p]),
         "itercur_time_gemm": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int32, vp, dp]),
+        "itercur_lupp_dist_step": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, C.c_int32, vp, C.c_int64, vp,
+                                             C.c_int64, vp, vp]),
+        "itercur_gemm_device": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64, vp,
+                                          C.c_int64, C.c_double, vp, C.c_int64, vp]),
+        "itercur_block_lu_device": (C.c_int, [vp, C.c_int64, C.c_int64, vp]),
+        "itercur_rows_lu_solve_device": (C.c_int, [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int64,
+                                                   vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -1378,6 +1378,66 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
   });
 }
 
+int itercur_lupp_dist_step(double* dW, int64_t rows, int64_t ldw, int32_t steps, int32_t s, const double* dPivotRow,
+                           int64_t pivot_local_row, uint8_t* dLive, int64_t row_offset, double* dCand, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (rows < 0 || steps < 1 || s < 0 || s >= steps || ldw < std::max<int64_t>(rows, 1) || (s > 0 && !dPivotRow))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "lupp_dist_step: invalid arguments");
+    CK(launch_lupp_dist_step(dW, rows, ldw, steps, s, s > 0 ? dPivotRow : nullptr, pivot_local_row, dLive, row_offset,
+                             dCand, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int itercur_gemm_device(int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda, const double* dB, int64_t ldb,
+                        const double* dBase, int64_t ldbase, double alpha, double* dC, int64_t ldc, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (M < 0 || N < 0 || K < 0 || (lda & 1) || (reinterpret_cast<uintptr_t>(dA) & 15) || ldc < std::max<int64_t>(M, 1) ||
+        ldb < std::max<int64_t>(K, 1) || (dBase && ldbase < std::max<int64_t>(M, 1)) || N > (1 << 30))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "gemm_device: invalid shape, leading dimension or alignment");
+    if (M == 0 || N == 0) return;
+    TsGemmParams p;
+    p.M = M;
+    p.K = K;
+    p.N = static_cast<int>(N);
+    p.A = dA;
+    p.lda = lda;
+    p.B = dB;
+    p.bsk = 1;
+    p.bsn = ldb;
+    p.base_mode = dBase ? kBaseContigCols : kBaseNone;
+    p.src = dBase;
+    p.lds = ldbase;
+    p.col0 = 0;
+    p.alpha = alpha;
+    p.out_mode = kOutColMajor;
+    p.C0 = dC;
+    p.ldc0 = ldc;
+    CK(run_ts_gemm(p, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int itercur_block_lu_device(double* dD, int64_t w, int64_t ldd, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (w < 0 || w > 4096 || ldd < std::max<int64_t>(w, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "block_lu: invalid shape");
+    CK(launch_dense_lu(dD, static_cast<int>(w), ldd, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int itercur_rows_lu_solve_device(const double* dX, int64_t ldx, int64_t M, const double* dLU, int64_t ldd, int64_t w,
+                                 double* dOut, int64_t ldo, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (M < 0 || w < 0 || w > 180 || ldx < std::max<int64_t>(M, 1) || ldo < std::max<int64_t>(M, 1) ||
+        ldd < std::max<int64_t>(w, 1))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "rows_lu_solve: invalid shape (block width above 180 unsupported)");
+    CK(launch_rows_lu_solve(dX, ldx, M, dLU, ldd, nullptr, static_cast<int>(w), dOut, ldo,
+                            static_cast<cudaStream_t>(stream), nullptr, 0));
+  });
+}
+
 int itercur_time_gemm(int64_t M, int32_t N, int64_t K, int32_t reps, void* stream, double* us_per_launch) {
   return guarded([&] {
     require_device();

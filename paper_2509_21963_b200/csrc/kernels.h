@@ -75,6 +75,11 @@ struct LuppArgs {
   const int64_t* d_lu_r = nullptr;
 };
 size_t lupp_scratch_bytes(int b);
+// column-sharded engine building blocks (shard.cu)
+cudaError_t launch_lupp_dist_step(double* W, int64_t rows, int64_t ldw, int steps, int s, const double* P,
+                                  int64_t piv_local, uint8_t* live, int64_t row_offset, double* cand,
+                                  cudaStream_t st);
+cudaError_t launch_dense_lu(double* D, int w, int64_t ldd, cudaStream_t st);
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used);
 cudaError_t launch_clear_epochs(uint8_t* mask, int64_t count, cudaStream_t st);
 // benchmarking: 0 automatic, 1 cluster only, 2 grid shared-memory only, 3 global only
