@@ -1357,9 +1357,9 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
           const long long* v = h.data() + q * 16;
           fprintf(stderr,
                   "lupp v2 step %d: [t32] eager %lld wcand %lld | [t0] B1-released %lld read-wc %lld argmax %lld vals "
-                  "%lld st.async %lld wait %lld read-in %lld argmax %lld tail %lld | B2-released(t32) %lld | step %lld\n",
+                  "%lld st.async %lld wait %lld read-in %lld argmax %lld tail %lld | B2-released(t32) %lld | step %lld [probe %lld]\n",
                   q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[10] - v[3], v[11] - v[10], v[12] - v[11], v[4] - v[12],
-                  v[5] - v[4], v[13] - v[5], v[14] - v[13], v[15] - v[14], v[8] - v[15], v[16] - v[0]);
+                  v[5] - v[4], v[13] - v[5], v[14] - v[13], v[15] - v[14], v[8] - v[15], v[16] - v[0], v[9] / 100);
         }
       } else
       for (int q = 0; q + 1 < steps; ++q) {

@@ -796,6 +796,7 @@ struct LuppClusterV2Args {
   LuppArgs a;
   long long* dbg;  // optional per-step clock64() trace of CTA 0 (16 slots per step)
   int skeleton;    // benchmarking only: 1 = skip the row eliminations (exchange cost alone)
+  int serial_exchange;  // reduce the CL slots lane-serially instead of with warp collectives
   int rows_per_cta;
   int smax;        // column capacity of the buffers (cols_max)
   int slot;        // doubles per inbox slot: 4 + smax rounded up to even
@@ -828,11 +829,11 @@ __device__ __forceinline__ double div_by_pivot(double a, double p, double y, boo
 
 template <int THREADS, int RMAX>
 __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppClusterV2Args ka) {
-  // warp roles by scheduler: warps 0, 4, 8, .. (all on sub-partition 0) are service warps
-  // (exchange pushes; warp 0 also reduces the inbox), the others own rows. Keeping the row
-  // work off sub-partition 0 leaves the latency-critical exchange its issue slots.
+  // warp roles: warps 0..3 (one per scheduler sub-partition) are service warps — each reduces
+  // the CTA's warp candidates and pushes the CTA slot to a quarter of the cluster; warp 0 also
+  // reduces the inbox — and warps 4.. own rows.
   constexpr int kWarps = THREADS / 32;
-  constexpr int kSvc = kWarps / 4;
+  constexpr int kSvc = 4;
   constexpr int kCompWarps = kWarps - kSvc;
   constexpr int kComp = kCompWarps * 32;
   constexpr int kPanel = 4;  // rank-1 updates of later columns are applied kPanel steps at a time
@@ -848,8 +849,8 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   const int CL = static_cast<int>(cluster.num_blocks());
   const int me = static_cast<int>(cluster.block_rank());
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool svc = (warp & 3) == 0;
-  const int cw = warp - (warp >> 2) - 1;  // compute-warp index (valid when !svc)
+  const bool svc = warp < kSvc;
+  const int cw = warp - kSvc;  // compute-warp index (valid when !svc)
   const int ctid = cw * 32 + lane;
   const int Rb = ka.rows_per_cta;
   const int smax = ka.smax, SL = ka.slot;
@@ -950,7 +951,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       const uint32_t bar = smem_u32(&mbar[par]);
       if (dbg && threadIdx.x == 0 && col > 0)
         dbg[(col - 1) * 16 + 12] = clock_after(__double_as_longlong(v0) ^ __double_as_longlong(v1));
-      for (int dst = warp >> 2; dst < CL; dst += kSvc)
+      for (int dst = warp; dst < CL; dst += kSvc)
         st_async_v2(map_cluster_addr(slot, dst), v0, v1, map_cluster_addr(bar, dst));
     }
   };
@@ -972,8 +973,44 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       }
     }
     const long long k13 = dbg ? clock_after(g.key) : 0;
-    WCand best = warp_argmax(g);
+    WCand best;
+    if (ka.serial_exchange) {
+      // every lane scans the CL slots itself (broadcast shared loads, no warp collectives):
+      // slots in rank order, strict '>' = lowest index on ties (rank order is index order)
+      best = WCand{0ull, -1, -1.0};
+      for (int q = 0; q < CL; ++q) {
+        const double* rs = inbox + (par * 16 + q) * SL;
+        const double mag = rs[0];
+        if (mag < 0.0) continue;
+        const uint64_t key = mag_key(mag);
+        if (key > best.key) {
+          best.second = fmax(key_mag(best.key), rs[1]);
+          best.key = key;
+          best.idx = static_cast<int32_t>(__double_as_longlong(rs[2]));
+        } else {
+          best.second = fmax(best.second, mag);
+        }
+      }
+    } else {
+      best = warp_argmax(g);
+    }
     const long long k14 = dbg ? clock_after(best.key) : 0;
+    if (ka.skeleton >= 2 && dbg && col == 5) {  // benchmarking: cost of 100 ALU ops / 100 argmaxes here
+      uint64_t x = best.key;
+      const long long q0 = clock_after(x);
+      if (ka.skeleton == 2) {
+        for (int q = 0; q < 100; ++q) x = x * 0x9e3779b97f4a7c15ull + (x >> 7);
+      } else {
+        WCand gg = g;
+        for (int q = 0; q < 100; ++q) {
+          const WCand bb = warp_argmax(gg);
+          gg.key ^= (bb.key & 1);
+          x ^= bb.key;
+        }
+      }
+      const long long q1 = clock_after(x);
+      if (lane == 0) dbg[(col - 1) * 16 + 9] = (q1 - q0) * 100 + (x & 1);
+    }
     if (dbg && lane == 0 && col > 0) {
       dbg[(col - 1) * 16 + 5] = k5;
       dbg[(col - 1) * 16 + 13] = k13;
@@ -1062,23 +1099,47 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       for (int j = 0; j < kPanel; ++j) ucol[j] = j <= jp ? U[(s0 + j) * smax + s + 1] : 0.0;
       WCand mine{0ull, -1, -1.0};
       if (ka.skeleton) mine = wcand_merge_row(mine, 1.0 + 1e-3 * ((ctid * 7 + s * 13) % 97), r0 + ctid);
+      const uint32_t act = ka.skeleton ? 0u : live;
+      // branch-free over this thread's rows so their latencies overlap: loads, quotient
+      // (Markstein), panel updates, then the (rare) IEEE fix-up, stores and merge
+      double wn[RMAX], fq[RMAX];
+      bool bad = false;
 #pragma unroll
       for (int k = 0; k < RMAX; ++k) {
-        const int rr = ctid + k * kComp;
-        if (!ka.skeleton && (live >> k & 1)) {
-          const double f = div_by_pivot(cur[k], pivot, y, p_ok);
+        const int rr = min(ctid + k * kComp, Rb - 1);
+        wn[k] = Ws[(s + 1) * Rb + rr];
+        const double x = cur[k];
+        const double q0 = __dmul_rn(x, y);
+        const double rm = __fma_rn(-q0, pivot, x);
+        fq[k] = __fma_rn(rm, y, q0);
+        const double aq = fabs(fq[k]), ax = fabs(x);
+        bad |= (act >> k & 1) && !(p_ok && aq > 0x1p-968 && aq < 0x1p968 && ax > 0x1p-968 && ax < 0x1p968);
+      }
+      if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
-          for (int j = 0; j < kPanel; ++j)
-            if (j == jp) fp[k][j] = f;
-          if (lu_blk) Ws[s * Rb + rr] = f;  // column s is dead for this row: keep its multiplier
-          // column s+1: eliminated through the previous panel in shared memory; apply this
-          // panel's steps s0..s in order (the same operation sequence as right-looking)
-          double v = Ws[(s + 1) * Rb + rr];
+        for (int k = 0; k < RMAX; ++k)
+          if (act >> k & 1) fq[k] = div_by_pivot(cur[k], pivot, y, p_ok);
+      }
 #pragma unroll
-          for (int j = 0; j < kPanel; ++j)
-            if (j <= jp) v = __dsub_rn(v, __dmul_rn(fp[k][j], ucol[j]));
+      for (int k = 0; k < RMAX; ++k) {
+#pragma unroll
+        for (int j = 0; j < kPanel; ++j)
+          if (j == jp) fp[k][j] = fq[k];
+        // column s+1: eliminated through the previous panel in shared memory; apply this
+        // panel's steps s0..s in order (the same operation sequence as right-looking)
+        double v = wn[k];
+#pragma unroll
+        for (int j = 0; j < kPanel; ++j)
+          if (j <= jp) v = __dsub_rn(v, __dmul_rn(fp[k][j], ucol[j]));
+        if (act >> k & 1) {
+          const int rr = ctid + k * kComp;
+          if (lu_blk) Ws[s * Rb + rr] = fq[k];  // column s is dead for this row: keep its multiplier
           cur[k] = v;
-          mine = wcand_merge_row(mine, fabs(v), r0 + rr);
+          const uint64_t key = mag_key(fabs(v));
+          const bool better = key > mine.key;
+          mine.second = better ? key_mag(mine.key) : fmax(mine.second, fabs(v));
+          mine.key = better ? key : mine.key;
+          mine.idx = better ? r0 + rr : mine.idx;
         }
       }
       if (dbg && threadIdx.x == 32) dbg[s * 16 + 1] = clock64();
@@ -1154,7 +1215,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
 }
 
 static size_t v2_smem_bytes(int threads, int smax, int Rb, int slot) {
-  const int comp_warps = threads / 32 - threads / 128;
+  const int comp_warps = threads / 32 - 4;
   return sizeof(double) * (static_cast<size_t>(smax) * Rb + static_cast<size_t>(smax) * smax + comp_warps * smax + 2 +
                            2 * 16 * static_cast<size_t>(slot)) +
          16;
@@ -1207,8 +1268,8 @@ static bool prepare_cluster_v2(size_t budget) {
 static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* grid_used) {
   const int smax = std::max(a.cols_max, 1);
   const size_t budget = 225 * 1024;
-  static int ready = -1;  // bit 0: 512-thread kernel usable, bit 1: 1024-thread kernel usable
-  if (ready < 0) ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) | (prepare_cluster_v2<1024, 2>(budget) ? 2 : 0);
+  static int ready = -1;  // bit 0: 512-thread kernel usable, bit 1: 768-thread kernel usable
+  if (ready < 0) ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) | (prepare_cluster_v2<768, 2>(budget) ? 2 : 0);
   static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;
   static const bool v1 = getenv("ITERCUR_LUPP_CLUSTER_V1") != nullptr;  // A/B switch
   static const int force_threads = [] {
@@ -1219,23 +1280,24 @@ static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* 
   const int slot = static_cast<int>(round_up(4 + smax + 1, 2));
   for (int cl = 1; cl <= 16; cl *= 2) {
     const int Rb = static_cast<int>(ceil_div(a.rows, cl));
-    // 512 threads (12 row warps, <= 4 rows each) measured faster than 1024 on B200 at every
-    // slab size that fits; the 1024-thread build is kept for A/B runs (ITERCUR_LUPP_THREADS)
-    const bool big = force_threads == 1024 && (ready & 2) && Rb <= 2 * 768;
-    const int threads = big ? 1024 : 512;
+    // 768 threads (20 row warps, <= 2 rows each) when the slab allows, else 512 (12 row
+    // warps, <= 4 rows each); ITERCUR_LUPP_THREADS=512|768 forces one for A/B runs
+    const bool big = force_threads != 512 && (ready & 2) && Rb <= 2 * 640;
+    const int threads = big ? 768 : 512;
     if (!big && (!(ready & 1) || Rb > 4 * 384)) continue;
     const size_t smem = v2_smem_bytes(threads, smax, Rb, slot);
     if (smem > budget) continue;
-    if (cl < 16 && Rb > 2 * (threads * 3 / 4)) continue;  // spread big slabs over more SMs
+    if (cl < 16 && Rb > 512) continue;  // spread slabs over more SMs: fewer rows per thread per step
     LuppClusterV2Args ka;
     ka.a = a;
     ka.dbg = g_lupp_dbg;
     ka.skeleton = getenv("ITERCUR_LUPP_SKELETON") ? atoi(getenv("ITERCUR_LUPP_SKELETON")) : 0;
+    ka.serial_exchange = getenv("ITERCUR_LUPP_SERIAL") != nullptr;
     ka.rows_per_cta = Rb;
     ka.smax = smax;
     ka.slot = slot;
     if (grid_used) *grid_used = -100 - cl;
-    return big ? launch_cluster_v2<1024, 2>(ka, cl, smem, st) : launch_cluster_v2<512, 4>(ka, cl, smem, st);
+    return big ? launch_cluster_v2<768, 2>(ka, cl, smem, st) : launch_cluster_v2<512, 4>(ka, cl, smem, st);
   }
   return cudaErrorNotSupported;
 }

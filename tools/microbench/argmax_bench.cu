@@ -59,6 +59,35 @@ __global__ void bench_big(long long* out, int iters, int mode, double seed) {
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x == 0) { out[3 + mode] = (t1 - t0) / iters; out[8] = c.key; }
 }
+__device__ __forceinline__ long long clock_after(unsigned long long dep) {
+  long long c;
+  asm volatile("{\n.reg .pred p;\nsetp.ne.u64 p, %1, 0x5a5a5a5a5a5a5a5a;\n@p mov.u64 %0, %%clock64;\n@!p mov.u64 %0, %%clock64;\n}\n"
+               : "=l"(c) : "l"(dep) : "memory");
+  return c;
+}
+// the LUPP push pattern: compute warps publish WCand to smem, barrier, warp 0 loads and reduces
+__global__ void push_pattern(long long* out, int iters, double seed) {
+  __shared__ WCand wc[16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long acc_ld = 0, acc_am = 0, acc_bar = 0;
+  uint64_t sink = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (warp >= 4 && lane == 0) wc[warp - 4] = WCand{mag_key(seed + warp * 0.1 + it), warp * 100 + it, 0.5};
+    const long long tb = clock64();
+    __syncthreads();
+    if (warp == 0) {
+      const long long t0 = clock_after(tb);
+      const WCand c = lane < 12 ? wc[lane] : WCand{0ull, -1, -1.0};
+      const long long t1 = clock_after(c.key ^ (uint64_t)c.idx ^ (uint64_t)__double_as_longlong(c.second));
+      const WCand r = warp_argmax(c);
+      const long long t2 = clock_after(r.key ^ (uint64_t)r.idx);
+      acc_ld += t1 - t0; acc_am += t2 - t1; acc_bar += t0 - tb;
+      sink ^= r.key;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[6] = acc_bar / iters; out[7] = acc_ld / iters; out[5] = acc_am / iters; out[9] = sink; }
+}
 int main() {
   long long* d; long long h[10];
   cudaMalloc(&d, sizeof(h));
@@ -79,5 +108,9 @@ int main() {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   printf("warp_argmax: all warps %lld, warp0 alone (others at barrier) %lld, warp0 + busy warps %lld cycles\n", h[0], h[1], h[2]);
   printf("warp0 alone, 225KB smem: %lld; same in a 16-CTA cluster: %lld (%s)\n", h[3], h[4], cudaGetErrorString(cudaGetLastError()));
+  push_pattern<<<1, 512>>>(d, 1000, 1.5);
+  push_pattern<<<1, 512>>>(d, 1000, 1.5);
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("push pattern: barrier %lld, smem load %lld, warp_argmax %lld cycles (%s)\n", h[6], h[7], h[5], cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
