@@ -118,6 +118,15 @@ __device__ __forceinline__ double block_sum(double v, double* smem_scratch) {
 // with g = lane / 4, t = lane % 4. Kernels permute K so logical (t, t+4) = physical
 // (2t, 2t+1): one 16-byte shared load per fragment pair.
 // ---------------------------------------------------------------------------------
+// programmatic dependent launch: wait for the preceding kernel's completion and memory
+// (no-op when launched without the PDL attribute); allow the next kernel to launch early
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+#ifdef ITERCUR_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], double a0, double a1, double a2, double a3, double b0,
                                             double b1) {
   asm(  // not volatile: lets the scheduler interleave independent MMAs with loads

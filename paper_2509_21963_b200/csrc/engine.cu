@@ -547,6 +547,10 @@ void run_iterative_cur(itercur_run* run) {
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
     int64_t batch_launches = 0;
     auto enqueue_batch = [&]() {
+      // programmatic dependent launch along the iteration's kernel chain: measured neutral to
+      // slightly slower inside the batch graphs on B200 (config 2: 38.5 vs 38.3 ms), so opt-in
+      static const bool pdl = getenv("ITERCUR_PDL") != nullptr;
+      PdlScope pdl_scope(pdl && !evs.on);
       batch_launches = 0;
       for (int j = 0; j < kBatch; ++j) {
         IterState* slot = reinterpret_cast<IterState*>(slots + slot_bytes * j);

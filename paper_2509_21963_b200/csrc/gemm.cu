@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
   extern __shared__ __align__(16) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  griddep_wait();
   if (p.ctl) {
     if (p.ctl->done) return;
     const int64_t r = p.ctl->r;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
     }
   }
   cp_async_wait<0>();
+  griddep_launch_dependents();
   gemm_epilogue<NT, WARPS>(p, acc, gsm, i0, q0, nvalid, splits);
 }
 
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
   extern __shared__ __align__(16) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  griddep_wait();
   if (p.ctl) {
     if (p.ctl->done) return;
     const int64_t r = p.ctl->r;
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
     }
   }
   cp_async_wait<0>();
+  griddep_launch_dependents();
   gemm_epilogue<NT, WARPS, UB>(p, acc, gsm, i0, q0, nvalid, splits);
 }
 
@@ -575,23 +579,7 @@ static int gemm_splits(int64_t tiles, int64_t K, int kt) {
 
 template <typename Kern>
 static cudaError_t launch_split(Kern kern, dim3 grid, int threads, int bytes, const TsGemmParams& p, cudaStream_t st) {
-  if (grid.z == 1) {
-    kern<<<grid, threads, bytes, st>>>(p);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = bytes;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = grid.z;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  return launch_ex(kern, grid, dim3(threads), bytes, st, dim3(grid.z > 1 ? 1 : 0, 1, grid.z), p);
 }
 
 template <int NT, int WARPS>

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace itercur_b200 {
 
 constexpr uint32_t kStreamSketch = 1;      // RngStream::Sketch, proj/include/itercur/rng.hpp:13
@@ -12,6 +14,45 @@ constexpr int kSketchSparseSign = 1;
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+// Programmatic dependent launch for the per-iteration kernel chain: while the engine enqueues
+// an iteration batch (pdl_scope), launches carry cudaLaunchAttributeProgrammaticStream-
+// Serialization, so each kernel is launched while its predecessor drains; every such kernel
+// calls griddep_wait() (common.cuh) before touching its predecessor's output.
+bool pdl_enabled();
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(bool on);
+  ~PdlScope();
+};
+// cudaLaunchKernelEx with optional cluster dims (cluster.x == 0: no cluster attribute) and the
+// PDL attribute when enabled.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, dim3 cluster,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cluster.x > 0) {  // explicit cluster launch (dim3(0, ...) = none)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster.x;
+    attr[na].val.clusterDim.y = cluster.y;
+    attr[na].val.clusterDim.z = cluster.z;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------- sketch
 // Dense sketch operator S (rows_pad x ldg, row-major: S[h * ldg + k]), rows h >= c and

@@ -856,6 +856,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   const int smax = ka.smax, SL = ka.slot;
   const int r0 = me * Rb;
   const int nr = max(0, min(Rb, static_cast<int>(a.rows) - r0));
+  griddep_wait();  // everything below reads the predecessor's output
   int steps = a.cols_max;
   if (a.d_steps) steps = min(steps, *a.d_steps);
   if (steps <= 0) {
@@ -1070,6 +1071,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       break;
     ++count;
     const bool last = s + 1 >= steps;
+    if (last) griddep_launch_dependents();
     const int jp = s % kPanel, s0 = s - jp;  // position in the current panel
     const double* P = U + s * smax;
     if (svc) {
@@ -1223,19 +1225,7 @@ static size_t v2_smem_bytes(int threads, int smax, int Rb, int slot) {
 
 template <int THREADS, int RMAX>
 static cudaError_t launch_cluster_v2(const LuppClusterV2Args& ka, int cl, size_t smem, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cl);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cl;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, lupp_cluster_v2_kernel<THREADS, RMAX>, ka);
+  return launch_ex(lupp_cluster_v2_kernel<THREADS, RMAX>, dim3(cl), dim3(THREADS), smem, st, dim3(cl, 1, 1), ka);
 }
 
 template <int THREADS, int RMAX>

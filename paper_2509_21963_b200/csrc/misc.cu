@@ -11,6 +11,13 @@
 
 namespace itercur_b200 {
 
+namespace {
+thread_local bool g_pdl = false;
+}
+bool pdl_enabled() { return g_pdl; }
+PdlScope::PdlScope(bool on) : prev(g_pdl) { g_pdl = on; }
+PdlScope::~PdlScope() { g_pdl = prev; }
+
 // Wc(j, h) = Y(h, j) for h < rows  (Wc column-major n x rows)
 __global__ void transpose_rows_kernel(const double* __restrict__ Y, int64_t cp, int64_t n, int rows,
                                       double* __restrict__ Wc, int64_t ldwc) {
@@ -25,6 +32,8 @@ __global__ void transpose_rows_kernel(const double* __restrict__ Y, int64_t cp, 
 __global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride, int64_t col_stride, int64_t Kmax,
                               const int64_t* __restrict__ idx, const int* __restrict__ d_w, int w_max,
                               double* __restrict__ out, int64_t ldo, const IterCtl* __restrict__ ctl, int k_from_r) {
+  griddep_wait();
+  griddep_launch_dependents();
   if (ctl && ctl->done) return;
   const int64_t K = (ctl && k_from_r) ? min(Kmax, ctl->r) : Kmax;
   const int w = d_w ? min(*d_w, w_max) : w_max;
@@ -50,9 +59,8 @@ cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_str
   const int64_t total = K * w_max;
   if (total <= 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
-  gather_kernel<<<blocks, 256, 0, st>>>(src, row_stride, col_stride, K, d_idx, d_w, w_max, out, ldo, ctl,
-                                        k_from_r ? 1 : 0);
-  return cudaGetLastError();
+  return launch_ex(gather_kernel, dim3(blocks), dim3(256), 0, st, dim3(0, 0, 0), src, row_stride, col_stride, K, d_idx,
+                   d_w, w_max, out, ldo, ctl, k_from_r ? 1 : 0);
 }
 
 __global__ void gather2_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ idx, int64_t K,
@@ -96,6 +104,8 @@ cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, ui
 __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
                                 const int* __restrict__ d_w, int w_max, double* __restrict__ lu, int64_t ldd,
                                 const IterCtl* __restrict__ ctl) {
+  griddep_wait();
+  griddep_launch_dependents();
   if (ctl) {
     if (ctl->done) return;
     Lk += ctl->r * ldl;
@@ -127,6 +137,8 @@ __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, cons
 __global__ void cross_lu_warp_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
                                      const int* __restrict__ d_w, double* __restrict__ lu, int64_t ldd,
                                      const IterCtl* __restrict__ ctl) {
+  griddep_wait();
+  griddep_launch_dependents();
   if (ctl) {
     if (ctl->done) return;
     Lk += ctl->r * ldl;
@@ -161,11 +173,8 @@ __global__ void cross_lu_warp_kernel(const double* __restrict__ Lk, int64_t ldl,
 
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
                             double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl) {
-  if (w_max <= 32)
-    cross_lu_warp_kernel<<<1, 32, 0, st>>>(Lk, ldl, d_rows, d_w, lu, ldd, ctl);
-  else
-    cross_lu_kernel<<<1, 256, 0, st>>>(Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
-  return cudaGetLastError();
+  if (w_max <= 32) return launch_ex(cross_lu_warp_kernel, dim3(1), dim3(32), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, lu, ldd, ctl);
+  return launch_ex(cross_lu_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
 }
 
 // Row-wise solves D x = u with D = Lhat * Uhat (cross_lu_kernel layout) for every row u of
@@ -178,6 +187,8 @@ __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, 
                                      int w_max, double* __restrict__ out, int64_t ldo,
                                      const IterCtl* __restrict__ ctl, int64_t out_off_per_r) {
   extern __shared__ double slu[];
+  griddep_wait();
+  griddep_launch_dependents();
   if (ctl) {
     if (ctl->done) return;
     lu += ctl->r * ldd;
@@ -254,11 +265,14 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 16));
   const size_t smem = sizeof(double) * static_cast<size_t>(w_max) * w_max;
   if (w_max <= 16) {
-    rows_lu_solve_kernel<16><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+    return launch_ex(rows_lu_solve_kernel<16>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
+                     w_max, out, ldo, ctl, out_off_per_r);
   } else if (w_max <= 32) {
-    rows_lu_solve_kernel<32><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+    return launch_ex(rows_lu_solve_kernel<32>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
+                     w_max, out, ldo, ctl, out_off_per_r);
   } else if (w_max <= 64) {
-    rows_lu_solve_kernel<64><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r);
+    return launch_ex(rows_lu_solve_kernel<64>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
+                     w_max, out, ldo, ctl, out_off_per_r);
   } else if (w_max <= 180) {
     // X itself serves as the per-row workspace when solving in place is not requested:
     // use the output buffer (each row's entries are private to its thread)
@@ -336,6 +350,8 @@ cudaError_t launch_count_nonfinite(const double* x, int64_t rows, int64_t cols, 
 
 // Iteration start (driver.cpp:87-95).
 __global__ void iter_begin_kernel(IterCtl* ctl, IterState* slot) {
+  griddep_wait();
+  griddep_launch_dependents();
   slot->ncols = slot->nrows = slot->width = 0;
   slot->valid = 0;
   if (ctl->done) {
@@ -352,8 +368,7 @@ __global__ void iter_begin_kernel(IterCtl* ctl, IterState* slot) {
   ctl->block = static_cast<int32_t>(min(static_cast<int64_t>(ctl->b), ctl->max_rank - ctl->r));
 }
 cudaError_t launch_iter_begin(IterCtl* ctl, IterState* slot, cudaStream_t st) {
-  iter_begin_kernel<<<1, 1, 0, st>>>(ctl, slot);
-  return cudaGetLastError();
+  return launch_ex(iter_begin_kernel, dim3(1), dim3(1), 0, st, dim3(0, 0, 0), ctl, slot);
 }
 
 __global__ void width_kernel(IterState* slot, const IterCtl* ctl) {
@@ -372,6 +387,8 @@ __global__ void commit_kernel(IterCtl* ctl, IterState* slot, IterArrays arr, int
                               int64_t y_parts) {
   __shared__ int s_stop;
   __shared__ double red[8];
+  griddep_wait();
+  griddep_launch_dependents();
   if (ctl->done) return;
   {  // ||Y||^2 of the downdated residual: fixed-order sum of the GEMM's per-CTA partials
     double sq = 0.0;
@@ -414,8 +431,8 @@ __global__ void commit_kernel(IterCtl* ctl, IterState* slot, IterArrays arr, int
 cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, int64_t* I_all, int64_t* J_all,
                           uint8_t* row_mask, uint8_t* col_mask, const double* y_partials, int64_t y_parts,
                           cudaStream_t st) {
-  commit_kernel<<<1, 256, 0, st>>>(ctl, slot, arr, I_all, J_all, row_mask, col_mask, y_partials, y_parts);
-  return cudaGetLastError();
+  return launch_ex(commit_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), ctl, slot, arr, I_all, J_all, row_mask,
+                   col_mask, y_partials, y_parts);
 }
 
 }  // namespace itercur_b200
