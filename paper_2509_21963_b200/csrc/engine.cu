@@ -546,6 +546,10 @@ void run_iterative_cur(itercur_run* run) {
     // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
     int64_t batch_launches = 0;
+    // iteration-begin + gathers folded into the cluster LUPP kernels: measured slightly slower
+    // than separate grid-wide gather launches inside the batch graphs (config 2: 39.4 vs
+    // 38.8 ms; the strided gathers then run on the cluster's 16 SMs only), so opt-in
+    static const bool fuse_off = getenv("ITERCUR_LUPP_FUSION") == nullptr;
     auto enqueue_batch = [&]() {
       // programmatic dependent launch along the iteration's kernel chain: measured neutral to
       // slightly slower inside the batch graphs on B200 (config 2: 38.5 vs 38.3 ms), so opt-in
@@ -561,9 +565,10 @@ void run_iterative_cur(itercur_run* run) {
           iter_events.push_back(e0);
           ev_i += 6;
         }
-        CK(launch_iter_begin(d_ctl, slot, st));
-
-        // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139)
+        // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139); on the
+        //     cluster path the same kernel also opens the iteration (iter_begin) and, after its
+        //     last pivot, gathers R~(:,J_k) (GEMM1's B) and Y(:,J_k) (the downdate's B)
+        bool col_fused = false;
         {
           LuppArgs la{};
           la.W = ws.Wc.p;
@@ -582,6 +587,15 @@ void run_iterative_cur(itercur_run* run) {
           la.d_gen_k = &d_ctl->k;
           la.gen_base = gen_base;
           la.gen_which = 0;
+          col_fused = fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
+          if (col_fused) {
+            la.begin_ctl = d_ctl;
+            la.begin_slot = slot;
+            la.post[0] = {run->Rt.p, run->ldR, 1, ldbg, &d_ctl->r, ws.Bg.p, ldbg, B};
+            la.post[1] = {ws.Y.p, 1, cp, cp, nullptr, ws.Yg.p, cp, B};
+          } else {
+            CK(launch_iter_begin(d_ctl, slot, st));
+          }
           CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
@@ -589,7 +603,8 @@ void run_iterative_cur(itercur_run* run) {
         // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60);
         //     Rt(:,J_k) is gathered once into a contiguous K x w block (a strided gather inside
         //     the GEMM loader would re-fetch one 32-B sector per element in every CTA)
-        CK(launch_gather(run->Rt.p, run->ldR, 1, ldbg, arr.col_idx, &slot->ncols, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        if (!col_fused)
+          CK(launch_gather(run->Rt.p, run->ldR, 1, ldbg, arr.col_idx, &slot->ncols, B, ws.Bg.p, ldbg, st, d_ctl, true));
         {
           TsGemmParams p;
           p.M = m;
@@ -619,6 +634,7 @@ void run_iterative_cur(itercur_run* run) {
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
 
         int row_lupp_path = 0;
+        bool row_fused = false;
         // (3) row selection: LUPP on S_row (select_rows, select.cpp:141-165), b = |cols|
         {
           LuppArgs la{};
@@ -643,6 +659,8 @@ void run_iterative_cur(itercur_run* run) {
           la.lu_out = run->Dinv.p;
           la.lu_ld = run->bmax;
           la.d_lu_r = &d_ctl->r;
+          row_fused = fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
+          if (row_fused) la.post[0] = {run->L.p, run->ldL, 1, ldbg, &d_ctl->r, ws.Bg.p, ldbg, B};  // L(I_k, :)
           CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, &row_lupp_path));
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
@@ -651,14 +669,16 @@ void run_iterative_cur(itercur_run* run) {
         //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
         if (row_lupp_path >= 0)  // the cluster LUPP emitted the factors of D_k itself
           CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
-        CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        if (!row_fused)
+          CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
         if (fused_ub) {
           // Y(:, J_k) before the downdate, then one kernel: U_k^T, the solves against D_k,
           // R~ rows, Y^T -= R~_k^T Y(:, J_k)^T, ||Y||^2 partials and Wc
-          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+          if (!col_fused)
+            CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
           TsGemmParams p = ublock_params(ldbg, slot, arr);
           CK(run_ts_gemm_ublock(p, st));
-          batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0);
+          batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0) - (col_fused ? 3 : 0) - (row_fused ? 1 : 0);
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));  // downdate fused into the core step
           CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p,

@@ -114,7 +114,26 @@ struct LuppArgs {
   double* lu_out = nullptr;
   int64_t lu_ld = 0;
   const int64_t* d_lu_r = nullptr;
+  // optional (cluster path, see lupp_fuses_iteration_work): the iteration-begin bookkeeping of
+  // misc.cu iter_begin_kernel runs in the prologue (steps then come from the loop control, not
+  // d_steps) ...
+  void* begin_ctl = nullptr;   // IterCtl*
+  void* begin_slot = nullptr;  // IterState*
+  // ... and up to two gathers indexed by the pivots just chosen run after the last step:
+  // out[k + q*ldo] = src[k*row_stride + idx[q]*col_stride] for k < K, q < count, zero for
+  // count <= q < w_fill; K = min(kmax, *k_cap) when k_cap is set.
+  struct Gather {
+    const double* src = nullptr;
+    int64_t row_stride = 0, col_stride = 0, kmax = 0;
+    const int64_t* k_cap = nullptr;
+    double* out = nullptr;
+    int64_t ldo = 0;
+    int w_fill = 0;
+  } post[2];
 };
+// true when run_lupp_with_scratch takes the cluster path for these arguments (which honours
+// begin_ctl / post gathers; the other paths ignore them and the caller launches them itself)
+bool lupp_fuses_iteration_work(const LuppArgs& a);
 size_t lupp_scratch_bytes(int b);
 // column-sharded engine building blocks (shard.cu)
 cudaError_t launch_lupp_dist_step(double* W, int64_t rows, int64_t ldw, int steps, int s, const double* P,

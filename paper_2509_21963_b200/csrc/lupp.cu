@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "misc.h"
 
 namespace cg = cooperative_groups;
 
@@ -773,6 +774,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
 
 
 static long long* g_lupp_dbg = nullptr;
+static int g_force_path = 0;  // benchmarking: 0 automatic, 1 cluster, 2 grid smem, 3 global
 
 // ---------------------------------------------------------------------------------
 // Cluster LUPP, v2 (the default cluster path). Same pivots and arithmetic as above, with a
@@ -846,6 +848,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   __shared__ WCand s_best[2];
   __shared__ double s_rcp[2];
   __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ int64_t s_piv[64];  // this call's pivots (all CTAs know them): post gathers
   const int CL = static_cast<int>(cluster.num_blocks());
   const int me = static_cast<int>(cluster.block_rank());
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -858,7 +861,27 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   const int nr = max(0, min(Rb, static_cast<int>(a.rows) - r0));
   griddep_wait();  // everything below reads the predecessor's output
   int steps = a.cols_max;
-  if (a.d_steps) steps = min(steps, *a.d_steps);
+  if (a.begin_ctl) {
+    // iteration begin (misc.cu iter_begin_kernel): every CTA derives the same step count from
+    // the loop control; CTA 0 records it (the others never read what it writes)
+    IterCtl* ctl = static_cast<IterCtl*>(a.begin_ctl);
+    const int done = ctl->done;
+    const bool budget_out = !done && (ctl->r >= ctl->max_rank || ctl->k >= ctl->max_iters);
+    const int blk = (done || budget_out) ? 0 : static_cast<int>(min(static_cast<int64_t>(ctl->b), ctl->max_rank - ctl->r));
+    steps = min(steps, blk);
+    if (me == 0 && threadIdx.x == 0) {
+      IterState* slot = static_cast<IterState*>(a.begin_slot);
+      slot->ncols = slot->nrows = slot->width = 0;
+      slot->valid = (done || budget_out) ? 0 : 1;
+      if (budget_out) {
+        ctl->done = 1;
+        ctl->status = 1;  // MaxRank
+      }
+      if (!done) ctl->block = blk;
+    }
+  } else if (a.d_steps) {
+    steps = min(steps, *a.d_steps);
+  }
   if (steps <= 0) {
     if (me == 0 && threadIdx.x == 0) {
       *a.d_count = 0;
@@ -1074,6 +1097,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
     if (last) griddep_launch_dependents();
     const int jp = s % kPanel, s0 = s - jp;  // position in the current panel
     const double* P = U + s * smax;
+    if (threadIdx.x == 0) s_piv[s] = best.idx;
     if (svc) {
       if (warp == 0) {
         // bookkeeping and the LU row of D_k (owner CTA) while the compute warps eliminate
@@ -1213,6 +1237,21 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
     *a.d_count = count;
     if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
   }
+  // post gathers indexed by the pivots (replacing separate gather launches), spread over the
+  // cluster's threads
+  __syncthreads();
+#pragma unroll
+  for (int gq = 0; gq < 2; ++gq) {
+    const LuppArgs::Gather& G = a.post[gq];
+    if (!G.src) continue;
+    const int64_t K = G.k_cap ? min(G.kmax, *G.k_cap) : G.kmax;
+    const int64_t total = K * G.w_fill;
+    const int64_t stride = static_cast<int64_t>(CL) * THREADS;
+    for (int64_t e = static_cast<int64_t>(me) * THREADS + threadIdx.x; e < total; e += stride) {
+      const int64_t q = e / K, kk = e - q * K;
+      G.out[kk + q * G.ldo] = q < count ? G.src[kk * G.row_stride + s_piv[q] * G.col_stride] : 0.0;
+    }
+  }
   cluster.sync();  // no CTA leaves while a peer may still push into it
 }
 
@@ -1255,7 +1294,35 @@ static bool prepare_cluster_v2(size_t budget) {
   return clusters >= 1;
 }
 
+struct V2Plan {
+  bool ok = false;
+  int cl = 0, threads = 0, Rb = 0, slot = 0;
+  size_t smem = 0;
+};
+static V2Plan plan_lupp_cluster_v2(const LuppArgs& a);
+
 static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* grid_used) {
+  const V2Plan pl = plan_lupp_cluster_v2(a);
+  if (!pl.ok) return cudaErrorNotSupported;
+  LuppClusterV2Args ka;
+  ka.a = a;
+  ka.dbg = g_lupp_dbg;
+  ka.skeleton = getenv("ITERCUR_LUPP_SKELETON") ? atoi(getenv("ITERCUR_LUPP_SKELETON")) : 0;
+  ka.serial_exchange = getenv("ITERCUR_LUPP_SERIAL") != nullptr;
+  ka.rows_per_cta = pl.Rb;
+  ka.smax = std::max(a.cols_max, 1);
+  ka.slot = pl.slot;
+  if (grid_used) *grid_used = -100 - pl.cl;
+  return pl.threads == 768 ? launch_cluster_v2<768, 2>(ka, pl.cl, pl.smem, st)
+                           : launch_cluster_v2<512, 4>(ka, pl.cl, pl.smem, st);
+}
+
+bool lupp_fuses_iteration_work(const LuppArgs& a) {
+  return (g_force_path == 0 || g_force_path == 1) && plan_lupp_cluster_v2(a).ok;
+}
+
+static V2Plan plan_lupp_cluster_v2(const LuppArgs& a) {
+  V2Plan pl;
   const int smax = std::max(a.cols_max, 1);
   const size_t budget = 225 * 1024;
   static int ready = -1;  // bit 0: 512-thread kernel usable, bit 1: 768-thread kernel usable
@@ -1266,7 +1333,7 @@ static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* 
     const char* e = getenv("ITERCUR_LUPP_THREADS");
     return e ? atoi(e) : 0;
   }();
-  if (disabled || v1 || !ready || a.rows >= (1ll << 31) - 1 || smax > 56) return cudaErrorNotSupported;
+  if (disabled || v1 || !ready || a.rows >= (1ll << 31) - 1 || smax > 56) return pl;
   const int slot = static_cast<int>(round_up(4 + smax + 1, 2));
   for (int cl = 1; cl <= 16; cl *= 2) {
     const int Rb = static_cast<int>(ceil_div(a.rows, cl));
@@ -1278,18 +1345,15 @@ static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* 
     const size_t smem = v2_smem_bytes(threads, smax, Rb, slot);
     if (smem > budget) continue;
     if (cl < 16 && Rb > 512) continue;  // spread slabs over more SMs: fewer rows per thread per step
-    LuppClusterV2Args ka;
-    ka.a = a;
-    ka.dbg = g_lupp_dbg;
-    ka.skeleton = getenv("ITERCUR_LUPP_SKELETON") ? atoi(getenv("ITERCUR_LUPP_SKELETON")) : 0;
-    ka.serial_exchange = getenv("ITERCUR_LUPP_SERIAL") != nullptr;
-    ka.rows_per_cta = Rb;
-    ka.smax = smax;
-    ka.slot = slot;
-    if (grid_used) *grid_used = -100 - cl;
-    return big ? launch_cluster_v2<768, 2>(ka, cl, smem, st) : launch_cluster_v2<512, 4>(ka, cl, smem, st);
+    pl.ok = true;
+    pl.cl = cl;
+    pl.threads = threads;
+    pl.Rb = Rb;
+    pl.slot = slot;
+    pl.smem = smem;
+    return pl;
   }
-  return cudaErrorNotSupported;
+  return pl;
 }
 
 
@@ -1394,7 +1458,6 @@ size_t lupp_scratch_bytes(int b) {
          sizeof(double) * 2 * kMaxLuppGrid * static_cast<size_t>(b + 4);
 }
 
-static int g_force_path = 0;
 void set_lupp_force_path(int path) { g_force_path = path; }
 void set_lupp_debug_trace(long long* dbg) { g_lupp_dbg = dbg; }
 
