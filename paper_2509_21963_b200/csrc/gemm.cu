@@ -108,16 +108,61 @@ __device__ __forceinline__ void gemm_load_stage(const TsGemmParams& p, double* s
 // Split-K cluster reduction (when gridDim.z > 1) and the fused epilogue: base + alpha * acc
 // written per out_mode, with the per-CTA sum of squares of C.
 template <int NT, int WARPS>
-__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
-                                                int w);
+__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], const double (&bv)[NT][4],
+                                                const double (&yv)[NT + 1][4], const double* s_lu, const double* s_yg,
+                                                int64_t i0, int w);
+
+// base(i, q) of the epilogue (loaded before the split-K exchange so its latency overlaps it)
+__device__ __forceinline__ double gemm_base(const TsGemmParams& p, int64_t i, int64_t q) {
+  switch (p.base_mode) {
+    case kBaseGatherCols: return p.src[i + p.idx[q] * p.lds];
+    case kBaseGatherRowsT: return p.src[p.idx[q] + i * p.lds];
+    case kBaseContigCols: return p.src[i + (p.col0 + q) * p.lds];
+    case kBaseInPlaceRowMajor: return p.C0[i * p.ldc0 + q];
+    case kBaseIdentityCols: return (i == p.col0 + q) ? 1.0 : 0.0;
+    default: return 0.0;
+  }
+}
 
 template <int NT, int WARPS, bool UB = false>
 __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
                                               int64_t q0, int nvalid, int splits) {
   constexpr int THREADS = WARPS * 32;
+  constexpr int W = NT * 8;
+  constexpr int NTY = NT + 1;
+  constexpr int YP = ((W + 15) / 16) * 16 + 8;
   __shared__ double red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  const int64_t r0 = i0 + warp * 16 + 2 * g;
+  // epilogue operands fetched before the split-K exchange (their latency overlaps it): the
+  // base values, and for the U block the Y^T rows to downdate and D_k's factors / Y(:,J_k)
+  const bool finisher = blockIdx.z == 0;
+  double bv[NT][4], yv[NTY][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq)
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int ql = nt * 8 + 2 * t + dq;
+        const int64_t i = r0 + dr;
+        bv[nt][dr * 2 + dq] = (finisher && ql < nvalid && i < p.M) ? gemm_base(p, i, q0 + ql) : 0.0;
+      }
+  double* s_lu = gsm + NT * 4 * THREADS;  // past the split-K exchange buffer
+  double* s_yg = s_lu + W * W;
+  if constexpr (UB) {
+#pragma unroll
+    for (int ny = 0; ny < NTY; ++ny)
+#pragma unroll
+      for (int dq = 0; dq < 2; ++dq)
+#pragma unroll
+        for (int dr = 0; dr < 2; ++dr) {
+          const int h = ny * 8 + 2 * t + dq;
+          const int64_t j = r0 + dr;
+          yv[ny][dr * 2 + dq] = (finisher && h < p.ycp && j < p.M) ? p.y[j * p.ycp + h] : 0.0;
+        }
+  }
   if (splits > 1) {
     // fixed-order reduction over the cluster: rank z publishes its fragments in its own
     // shared memory, rank 0 adds ranks 1..S-1 in order (deterministic for a given S)
@@ -144,13 +189,24 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
     if (blockIdx.z != 0) return;
   }
   if constexpr (UB) {
-    ublock_epilogue<NT, WARPS>(p, acc, gsm, i0, nvalid);
+    __syncthreads();  // the ring (and the split exchange buffer) is drained: reuse it
+    const int64_t rr = p.ctl ? p.ctl->r : 0;
+    const double* lu = p.lu + rr * p.ldd;
+    for (int e = threadIdx.x; e < W * W; e += THREADS) {
+      const int a = e % W, b = e / W;
+      s_lu[e] = (a < nvalid && b < nvalid) ? lu[a + b * p.ldd] : 0.0;
+    }
+    for (int e = threadIdx.x; e < NTY * 8 * W; e += THREADS) {
+      const int h = e / W, q = e % W;
+      s_yg[h * YP + q] = (q < nvalid && h < p.ycp) ? p.yg[h + q * p.ycp] : 0.0;
+    }
+    __syncthreads();
+    ublock_epilogue<NT, WARPS>(p, acc, bv, yv, s_lu, s_yg, i0, nvalid);
     return;
   }
 
   // ---------------- epilogue: physical rows (2g, 2g+1), columns (2t, 2t+1) ----------
   double sq = 0.0;
-  const int64_t r0 = i0 + warp * 16 + 2 * g;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -162,16 +218,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
       for (int dr = 0; dr < 2; ++dr) {
         const int64_t i = r0 + dr;
         if (i >= p.M) continue;
-        double base = 0.0;
-        switch (p.base_mode) {
-          case kBaseGatherCols: base = p.src[i + p.idx[q] * p.lds]; break;
-          case kBaseGatherRowsT: base = p.src[p.idx[q] + i * p.lds]; break;
-          case kBaseContigCols: base = p.src[i + (p.col0 + q) * p.lds]; break;
-          case kBaseInPlaceRowMajor: base = p.C0[i * p.ldc0 + q]; break;
-          case kBaseIdentityCols: base = (i == p.col0 + q) ? 1.0 : 0.0; break;
-          default: break;
-        }
-        const double v = base + p.alpha * acc[nt][dr * 2 + dq];
+        const double v = bv[nt][dr * 2 + dq] + p.alpha * acc[nt][dr * 2 + dq];
         sq = fma(v, v, sq);
         if (p.out_mode == kOutColMajor) {
           p.C0[i + q * p.ldc0] = v;
@@ -203,8 +250,9 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
 // loop: logical k t <-> column 2t, t+4 <-> 2t+1), so Y^T -= X Yg^T runs on DMMA without
 // leaving registers.
 template <int NT, int WARPS>
-__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
-                                                int w) {
+__device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&acc)[NT][4], const double (&bv)[NT][4],
+                                                const double (&yv)[NT + 1][4], const double* s_lu, const double* s_yg,
+                                                int64_t i0, int w) {
   constexpr int W = NT * 8;          // max block width
   constexpr int NTY = NT + 1;        // n-tiles of the downdate (ycp <= 8 * (NT + 1))
   constexpr int YP = ((W + 15) / 16) * 16 + 8;  // Yg^T pitch: 16-byte loads conflict-free
@@ -212,21 +260,8 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int64_t r = p.ctl ? p.ctl->r : 0;
-  const double* lu = p.lu + r * p.ldd;
-  double* s_lu = gsm;            // [W][W]: s_lu[a + b*W] = LU(a, b)
-  double* s_yg = gsm + W * W;    // [NTY*8][YP]: s_yg[h*YP + q] = Yg(h, q) = Y(h, J_k[q])
-  __syncthreads();               // the ring is drained: reuse it
-  for (int e = threadIdx.x; e < W * W; e += WARPS * 32) {
-    const int a = e % W, b = e / W;
-    s_lu[e] = (a < w && b < w) ? lu[a + b * p.ldd] : 0.0;
-  }
-  for (int e = threadIdx.x; e < NTY * 8 * W; e += WARPS * 32) {
-    const int h = e / W, q = e % W;
-    s_yg[h * YP + q] = (q < w && h < p.ycp) ? p.yg[h + q * p.ycp] : 0.0;
-  }
-  __syncthreads();
 
-  // u = base + alpha * acc (base = A(I_k[q], j)), zero outside the block
+  // u = base + alpha * acc (base = A(I_k[q], j), prefetched), zero outside the block
   const int64_t r0 = i0 + warp * 16 + 2 * g;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
@@ -237,7 +272,7 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
       for (int dr = 0; dr < 2; ++dr) {
         const int64_t j = r0 + dr;
         double v = 0.0;
-        if (q < w && j < p.M) v = p.src[p.idx[q] + j * p.lds] + p.alpha * acc[nt][dr * 2 + dq];
+        if (q < w && j < p.M) v = bv[nt][dr * 2 + dq] + p.alpha * acc[nt][dr * 2 + dq];
         acc[nt][dr * 2 + dq] = v;
       }
     }
@@ -324,9 +359,8 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
       for (int dr = 0; dr < 2; ++dr) {
         const int64_t j = r0 + dr;
         if (j >= p.M) continue;
-        double* yp = p.y + j * p.ycp + h;
-        const double v = *yp + p.alpha * yacc[ny][dr * 2 + dq];
-        *yp = v;
+        const double v = yv[ny][dr * 2 + dq] + p.alpha * yacc[ny][dr * 2 + dq];
+        p.y[j * p.ycp + h] = v;
         sq = fma(v, v, sq);
         if (h < p.wc_rows) p.Wc[j + h * p.ldwc] = v;
       }
@@ -600,7 +634,7 @@ static cudaError_t launch_cfg(const TsGemmParams& p, cudaStream_t st) {
 template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
 static cudaError_t launch_lean(const TsGemmParams& p, cudaStream_t st) {
   using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
-  static_assert(!UB || (NT * 8 * NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
+  static_assert(!UB || (NT * 4 * Cfg::THREADS + NT * 8 * NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
                         STAGES * Cfg::STAGE_ELEMS), "U-block epilogue buffers must fit the ring");
   static bool attr_set = false;
   if (!attr_set) {
