@@ -1363,7 +1363,9 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
       total += ms;
     }
     set_lupp_force_path(0);
-    if (getenv("ITERCUR_LUPP_TRACE")) {  // one traced launch: per-step phase cycles of CTA 0
+    // one traced launch: per-step phase cycles of CTA 0 (the cluster kernel records them only
+    // in an instrumented build: ITERCUR_NVCC_EXTRA=-DITERCUR_LUPP_INSTRUMENT)
+    if (getenv("ITERCUR_LUPP_TRACE")) {
       DevBuf<long long> tr;
       tr.alloc(static_cast<size_t>(steps) * 16);
       CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * 16, st));

@@ -939,7 +939,13 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   }
   const double abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(nsq);
   double* lu_blk = a.lu_out ? a.lu_out + (a.d_lu_r ? *a.d_lu_r : 0) * a.lu_ld : nullptr;
+#ifdef ITERCUR_LUPP_INSTRUMENT  // tracing / ablation build (tools/lupp_one.py with ITERCUR_LUPP_TRACE)
   long long* dbg = (ka.dbg && me == 0) ? ka.dbg : nullptr;
+  const int kSkel = ka.skeleton, kSerial = ka.serial_exchange;
+#else  // production: the instrumentation folds away
+  long long* const dbg = nullptr;
+  constexpr int kSkel = 0, kSerial = 0;
+#endif
 
   // bytes one CTA pushes per step (header + pair-aligned tail from column col)
   auto push_pairs = [&](int col) { return 2 + (steps - (col & ~1) + 1) / 2; };
@@ -998,7 +1004,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
     }
     const long long k13 = dbg ? clock_after(g.key) : 0;
     WCand best;
-    if (ka.serial_exchange) {
+    if (kSerial) {
       // every lane scans the CL slots itself (broadcast shared loads, no warp collectives):
       // slots in rank order, strict '>' = lowest index on ties (rank order is index order)
       best = WCand{0ull, -1, -1.0};
@@ -1019,10 +1025,10 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       best = warp_argmax(g);
     }
     const long long k14 = dbg ? clock_after(best.key) : 0;
-    if (ka.skeleton >= 2 && dbg && col == 5) {  // benchmarking: cost of 100 ALU ops / 100 argmaxes here
+    if (kSkel >= 2 && dbg && col == 5) {  // benchmarking: cost of 100 ALU ops / 100 argmaxes here
       uint64_t x = best.key;
       const long long q0 = clock_after(x);
-      if (ka.skeleton == 2) {
+      if (kSkel == 2) {
         for (int q = 0; q < 100; ++q) x = x * 0x9e3779b97f4a7c15ull + (x >> 7);
       } else {
         WCand gg = g;
@@ -1041,7 +1047,9 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       dbg[(col - 1) * 16 + 14] = k14;
     }
     if (best.key) {
-      const double* ws_ = inbox + (par * 16 + best.idx / Rb) * SL + 4;
+      // the winning slot's lane is its CTA rank (no division by the runtime slab size)
+      const unsigned own = __ballot_sync(0xffffffffu, lane < CL && g.key == best.key && g.idx == best.idx);
+      const double* ws_ = inbox + (par * 16 + (__ffs(own) - 1)) * SL + 4;
       for (int t = col + lane; t < steps; t += 32) U[col * smax + t] = ws_[t];
       if (lane == 0) s_rcp[par] = __drcp_rn(ws_[col]);
     }
@@ -1124,8 +1132,8 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
 #pragma unroll
       for (int j = 0; j < kPanel; ++j) ucol[j] = j <= jp ? U[(s0 + j) * smax + s + 1] : 0.0;
       WCand mine{0ull, -1, -1.0};
-      if (ka.skeleton) mine = wcand_merge_row(mine, 1.0 + 1e-3 * ((ctid * 7 + s * 13) % 97), r0 + ctid);
-      const uint32_t act = ka.skeleton ? 0u : live;
+      if (kSkel) mine = wcand_merge_row(mine, 1.0 + 1e-3 * ((ctid * 7 + s * 13) % 97), r0 + ctid);
+      const uint32_t act = kSkel ? 0u : live;
       // branch-free over this thread's rows so their latencies overlap: loads, quotient
       // (Markstein), panel updates, then the (rare) IEEE fix-up, stores and merge
       double wn[RMAX], fq[RMAX];
@@ -1213,7 +1221,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
         exchange(s + 1);
         if (dbg && lane == 0) dbg[s * 16 + 6] = clock64();
       }
-    } else if (jp == kPanel - 1 && !ka.skeleton) {
+    } else if (jp == kPanel - 1 && !kSkel) {
       // panel end: apply the panel's kPanel rank-1 updates to columns s+2.. in one pass
       // (each element read and written once per panel instead of once per step)
       const double* Up = U + s0 * smax;
