@@ -969,11 +969,27 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       } else if (lane == 1) {
         v0 = __longlong_as_double(bc.key ? static_cast<long long>(bc.idx) : -1ll);
       } else if (bc.key) {
+        // the CTA winner's row from column col on: column col was eliminated through step
+        // col-1 by its owner (stored), later columns still owe the open panel's steps
+        // s0..col-1, applied here in step order with the multipliers kept in Ws
         const int lr = bc.idx - r0;
-        const double* wt = wtail + ((lr % kComp) / 32) * smax;
         const int t0 = (col & ~1) + 2 * (lane - 2);
-        v0 = (t0 >= col && t0 < steps) ? wt[t0] : 0.0;
-        v1 = (t0 + 1 < steps) ? wt[t0 + 1] : 0.0;
+        const int sp = col - 1, jp = sp >= 0 ? sp % kPanel : -1, s0 = sp - jp;
+        double fm[kPanel];
+#pragma unroll
+        for (int j = 0; j < kPanel; ++j) fm[j] = j <= jp ? Ws[(s0 + j) * Rb + lr] : 0.0;
+        auto tail_at = [&](int t) {
+          if (t < col || t >= steps) return 0.0;
+          double x = Ws[t * Rb + lr];
+          if (t > col) {
+#pragma unroll
+            for (int j = 0; j < kPanel; ++j)
+              if (j <= jp) x = __dsub_rn(x, __dmul_rn(fm[j], U[(s0 + j) * smax + t]));
+          }
+          return x;
+        };
+        v0 = tail_at(t0);
+        v1 = tail_at(t0 + 1);
       }
       const int t0 = (col & ~1) + 2 * (lane - 2);
       const int off = lane < 2 ? 2 * lane : 4 + t0;
@@ -985,6 +1001,10 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
         st_async_v2(map_cluster_addr(slot, dst), v0, v1, map_cluster_addr(bar, dst));
     }
   };
+  // named barrier 1: the service warps have read the CTA winner's row (push), so the row
+  // warps may apply a panel's trailing update to Ws
+  auto tail_read_arrive = [&]() { asm volatile("bar.arrive 1, %0;\n" ::"n"(THREADS) : "memory"); };
+  auto tail_read_wait = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(THREADS) : "memory"); };
   // warp 0: wait for the CL slots of column col, reduce them in fixed order, copy the
   // winner's tail, form the next reciprocal
   auto exchange = [&](int col) {
@@ -1077,10 +1097,6 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       }
     }
     const WCand w = warp_argmax(mine);
-    if (w.key) {
-      const int lr = w.idx - r0;
-      for (int t = lane; t < steps; t += 32) wtail[cw * smax + t] = Ws[t * Rb + lr];
-    }
     if (lane == 0) wc[cw] = w;
   }
   __syncthreads();
@@ -1167,7 +1183,8 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
           if (j <= jp) v = __dsub_rn(v, __dmul_rn(fp[k][j], ucol[j]));
         if (act >> k & 1) {
           const int rr = ctid + k * kComp;
-          if (lu_blk) Ws[s * Rb + rr] = fq[k];  // column s is dead for this row: keep its multiplier
+          Ws[s * Rb + rr] = fq[k];  // column s is dead for this row: keep its multiplier
+          Ws[(s + 1) * Rb + rr] = v;  // column s+1, eliminated through step s
           cur[k] = v;
           const uint64_t key = mag_key(fabs(v));
           const bool better = key > mine.key;
@@ -1178,36 +1195,6 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
       }
       if (dbg && threadIdx.x == 32) dbg[s * 16 + 1] = clock64();
       const WCand w = warp_argmax(mine);
-      if (w.key) {
-        // the warp winner's full row tail (columns s+1..), pending panel updates applied
-        const int lr = w.idx - r0;
-        const int kw = lr / kComp, wl = lr & 31;
-        double fw[kPanel];
-        double vsel = cur[0];
-#pragma unroll
-        for (int k = 1; k < RMAX; ++k)
-          if (k == kw) vsel = cur[k];
-#pragma unroll
-        for (int j = 0; j < kPanel; ++j) {
-          double fsel = fp[0][j];
-#pragma unroll
-          for (int k = 1; k < RMAX; ++k)
-            if (k == kw) fsel = fp[k][j];
-          fw[j] = __shfl_sync(0xffffffffu, fsel, wl);
-        }
-        const double vw = __shfl_sync(0xffffffffu, vsel, wl);
-        double* wt = wtail + cw * smax;
-        for (int t = s + 1 + lane; t < steps; t += 32) {
-          double x = vw;
-          if (t > s + 1) {
-            x = Ws[t * Rb + lr];
-#pragma unroll
-            for (int j = 0; j < kPanel; ++j)
-              if (j <= jp) x = __dsub_rn(x, __dmul_rn(fw[j], U[(s0 + j) * smax + t]));
-          }
-          wt[t] = x;
-        }
-      }
       if (lane == 0) wc[cw] = w;
       if (dbg && threadIdx.x == 32) dbg[s * 16 + 2] = clock64();
     }
@@ -1216,12 +1203,14 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
     if (dbg && threadIdx.x == 0) dbg[s * 16 + 3] = clock_after(wc[0].key);
     if (svc) {
       push(s + 1);
+      if (jp == kPanel - 1) tail_read_arrive();
       if (dbg && threadIdx.x == 0) dbg[s * 16 + 4] = clock64();
       if (warp == 0) {
         exchange(s + 1);
         if (dbg && lane == 0) dbg[s * 16 + 6] = clock64();
       }
-    } else if (jp == kPanel - 1 && !kSkel) {
+    } else if (jp == kPanel - 1) {
+      tail_read_wait();  // the service warps have read the CTA winner's row
       // panel end: apply the panel's kPanel rank-1 updates to columns s+2.. in one pass
       // (each element read and written once per panel instead of once per step)
       const double* Up = U + s0 * smax;
