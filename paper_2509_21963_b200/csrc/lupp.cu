@@ -1310,8 +1310,10 @@ static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* 
   ka.smax = std::max(a.cols_max, 1);
   ka.slot = pl.slot;
   if (grid_used) *grid_used = -100 - pl.cl;
-  return pl.threads == 768 ? launch_cluster_v2<768, 2>(ka, pl.cl, pl.smem, st)
-                           : launch_cluster_v2<512, 4>(ka, pl.cl, pl.smem, st);
+  if (pl.threads == 768)
+    return pl.Rb <= 640 ? launch_cluster_v2<768, 1>(ka, pl.cl, pl.smem, st)   // one row per row thread
+                        : launch_cluster_v2<768, 2>(ka, pl.cl, pl.smem, st);
+  return launch_cluster_v2<512, 4>(ka, pl.cl, pl.smem, st);
 }
 
 bool lupp_fuses_iteration_work(const LuppArgs& a) {
@@ -1323,7 +1325,9 @@ static V2Plan plan_lupp_cluster_v2(const LuppArgs& a) {
   const int smax = std::max(a.cols_max, 1);
   const size_t budget = 225 * 1024;
   static int ready = -1;  // bit 0: 512-thread kernel usable, bit 1: 768-thread kernel usable
-  if (ready < 0) ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) | (prepare_cluster_v2<768, 2>(budget) ? 2 : 0);
+  if (ready < 0)
+    ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) |
+            (prepare_cluster_v2<768, 2>(budget) && prepare_cluster_v2<768, 1>(budget) ? 2 : 0);
   static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;
   static const bool v1 = getenv("ITERCUR_LUPP_CLUSTER_V1") != nullptr;  // A/B switch
   static const int force_threads = [] {
