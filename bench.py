@@ -111,11 +111,11 @@ def ncu_traffic(kernel_substr, profile="profiles/ncu_full_r01_cfg2.txt"):
     return total if inside or total else None
 
 
-def kernel_rooflines(engine, stages, cfg, rank_final, n_iters, hbm):
+def kernel_rooflines(engine, stages, cfg, m, n, rank_final, n_iters, hbm):
     """Live CUDA-event timings of the per-iteration kernels at the run's mean shapes: the two
     tall-skinny GEMMs (row residual on L: M = m; U block on R~: M = n, K = mean rank) against
     max(bytes/BW, flops/FP64 peak), and the LUPP (latency-bound: microseconds per pivot step)."""
-    m, n, b = cfg["m"], cfg["n"], cfg["b"]
+    b = cfg["b"]
     k_mean = max(8, int(rank_final / 2))
     out = {}
     for name, M in (("row_residual_gemm", m), ("u_block_gemm", n)):
@@ -404,7 +404,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
             "config": cfg_line, "e2e": e2e, "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
-            "kernels": kernel_rooflines(engine, stages, cfg, rank_final, n_iters, hbm),
+            "kernels": kernel_rooflines(engine, stages, cfg, m, n, rank_final, n_iters, hbm),
             "run": {"status": status, "rank": rank_final, "iterations": n_iters, "phases_s": phases}}
 
     if rank == 0 and not args.no_cpu_baseline:
