@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libitercur_b200.so")
+LIB_PATH = os.environ.get("ITERCUR_LIB_OVERRIDE") or os.path.join(_HERE, "libitercur_b200.so")  # A/B builds
 
 OK = 0
 E_INVALID, E_RANGE, E_DOMAIN, E_RUNTIME, E_LOGIC = 1, 2, 3, 4, 5

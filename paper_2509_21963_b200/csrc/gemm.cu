@@ -603,8 +603,10 @@ static int gemm_warps(int64_t) {
 }
 
 // split-K factor: enough CTAs for ~4 resident per SM, each split keeping >= 4 k-stages.
+static thread_local int g_splits_override = 0;  // per-launch override (U block tuning)
 static int gemm_splits(int64_t tiles, int64_t K, int kt) {
-  static const int forced = env_int("ITERCUR_GEMM_SPLITS", 0);
+  static const int forced_env = env_int("ITERCUR_GEMM_SPLITS", 0);
+  const int forced = g_splits_override > 0 ? g_splits_override : forced_env;
   const int64_t stages = ceil_div(K, kt);
   int s = forced > 0 ? forced : static_cast<int>(ceil_div(4 * kNumSMs, std::max<int64_t>(tiles, 1)));
   s = static_cast<int>(std::min<int64_t>(s, std::max<int64_t>(1, stages / 4)));
@@ -684,10 +686,13 @@ int64_t ts_gemm_ublock_parts(int64_t M) { return ceil_div(M, 64); }
 
 template <int NT>
 static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
-  static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
+  static const int forced = env_int("ITERCUR_UB_LEAN", env_int("ITERCUR_GEMM_LEAN", -1));
+  static const int ub_splits = env_int("ITERCUR_UB_SPLITS", 0);
   const int lean = forced > 0 ? forced : (p.M >= 16000 ? 2 : 1);
-  if (lean == 2) return launch_lean<NT, 4, 32, 3, true>(p, st);
-  return launch_lean<NT, 4, 16, 4, true>(p, st);
+  g_splits_override = ub_splits;
+  const cudaError_t e = lean == 2 ? launch_lean<NT, 4, 32, 3, true>(p, st) : launch_lean<NT, 4, 16, 4, true>(p, st);
+  g_splits_override = 0;
+  return e;
 }
 
 cudaError_t run_ts_gemm_ublock(const TsGemmParams& p, cudaStream_t st) {

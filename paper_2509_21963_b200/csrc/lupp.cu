@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppCluster
   constexpr int kSvc = 4;
   constexpr int kCompWarps = kWarps - kSvc;
   constexpr int kComp = kCompWarps * 32;
-  constexpr int kPanel = 4;  // rank-1 updates of later columns are applied kPanel steps at a time
+  constexpr int kPanel = 2;  // rank-1 updates of later columns are applied kPanel steps at a time
   cg::cluster_group cluster = cg::this_cluster();
   const LuppArgs& a = ka.a;
   extern __shared__ __align__(16) double sm[];
