@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define ITERCUR_B200_ABI_VERSION 1
+#define ITERCUR_B200_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ITERCUR_API __attribute__((visibility("default")))
@@ -87,7 +87,8 @@ typedef struct itercur_config {
   int32_t sketch_kind; /* ITERCUR_SKETCH_GAUSSIAN (the reference's only kind) */
   int32_t sparse_nnz;  /* 8 */
   int32_t profile;     /* 1: record per-phase CUDA-event times into the trace */
-  int32_t reserved;
+  int32_t sketch_stream; /* 0 -> RngStream::Sketch (1); 2 = SluppSketch (the s-LUPP baseline) */
+  int64_t sketch_rows;   /* 0 -> floor(1.1 b) (sketch.hpp:10); > 0 overrides (s-LUPP: ceil(1.1 r)) */
 } itercur_config;
 
 /* One IterationRecord (proj/include/itercur/driver.hpp:32-44) plus pivot-margin data. */

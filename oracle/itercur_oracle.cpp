@@ -913,6 +913,45 @@ int oracle_core_matrix(const double* A, int64_t m, int64_t n, int64_t lda, const
   });
 }
 
+// slupp_cur, proj/src/baselines.cpp:39-62: one sketch of ceil(1.1 r) rows (stream
+// SluppSketch), r LUPP column pivots, LUPP row pivots on A(:, J), then the factors.
+int oracle_slupp_cur(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r, uint64_t seed, int64_t* I,
+                     int64_t* J, int64_t* rank) {
+  return guarded([&] {
+    const oracle::View a{A, m, n, lda};
+    if (r < 0 || r > std::min(m, n)) throw std::invalid_argument("rank must lie in [0, min(m, n)]");
+    *rank = 0;
+    if (r == 0) return;
+    const int64_t c = (11 * r + 9) / 10;  // ceil(1.1 r)
+    const oracle::Mat g = oracle::gaussian_matrix(c, m, seed, ORACLE_STREAM_SLUPP_SKETCH);
+    oracle::Mat sketched(c, n);  // matmul(G, A)
+    for (int64_t j = 0; j < n; ++j) {
+      double* y = sketched.col(j);
+      const double* aj = A + j * lda;
+      for (int64_t k = 0; k < m; ++k) {
+        const double* gk = g.col(k);
+        for (int64_t i = 0; i < c; ++i) y[i] += gk[i] * aj[k];
+      }
+    }
+    const oracle::SelectionResult cols =
+        oracle::select_columns(sketched, std::min(r, c), ORACLE_PIVOT_LUPP, 1e-13, {});
+    if (cols.indices.empty()) throw std::runtime_error("singular cross block");
+    const oracle::Mat picked = oracle::gather_cols(a, cols.indices);
+    const oracle::SelectionResult rows = oracle::select_rows(picked, static_cast<int64_t>(cols.indices.size()),
+                                                             ORACLE_PIVOT_LUPP, 1e-13, {});
+    if (rows.indices.empty()) throw std::runtime_error("singular cross block");
+    const size_t width = std::min(cols.indices.size(), rows.indices.size());
+    oracle::IndexList Ik(rows.indices.begin(), rows.indices.begin() + static_cast<std::ptrdiff_t>(width));
+    oracle::IndexList Jk(cols.indices.begin(), cols.indices.begin() + static_cast<std::ptrdiff_t>(width));
+    const oracle::CurFactors cur = oracle::make_cur_factors(a, Ik, Jk);  // may throw "singular cross block"
+    for (size_t q = 0; q < width; ++q) {
+      I[q] = cur.I[q];
+      J[q] = cur.J[q];
+    }
+    *rank = static_cast<int64_t>(width);
+  });
+}
+
 // Reference test fixtures (proj/tests/oracles.hpp:20-37): std::mt19937_64 with libstdc++'s
 // uniform_real_distribution / normal_distribution, filled column by column — the exact
 // inputs the reference's own unit tests use (g++/libstdc++ here, as there).

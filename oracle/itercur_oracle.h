@@ -37,7 +37,7 @@ enum {
 };
 
 /* proj/include/itercur/rng.hpp:12-19 stream tags, plus the new SparseSign = 7. */
-enum { ORACLE_STREAM_SKETCH = 1, ORACLE_STREAM_SPARSE_SIGN = 7 };
+enum { ORACLE_STREAM_SKETCH = 1, ORACLE_STREAM_SLUPP_SKETCH = 2, ORACLE_STREAM_SPARSE_SIGN = 7 };
 enum { ORACLE_SKETCH_GAUSSIAN = 0, ORACLE_SKETCH_SPARSE_SIGN = 1 };
 enum { ORACLE_PIVOT_LUPP = 0, ORACLE_PIVOT_QRCP = 1, ORACLE_PIVOT_OSINSKY = 2 };
 enum { ORACLE_CONVERGED = 0, ORACLE_MAX_RANK = 1, ORACLE_RESIDUAL_EXHAUSTED = 2 };
@@ -120,6 +120,10 @@ int oracle_true_relative_error(const double* A, int64_t m, int64_t n, int64_t ld
 /* core_out = A(I,J)^+ (r x r column-major), via the COD restatement (proj/src/pinv.cpp:40-65) */
 int oracle_core_matrix(const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I,
                        const int64_t* J, int64_t r, double* core_out);
+
+/* one-shot s-LUPP CUR baseline (proj/src/baselines.cpp:39-62): I, J (length *rank <= r) */
+int oracle_slupp_cur(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r, uint64_t seed, int64_t* I,
+                     int64_t* J, int64_t* rank);
 
 /* proj/tests/oracles.hpp:20-37 fixtures (std::mt19937_64 + libstdc++ distributions) */
 void oracle_fixture_random_dense(int64_t rows, int64_t cols, uint32_t seed, double lo, double hi, double* out);

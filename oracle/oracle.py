@@ -90,6 +90,8 @@ def lib() -> C.CDLL:
                                            C.POINTER(_Result)]
         L.oracle_true_relative_error.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, i64p, i64p, C.c_int64, dp]
         L.oracle_core_matrix.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, i64p, i64p, C.c_int64, dp]
+        L.oracle_slupp_cur.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, i64p, i64p,
+                                       C.POINTER(C.c_int64)]
         L.oracle_fixture_random_dense.argtypes = [C.c_int64, C.c_int64, C.c_uint32, C.c_double, C.c_double, dp]
         L.oracle_fixture_random_gaussian.argtypes = [C.c_int64, C.c_int64, C.c_uint32, dp]
         _lib = L
@@ -291,6 +293,18 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     return OracleRun([int(v) for v in I[:r]], [int(v) for v in J[:r]], STATUS_NAMES[res.status], res.final_rho,
                      res.threshold, list(rhos[:k]), [int(v) for v in widths[:k]], res.note.decode(),
                      res.sketch_s, res.total_s, res.ga_norm, res.c, steps, list(iter_s[:k]))
+
+
+def slupp_cur(a, rank, seed=0):
+    """One-shot s-LUPP CUR baseline (proj/src/baselines.cpp:39-62): (row_indices, col_indices)."""
+    a = _colmajor(a)
+    m, n = a.shape
+    cap = max(int(rank), 1)
+    I = np.zeros(cap, dtype=np.int64)
+    J = np.zeros(cap, dtype=np.int64)
+    k = C.c_int64()
+    _check(lib().oracle_slupp_cur(_dp(a), m, n, max(m, 1), int(rank), int(seed), _i64p(I), _i64p(J), C.byref(k)))
+    return [int(v) for v in I[:k.value]], [int(v) for v in J[:k.value]]
 
 
 def true_relative_error(a, row_indices, col_indices) -> float:

@@ -284,6 +284,42 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     return _collect(out.value, None)
 
 
+def slupp_cur(a, rank, seed=0) -> CurFactors:
+    """One-shot s-LUPP CUR baseline (proj/src/baselines.cpp:39-62, binding module.cpp:106-108):
+    one Gaussian sketch of ceil(1.1 r) rows on stream SluppSketch, r LUPP column pivots, LUPP
+    row pivots on A(:, J) — i.e. one block of the engine's iteration with b = r and no
+    stopping test. Raises ValueError outside [0, min(m, n)] and RuntimeError("singular cross
+    block") as the reference does."""
+    h = _as_handle(a)
+    r = int(rank)
+    if r < 0 or r > min(h.rows, h.cols):
+        raise ValueError("rank must lie in [0, min(m, n)]")
+    if r == 0:
+        return CurFactors(None, [], [])
+    cfg = _config(0.0, r, 0.0, 0.05, False, r, 1, "lupp", "lupp", 1e-13, seed, "gaussian", 8, False)
+    cfg.sketch_stream = 2
+    cfg.sketch_rows = (11 * r + 9) // 10
+    L = _lib()
+    out = C.c_void_p()
+    if h.is_device:
+        import torch
+
+        t = h._tensor
+        with torch.cuda.device(t.device):
+            stream = torch.cuda.current_stream(t.device).cuda_stream
+            _check(L.itercur_iterative_cur_device(C.c_void_p(t.data_ptr()), h.rows, h.cols, h.lda, C.byref(cfg),
+                                                  C.c_void_p(stream), C.byref(out)))
+        factors, trace = _collect(out.value, h)
+    else:
+        host = h._host
+        _check(L.itercur_iterative_cur_host(host.ctypes.data_as(C.c_void_p), h.rows, h.cols, max(h.rows, 1),
+                                            C.byref(cfg), C.byref(out)))
+        factors, trace = _collect(out.value, None)
+    if factors.rank == 0:
+        raise RuntimeError("singular cross block")
+    return factors
+
+
 def true_relative_error(a, factors: CurFactors) -> float:
     """||A - CUR||_F / ||A||_F (proj/src/driver.cpp:169-190), evaluated on the device from the
     run's factors (A is the matrix the factors were computed from)."""
@@ -315,6 +351,6 @@ def sketch_rows_for_block(b: int) -> int:
 
 
 __all__ = [
-    "CurFactors", "IterationRecord", "MatrixHandle", "RunTrace", "__version__", "adjusted_threshold",
+    "CurFactors", "IterationRecord", "MatrixHandle", "RunTrace", "__version__", "adjusted_threshold", "slupp_cur",
     "gratton_tail", "iterative_cur", "sketch_rows_for_block", "true_relative_error",
 ]

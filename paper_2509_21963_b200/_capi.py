@@ -38,7 +38,7 @@ class Config(C.Structure):
         ("risk_adjust", C.c_int32), ("max_rank", C.c_int64), ("max_iters", C.c_int64),
         ("col_method", C.c_int32), ("row_method", C.c_int32), ("pivot_floor", C.c_double),
         ("seed", C.c_uint64), ("sketch_kind", C.c_int32), ("sparse_nnz", C.c_int32),
-        ("profile", C.c_int32), ("reserved", C.c_int32),
+        ("profile", C.c_int32), ("sketch_stream", C.c_int32), ("sketch_rows", C.c_int64),
     ]
 
 

@@ -330,7 +330,8 @@ void run_iterative_cur(itercur_run* run) {
   const int64_t min_dim = std::min(m, n);
   const int64_t max_rank = cfg.max_rank > 0 ? std::min(cfg.max_rank, min_dim) : min_dim;
   const int64_t max_iters = cfg.max_iters > 0 ? cfg.max_iters : (min_dim + b - 1) / b + 1;
-  const int64_t c = sketch_rows(b);
+  const int64_t c = cfg.sketch_rows > 0 ? cfg.sketch_rows : sketch_rows(b);
+  if (c < b) fail(ITERCUR_E_INVALID_ARGUMENT, "sketch rows must be at least the block size");
   const int64_t cp = round_up(c, 8);
   run->c = c;
   run->cp = cp;
@@ -353,7 +354,8 @@ void run_iterative_cur(itercur_run* run) {
     CK(launch_gen_sketch_operator(ws.S.p, cp, ldg, c, m, cfg.seed, cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN
                                                                        ? kSketchSparseSign
                                                                        : kSketchGaussian,
-                                  cfg.sparse_nnz, st));
+                                  cfg.sparse_nnz, st,
+                                  cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch));
     run->launches += 1;
     const int64_t wse = sketch_workspace_elems(m, n, cp);
     ws.sk_ws.alloc(wse);

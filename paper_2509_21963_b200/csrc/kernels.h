@@ -8,6 +8,7 @@
 namespace itercur_b200 {
 
 constexpr uint32_t kStreamSketch = 1;      // RngStream::Sketch, proj/include/itercur/rng.hpp:13
+constexpr uint32_t kStreamSluppSketch = 2; // RngStream::SluppSketch (the s-LUPP baseline, baselines.cpp:44-46)
 constexpr uint32_t kStreamSparseSign = 7;  // new tag
 constexpr int kSketchGaussian = 0;
 constexpr int kSketchSparseSign = 1;
@@ -59,7 +60,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 // columns k >= m are zero. Gaussian: S(h,k) = normal_at(seed, Sketch, h, k)
 // (proj/src/sketch.cpp:19 -> rng.cpp:61-67). Sparse-sign: +-1 at the A.8 positions.
 cudaError_t launch_gen_sketch_operator(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed,
-                                       int kind, int zeta, cudaStream_t st);
+                                       int kind, int zeta, cudaStream_t st, uint32_t stream_tag = kStreamSketch);
 
 struct SketchStats {
   double* d_asq;  // ||A||_F^2 (device scalar)

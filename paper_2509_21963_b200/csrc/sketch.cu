@@ -28,11 +28,12 @@ namespace itercur_b200 {
 // One thread per (h, k) for the Gaussian sketch; one thread per column k of Omega for
 // the sparse-sign sketch (partial Fisher-Yates over [0,c), one Philox
 // block per slot, sign = low bit of word 1).
-__global__ void gen_gaussian_kernel(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed) {
+__global__ void gen_gaussian_kernel(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed,
+                                    uint32_t stream) {
   const int64_t total = rows_pad * ldg;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t h = e / ldg, k = e - h * ldg;
-    S[e] = (h < c && k < m) ? normal_at_dev(seed, kStreamSketch, h, k) : 0.0;
+    S[e] = (h < c && k < m) ? normal_at_dev(seed, stream, h, k) : 0.0;
   }
 }
 
@@ -76,11 +77,11 @@ __global__ void gen_sparse_sign_kernel(double* S, int64_t ldg, int64_t c, int64_
 }
 
 cudaError_t launch_gen_sketch_operator(double* S, int64_t rows_pad, int64_t ldg, int64_t c, int64_t m, uint64_t seed,
-                                       int kind, int zeta, cudaStream_t st) {
+                                       int kind, int zeta, cudaStream_t st, uint32_t stream_tag) {
   if (kind == kSketchGaussian) {
     const int64_t total = rows_pad * ldg;
     const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 16));
-    gen_gaussian_kernel<<<blocks, 256, 0, st>>>(S, rows_pad, ldg, c, m, seed);
+    gen_gaussian_kernel<<<blocks, 256, 0, st>>>(S, rows_pad, ldg, c, m, seed, stream_tag);
   } else {
     cudaError_t e = cudaMemsetAsync(S, 0, sizeof(double) * rows_pad * ldg, st);
     if (e != cudaSuccess) return e;

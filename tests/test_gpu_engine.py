@@ -211,3 +211,29 @@ def test_device_entry_with_torch_tensor(engine, oracle):
 def test_closed_forms(engine):  # test_smoke.py:65-69
     assert engine.adjusted_threshold(1.0, 0.0, 1e-10, 100) == pytest.approx(1 / 4.98, rel=5e-4)
     assert engine.gratton_tail(4, math.sqrt(2.0)) == pytest.approx(math.exp(-0.25))
+
+
+# ------------------------- s-LUPP one-shot baseline (proj/src/baselines.cpp:39-62) ---------
+def test_slupp_recovers_exact_rank(engine, oracle):  # proj/tests/test_baselines.cpp:53-57
+    a = oracle.random_gaussian(60, 7, 11) @ oracle.random_gaussian(50, 7, 12).T
+    f = engine.slupp_cur(a, 7, 13)
+    assert f.rank == 7
+    assert engine.true_relative_error(a, f) <= 1e-10
+
+
+@pytest.mark.parametrize("rank,seed", [(10, 0), (25, 3), (64, 1)])
+def test_slupp_matches_oracle(engine, oracle, rank, seed):
+    rng = np.random.default_rng(rank)
+    a = exp_decay(300, 10 ** (-1 / 30), rng)[:, :240]
+    f = engine.slupp_cur(a, rank, seed)
+    I, J = oracle.slupp_cur(a, rank, seed)
+    assert f.row_indices == I and f.col_indices == J
+    err = engine.true_relative_error(a, f)
+    assert abs(err - oracle.true_relative_error(a, I, J)) <= 1e-8
+
+
+def test_slupp_validation(engine, oracle):
+    a = oracle.random_dense(10, 8, 3)
+    with pytest.raises(ValueError, match="rank must lie"):
+        engine.slupp_cur(a, 9)
+    assert engine.slupp_cur(a, 0).rank == 0

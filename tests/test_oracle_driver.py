@@ -132,3 +132,12 @@ def test_sparse_sign_run_converges(oracle):
     r = oracle.iterative_cur(a, epsilon=1e-8, b=5, seed=7, sketch="sparse_sign")
     assert r.status == "Converged" and r.rank == 10
     assert oracle.true_relative_error(a, r.row_indices, r.col_indices) <= 1e-10
+
+
+def test_oracle_slupp_exact_rank(oracle):  # proj/tests/test_baselines.cpp:53-57
+    a = oracle.random_gaussian(60, 7, 11) @ oracle.random_gaussian(50, 7, 12).T
+    I, J = oracle.slupp_cur(a, 7, 13)
+    assert len(I) == 7 and len(J) == 7
+    assert oracle.true_relative_error(a, I, J) <= 1e-10
+    with pytest.raises(Exception, match="rank must lie"):
+        oracle.slupp_cur(a, 51, 0)
