@@ -175,6 +175,13 @@ ITERCUR_API int itercur_select_device(const double* dM, int64_t rows, int64_t co
                           double* second_out, void* stream);
 /* Time the sketch-apply DMMA kernel alone (CUDA events on `stream`), `reps` launches;
    returns the mean milliseconds per launch and the kernel's launch geometry. */
+/* The same selections by QRCP (greedy orthogonalised column norms, select.cpp:79-117):
+ * candidates are the columns of M (is_columns=1, select.cpp:121-139) or its rows
+ * (select.cpp:141-165); second_out entries are -1 (no runner-up is tracked). */
+ITERCUR_API int itercur_select_qrcp_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b,
+                                           int32_t is_columns, double pivot_floor, const int64_t* exclude,
+                                           int64_t n_exclude, int64_t* idx_out, int64_t* n_idx, int32_t* truncated,
+                                           double* last_pivot, double* best_out, double* second_out, void* stream);
 ITERCUR_API int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, int32_t kind,
                                int32_t reps, void* stream, double* ms_per_launch, int32_t* ctas, int32_t* splits,
                                int32_t* uses_tma);

@@ -227,8 +227,7 @@ int64_t sketch_rows(int64_t b) { return (11 * b) / 10; }  // proj/include/itercu
 
 void check_method(int32_t kind) {
   if (kind == ITERCUR_PIVOT_OSINSKY) fail(ITERCUR_E_RUNTIME, "Osinsky selection not implemented");
-  if (kind == ITERCUR_PIVOT_QRCP) fail(ITERCUR_E_RUNTIME, "QRCP selection not implemented in the B200 engine");
-  if (kind != ITERCUR_PIVOT_LUPP) fail(ITERCUR_E_LOGIC, "unknown selection method");
+  if (kind != ITERCUR_PIVOT_LUPP && kind != ITERCUR_PIVOT_QRCP) fail(ITERCUR_E_LOGIC, "unknown selection method");
 }
 
 // ||A||_F^2 via a dedicated pass (only used when validation must report in the reference's
@@ -247,7 +246,8 @@ double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cud
 struct Workspace {
   DevBuf<double> Y, Wc, Wr, Bg, Ut, Yg, lu, part, sk_ws, S;
   DevBuf<uint8_t> col_mask, row_mask;
-  DevBuf<char> state, lupp_scratch;
+  DevBuf<char> state, lupp_scratch, qrcp_scratch;
+  DevBuf<double> Wq;  // Y copy for the QRCP column selection (qrcp_pivot_cols takes W by value)
   DevBuf<double> scal;  // [0] asq, [1] ysq
   DevBuf<unsigned long long> nonfinite;
   char* h_state = nullptr;  // pinned mirror (thread-local cache, see pinned_state)
@@ -420,6 +420,9 @@ void run_iterative_cur(itercur_run* run) {
   CK(cudaMemsetAsync(ws.col_mask.p, 0, n, st));
   CK(cudaMemsetAsync(ws.row_mask.p, 0, m, st));
   ws.lupp_scratch.alloc(lupp_scratch_bytes(B));
+  const bool col_qrcp = cfg.col_method == ITERCUR_PIVOT_QRCP, row_qrcp = cfg.row_method == ITERCUR_PIVOT_QRCP;
+  if (col_qrcp || row_qrcp) ws.qrcp_scratch.alloc(qrcp_scratch_bytes());
+  if (col_qrcp) ws.Wq.alloc(static_cast<size_t>(cp) * n);
   // iterations are enqueued in batches of kBatch without a host round trip; the loop control
   // (budgets, stop tests, rank) lives on the device (IterCtl), and every kernel of an
   // iteration after the stop returns immediately.
@@ -589,7 +592,7 @@ void run_iterative_cur(itercur_run* run) {
           la.d_gen_k = &d_ctl->k;
           la.gen_base = gen_base;
           la.gen_which = 0;
-          col_fused = fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
+          col_fused = !col_qrcp && fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
           if (col_fused) {
             la.begin_ctl = d_ctl;
             la.begin_slot = slot;
@@ -598,7 +601,14 @@ void run_iterative_cur(itercur_run* run) {
           } else {
             CK(launch_iter_begin(d_ctl, slot, st));
           }
-          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+          if (col_qrcp) {  // QRCP over the c-row columns of (a copy of) Y, select.cpp:79-117,121-139
+            CK(cudaMemcpyAsync(ws.Wq.p, ws.Y.p, sizeof(double) * cp * n, cudaMemcpyDeviceToDevice, st));
+            CK(run_qrcp(ws.Wq.p, n, static_cast<int>(c), nullptr, 1, cp, &d_ctl->block, B, ws.col_mask.p, epoch,
+                        &d_ctl->ysq, cfg.pivot_floor, arr.col_idx, arr.col_best, arr.col_second, &slot->ncols,
+                        nullptr, nullptr, ws.qrcp_scratch.p, d_ctl, st));
+          } else {
+            CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
+          }
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 1), st));
 
@@ -661,9 +671,16 @@ void run_iterative_cur(itercur_run* run) {
           la.lu_out = run->Dinv.p;
           la.lu_ld = run->bmax;
           la.d_lu_r = &d_ctl->r;
-          row_fused = fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
+          row_fused = !row_qrcp && fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
           if (row_fused) la.post[0] = {run->L.p, run->ldL, 1, ldbg, &d_ctl->r, ws.Bg.p, ldbg, B};  // L(I_k, :)
-          CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, &row_lupp_path));
+          if (row_qrcp) {  // QRCP over the rows of S_row (select.cpp:141-165); D_k by cross_lu below
+            row_lupp_path = 0;
+            CK(run_qrcp(ws.Wr.p, m, B, &slot->ncols, ldm, 1, &slot->ncols, B, ws.row_mask.p, epoch, nullptr,
+                        cfg.pivot_floor, arr.row_idx, arr.row_best, arr.row_second, &slot->nrows, &slot->width,
+                        &slot->ncols, ws.qrcp_scratch.p, d_ctl, st));
+          } else {
+            CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, &row_lupp_path));
+          }
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 3), st));
 
@@ -1178,10 +1195,10 @@ int itercur_sketch_device(const double* dA, int64_t m, int64_t n, int64_t lda, i
   });
 }
 
-int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b, int32_t is_columns,
-                          double pivot_floor, const int64_t* exclude, int64_t n_exclude, int64_t* idx_out,
-                          int64_t* n_idx, int32_t* truncated, double* last_pivot, double* best_out,
-                          double* second_out, void* stream) {
+static int select_impl(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b, int32_t is_columns,
+                       double pivot_floor, const int64_t* exclude, int64_t n_exclude, int64_t* idx_out, int64_t* n_idx,
+                       int32_t* truncated, double* last_pivot, double* best_out, double* second_out, void* stream,
+                       int32_t method) {
   return guarded([&] {
     require_device();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1226,8 +1243,13 @@ int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t 
     DevBuf<uint8_t> mask;
     DevBuf<char> scratch, outs;
     const int64_t ldw = even(wrows);
-    W.alloc(static_cast<size_t>(ldw) * steps);
-    if (is_columns)
+    const bool qrcp = method == ITERCUR_PIVOT_QRCP;
+    const int64_t ldq = even(rows);  // QRCP works on a copy of M itself
+    W.alloc(qrcp ? static_cast<size_t>(ldq) * cols : static_cast<size_t>(ldw) * steps);
+    if (qrcp)
+      CK(cudaMemcpy2DAsync(W.p, sizeof(double) * ldq, dM, sizeof(double) * ldm, sizeof(double) * rows, cols,
+                           cudaMemcpyDeviceToDevice, st));
+    else if (is_columns)
       CK(launch_transpose_rows(dM, ldm, cols, static_cast<int>(steps), W.p, ldw, st));
     else
       CK(cudaMemcpy2DAsync(W.p, sizeof(double) * ldw, dM, sizeof(double) * ldm, sizeof(double) * rows, steps,
@@ -1258,7 +1280,16 @@ int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t 
     la.d_best = d_best;
     la.d_second = d_second;
     la.d_count = d_count;
-    CK(run_lupp_with_scratch(la, scratch.p, st, nullptr));
+    if (qrcp) {  // candidates: columns of M (select_columns) or rows of M (select_rows)
+      DevBuf<char> qs;
+      qs.alloc(qrcp_scratch_bytes());
+      CK(run_qrcp(W.p, wrows, static_cast<int>(wcols), nullptr, is_columns ? 1 : ldq, is_columns ? ldq : 1, nullptr, S,
+                  mask.p, 2, scal.p, pivot_floor, d_idx, d_best, d_second, d_count, nullptr, nullptr, qs.p, nullptr,
+                  st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      CK(run_lupp_with_scratch(la, scratch.p, st, nullptr));
+    }
     std::vector<char> h(outs.count);
     CK(cudaMemcpyAsync(h.data(), outs.p, outs.count, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1275,6 +1306,22 @@ int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t 
     *last_pivot = cnt > 0 ? hb[cnt - 1] : 0.0;
     *truncated = cnt < b ? 1 : 0;
   });
+}
+
+int itercur_select_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b, int32_t is_columns,
+                          double pivot_floor, const int64_t* exclude, int64_t n_exclude, int64_t* idx_out,
+                          int64_t* n_idx, int32_t* truncated, double* last_pivot, double* best_out,
+                          double* second_out, void* stream) {
+  return select_impl(dM, rows, cols, ldm, b, is_columns, pivot_floor, exclude, n_exclude, idx_out, n_idx, truncated,
+                     last_pivot, best_out, second_out, stream, ITERCUR_PIVOT_LUPP);
+}
+
+int itercur_select_qrcp_device(const double* dM, int64_t rows, int64_t cols, int64_t ldm, int64_t b,
+                               int32_t is_columns, double pivot_floor, const int64_t* exclude, int64_t n_exclude,
+                               int64_t* idx_out, int64_t* n_idx, int32_t* truncated, double* last_pivot,
+                               double* best_out, double* second_out, void* stream) {
+  return select_impl(dM, rows, cols, ldm, b, is_columns, pivot_floor, exclude, n_exclude, idx_out, n_idx, truncated,
+                     last_pivot, best_out, second_out, stream, ITERCUR_PIVOT_QRCP);
 }
 
 int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t lda, int64_t b, int32_t kind,

@@ -132,6 +132,15 @@ struct LuppArgs {
     int w_fill = 0;
   } post[2];
 };
+// QRCP selection (qrcp.cu, select.cpp:79-117): candidates are the ncand vectors of length len
+// at W[i*rs + j*cs] (modified in place); same outputs as the LUPP launchers.
+struct IterCtl;
+size_t qrcp_scratch_bytes();
+cudaError_t run_qrcp(double* W, int64_t ncand, int len, const int* d_len, int64_t rs, int64_t cs, const int* d_steps,
+                     int steps_max,
+                     uint8_t* mask, uint8_t epoch, const double* d_norm_sq, double pivot_floor, int64_t* d_idx,
+                     double* d_best, double* d_second, int* d_count, int* d_width_out, const int* d_width_cap,
+                     void* scratch, const IterCtl* ctl, cudaStream_t st);
 // true when run_lupp_with_scratch takes the cluster path for these arguments (which honours
 // begin_ctl / post gathers; the other paths ignore them and the caller launches them itself)
 bool lupp_fuses_iteration_work(const LuppArgs& a);

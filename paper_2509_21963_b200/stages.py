@@ -66,7 +66,7 @@ class Selection:
     second: list
 
 
-def _select(m: torch.Tensor, b: int, is_columns: bool, pivot_floor: float, exclude) -> Selection:
+def _select(m: torch.Tensor, b: int, is_columns: bool, pivot_floor: float, exclude, method: str = "lupp") -> Selection:
     rows, cols = m.shape
     ex = np.asarray(list(exclude), dtype=np.int64)
     cap = max(int(b), 1) + 1
@@ -76,7 +76,10 @@ def _select(m: torch.Tensor, b: int, is_columns: bool, pivot_floor: float, exclu
     nidx, trunc, last = C.c_int64(), C.c_int32(), C.c_double()
     i64p = C.POINTER(C.c_int64)
     dp = C.POINTER(C.c_double)
-    _check(_capi.lib().itercur_select_device(
+    if method not in ("lupp", "qrcp"):
+        raise ValueError(f"unknown selection method '{method}'")
+    fn = _capi.lib().itercur_select_device if method == "lupp" else _capi.lib().itercur_select_qrcp_device
+    _check(fn(
         C.c_void_p(m.data_ptr()), rows, cols, _colmajor_ld(m), int(b), 1 if is_columns else 0, float(pivot_floor),
         ex.ctypes.data_as(i64p), len(ex), idx.ctypes.data_as(i64p), C.byref(nidx), C.byref(trunc), C.byref(last),
         best.ctypes.data_as(dp), second.ctypes.data_as(dp), _stream(m)))
@@ -84,12 +87,12 @@ def _select(m: torch.Tensor, b: int, is_columns: bool, pivot_floor: float, exclu
     return Selection([int(v) for v in idx[:k]], bool(trunc.value), last.value, list(best[:k]), list(second[:k]))
 
 
-def select_columns(m: torch.Tensor, b: int, pivot_floor: float = 1e-13, exclude=()) -> Selection:
-    return _select(m, b, True, pivot_floor, exclude)
+def select_columns(m: torch.Tensor, b: int, pivot_floor: float = 1e-13, exclude=(), method="lupp") -> Selection:
+    return _select(m, b, True, pivot_floor, exclude, method)
 
 
-def select_rows(m: torch.Tensor, b: int, pivot_floor: float = 1e-13, exclude=()) -> Selection:
-    return _select(m, b, False, pivot_floor, exclude)
+def select_rows(m: torch.Tensor, b: int, pivot_floor: float = 1e-13, exclude=(), method="lupp") -> Selection:
+    return _select(m, b, False, pivot_floor, exclude, method)
 
 
 def time_sketch_kernel(a: torch.Tensor, b: int, kind: str = "gaussian", reps: int = 5):

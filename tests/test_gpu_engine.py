@@ -237,3 +237,15 @@ def test_slupp_validation(engine, oracle):
     with pytest.raises(ValueError, match="rank must lie"):
         engine.slupp_cur(a, 9)
     assert engine.slupp_cur(a, 0).rank == 0
+
+
+@pytest.mark.parametrize("cm,rm", [("qrcp", "qrcp"), ("qrcp", "lupp"), ("lupp", "qrcp")])
+def test_qrcp_methods_match_oracle(engine, oracle, cm, rm):
+    a = low_rank_plus_noise(oracle, 260, 200, 30, 1e-10, 51)
+    kw = dict(epsilon=1e-8, b=8, seed=3, col_method=cm, row_method=rm)
+    f, t = engine.iterative_cur(a, **kw)
+    o = oracle.iterative_cur(a, **kw)
+    assert t.status == o.status
+    assert f.row_indices == list(o.row_indices) and f.col_indices == list(o.col_indices)
+    err = engine.true_relative_error(a, f)
+    assert abs(err - oracle.true_relative_error(a, o.row_indices, o.col_indices)) <= 1e-8

@@ -126,3 +126,34 @@ def test_lupp_reference_cases(engine, oracle):
     m[:4, :] = 0.0
     got = S.select_rows(S.colmajor(m), 2, exclude=[0, 1, 2, 3])
     assert all(i >= 4 for i in got.indices) and len(got.indices) == 2
+
+
+# ------------------------- QRCP selection (proj/src/select.cpp:79-117) -------------------------
+@pytest.mark.parametrize("shape,b,is_cols", [((22, 500), 20, True), ((35, 2000), 32, True), ((700, 24), 24, False),
+                                             ((300, 12), 9, False)])
+def test_qrcp_selection_matches_oracle(oracle, shape, b, is_cols):
+    import torch
+
+    from paper_2509_21963_b200 import stages
+    rng = np.random.default_rng(shape[0] * 7 + b)
+    m = rng.standard_normal(shape) * (0.9 ** np.arange(shape[1]))[None, :]
+    ex = [3, 7] if not is_cols else [1, 5, 11]
+    t = torch.from_numpy(np.asfortranarray(m)).cuda().t().contiguous().t()
+    fn_d = stages.select_columns if is_cols else stages.select_rows
+    fn_o = oracle.select_columns if is_cols else oracle.select_rows
+    got = fn_d(t, b, exclude=ex, method="qrcp")
+    ref = fn_o(m, b, method="qrcp", exclude=ex)
+    assert got.indices == ref.indices
+    assert np.allclose(got.best, ref.best, rtol=1e-13, atol=0)
+
+
+def test_qrcp_reference_cases(oracle):  # proj/tests/test_select.cpp:32-50
+    import torch
+
+    from paper_2509_21963_b200 import stages
+    m = np.array([[1.0, 0.0, 3.0], [0.0, 2.0, 4.0]])
+    t = torch.from_numpy(np.asfortranarray(m)).cuda().t().contiguous().t()
+    assert stages.select_columns(t, 1, method="qrcp").indices == [2]
+    r = oracle.random_dense(6, 9, 17)
+    t = torch.from_numpy(np.asfortranarray(r)).cuda().t().contiguous().t()
+    assert stages.select_columns(t, 5, method="qrcp").indices == oracle.select_columns(r, 5, method="qrcp").indices
