@@ -194,6 +194,12 @@ ITERCUR_API int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int
 
 /* Time the tall-skinny DMMA GEMM C = A(:,idx) - L * B (the row-residual shape) on random
    data: M x K times K x N, `reps` launches; returns microseconds per launch. */
+/* CSR input (MatrixHandle sparse path, proj/src/matrix.cpp:79-104): scatter a validated CSR
+ * matrix (int64 row_ptr / col_idx, double values, all device pointers) into a dense column-major
+ * rows x cols buffer (ld >= rows) that the dense entries then take. */
+ITERCUR_API int itercur_csr_to_dense_device(int64_t rows, int64_t cols, const int64_t* dRowPtr, const int64_t* dColIdx,
+                                            const double* dValues, double* dOut, int64_t ld, void* stream);
+
 /* ---- column-sharded engine building blocks (paper_2509_21963_b200/sharded.py) ----
  * One pivot step of the distributed column LUPP on this rank's rows of W = Y^T (select.cpp:34-74):
  * eliminate the live rows with the previous step's pivot row dPivotRow (NULL at s == 0; the pivot's

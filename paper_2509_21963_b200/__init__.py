@@ -47,13 +47,58 @@ class MatrixHandle:
     ``torch.empty(n, m, device="cuda", dtype=torch.float64).t()``.
     """
 
-    def __init__(self, host=None, tensor=None):
+    def __init__(self, host=None, tensor=None, csr=None, shape=None):
         self._host = host
         self._tensor = tensor
+        self._csr = csr  # (row_ptr, col_idx, values) int64 / int64 / float64 numpy arrays
         if host is not None:
             self.rows, self.cols = host.shape
-        else:
+        elif tensor is not None:
             self.rows, self.cols = int(tensor.shape[0]), int(tensor.shape[1])
+        else:
+            self.rows, self.cols = shape
+
+    @staticmethod
+    def sparse_csr(rows, cols, indptr, indices, data) -> "MatrixHandle":
+        """CSR matrix (binding module.cpp:40-48 -> matrix.cpp:79-104), validated as the
+        reference validates it. The engine densifies it on the device before a run."""
+        rows, cols = int(rows), int(cols)
+        if rows < 0 or cols < 0:
+            raise ValueError("negative matrix dimension")
+        rp = np.asarray(indptr, dtype=np.int64)
+        ci = np.asarray(indices, dtype=np.int64)
+        v = np.asarray(data, dtype=np.float64)
+        if rp.shape != (rows + 1,):
+            raise ValueError("row_ptr must have rows+1 entries")
+        if rp[0] != 0 or rp[-1] != v.size:
+            raise ValueError("row_ptr must start at 0 and end at nnz")
+        if ci.size != v.size:
+            raise ValueError("col_idx and values must have equal length")
+        if np.any(np.diff(rp) < 0):
+            raise ValueError("row_ptr must be nondecreasing")
+        bad = np.nonzero((ci < 0) | (ci >= cols))[0]
+        if bad.size:
+            raise IndexError(f"csr column index {int(ci[bad[0]])} out of range [0, {cols})")
+        for i in range(rows):
+            seg = ci[rp[i]:rp[i + 1]]
+            if seg.size > 1 and np.any(np.diff(seg) <= 0):
+                raise ValueError("csr column indices must be strictly increasing within each row")
+        if not np.all(np.isfinite(v)):
+            raise ValueError("matrix contains non-finite entries")
+        return MatrixHandle(csr=(rp, ci, v), shape=(rows, cols))
+
+    def _densified_on_device(self) -> "MatrixHandle":
+        """The CSR matrix scattered into a dense column-major device buffer (B200 kernel)."""
+        import torch
+
+        rp, ci, v = (torch.from_numpy(x).cuda() for x in self._csr)
+        out = torch.empty(max(self.cols, 1), max(self.rows, 1), dtype=torch.float64, device="cuda").t()
+        out = out[:self.rows, :self.cols]
+        stream = torch.cuda.current_stream().cuda_stream
+        _check(_lib().itercur_csr_to_dense_device(self.rows, self.cols, C.c_void_p(rp.data_ptr()),
+                                                  C.c_void_p(ci.data_ptr()), C.c_void_p(v.data_ptr()),
+                                                  C.c_void_p(out.data_ptr()), max(self.rows, 1), C.c_void_p(stream)))
+        return MatrixHandle(tensor=out)
 
     @staticmethod
     def dense(array) -> "MatrixHandle":
@@ -79,7 +124,7 @@ class MatrixHandle:
 
     @property
     def is_sparse(self) -> bool:
-        return False
+        return self._csr is not None
 
     @property
     def is_device(self) -> bool:
@@ -87,7 +132,7 @@ class MatrixHandle:
 
     @property
     def nnz(self) -> int:
-        return self.rows * self.cols
+        return int(self._csr[2].size) if self._csr is not None else self.rows * self.cols
 
     @property
     def lda(self) -> int:
@@ -96,6 +141,12 @@ class MatrixHandle:
         return max(self.rows, 1)
 
     def to_numpy(self) -> np.ndarray:
+        if self._csr is not None:
+            rp, ci, v = self._csr
+            out = np.zeros((self.rows, self.cols), order="F")
+            for i in range(self.rows):
+                out[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+            return out
         if self._host is not None:
             return np.array(self._host)
         return self._tensor.detach().cpu().numpy()
@@ -109,7 +160,7 @@ class MatrixHandle:
 
 def _as_handle(a) -> MatrixHandle:
     if isinstance(a, MatrixHandle):
-        return a
+        return a._densified_on_device() if a.is_sparse else a
     try:
         import torch
 

@@ -29,7 +29,7 @@ EXPORTED = [
     "itercur_gaussian_matrix_device", "itercur_sketch_device", "itercur_select_device",
     "itercur_time_sketch_kernel", "itercur_time_lupp", "itercur_time_gemm",
     "itercur_lupp_dist_step", "itercur_gemm_device", "itercur_block_lu_device", "itercur_rows_lu_solve_device",
-    "itercur_select_qrcp_device",
+    "itercur_select_qrcp_device", "itercur_csr_to_dense_device",
 ]
 
 
@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
                                             C.c_int32, vp, dp, dp, vp]),
         "itercur_select_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_double,
                                             i64p, C.c_int64, i64p, i64p, i32p, dp, dp, dp, vp]),
+        "itercur_csr_to_dense_device": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]),
         "itercur_select_qrcp_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                                  C.c_double, i64p, C.c_int64, i64p, i64p, i32p, dp, dp, dp, vp]),
         "itercur_time_sketch_kernel": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32,

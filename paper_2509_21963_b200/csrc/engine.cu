@@ -1453,6 +1453,18 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
   });
 }
 
+int itercur_csr_to_dense_device(int64_t rows, int64_t cols, const int64_t* dRowPtr, const int64_t* dColIdx,
+                                const double* dValues, double* dOut, int64_t ld, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (rows < 0 || cols < 0 || ld < std::max<int64_t>(rows, 1))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "csr_to_dense: invalid shape or leading dimension");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(cudaMemsetAsync(dOut, 0, sizeof(double) * ld * cols, st));
+    CK(launch_csr_to_dense(rows, dRowPtr, dColIdx, dValues, dOut, ld, st));
+  });
+}
+
 int itercur_lupp_dist_step(double* dW, int64_t rows, int64_t ldw, int32_t steps, int32_t s, const double* dPivotRow,
                            int64_t pivot_local_row, uint8_t* dLive, int64_t row_offset, double* dCand, void* stream) {
   return guarded([&] {

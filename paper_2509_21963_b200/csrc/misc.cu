@@ -289,6 +289,22 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
   return cudaGetLastError();
 }
 
+// CSR (row_ptr, col_idx, values; proj/src/matrix.cpp:79-104 layout) -> dense column-major
+// (the output must be zeroed by the caller); one thread per row.
+__global__ void csr_to_dense_kernel(int64_t rows, const int64_t* __restrict__ row_ptr,
+                                    const int64_t* __restrict__ col_idx, const double* __restrict__ values,
+                                    double* __restrict__ out, int64_t ld) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) out[i + col_idx[p] * ld] = values[p];
+}
+cudaError_t launch_csr_to_dense(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                double* out, int64_t ld, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows, 256), 148 * 8));
+  csr_to_dense_kernel<<<blocks, 256, 0, st>>>(rows, row_ptr, col_idx, values, out, ld);
+  return cudaGetLastError();
+}
+
 // Sum `count` partials into *out in a fixed order (one CTA).
 __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t count, double* __restrict__ out,
                                     const IterCtl* __restrict__ ctl) {

@@ -100,4 +100,7 @@ cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, 
                           uint8_t* row_mask, uint8_t* col_mask, const double* y_partials, int64_t y_parts,
                           cudaStream_t st);
 
+cudaError_t launch_csr_to_dense(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                double* out, int64_t ld, cudaStream_t st);
+
 }  // namespace itercur_b200

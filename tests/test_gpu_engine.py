@@ -249,3 +249,14 @@ def test_qrcp_methods_match_oracle(engine, oracle, cm, rm):
     assert f.row_indices == list(o.row_indices) and f.col_indices == list(o.col_indices)
     err = engine.true_relative_error(a, f)
     assert abs(err - oracle.true_relative_error(a, o.row_indices, o.col_indices)) <= 1e-8
+
+
+def test_sparse_csr_input_matches_dense(engine, oracle):  # MatrixHandle.sparse_csr path
+    a = low_rank_plus_noise(oracle, 120, 90, 8, 1e-10, 61)
+    a[np.abs(a) < 0.5 * np.abs(a).mean()] = 0.0
+    rows, cols = np.nonzero(a)
+    indptr = np.searchsorted(rows, np.arange(a.shape[0] + 1))
+    h = engine.MatrixHandle.sparse_csr(a.shape[0], a.shape[1], indptr, cols, a[rows, cols])
+    f, t = engine.iterative_cur(h, epsilon=1e-6, b=5, seed=1)
+    f2, t2 = engine.iterative_cur(a, epsilon=1e-6, b=5, seed=1)
+    assert f.row_indices == f2.row_indices and f.col_indices == f2.col_indices and t.status == t2.status
