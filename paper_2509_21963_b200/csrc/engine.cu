@@ -498,7 +498,7 @@ void run_iterative_cur(itercur_run* run) {
     p.norm_part = ws.part.p;
     return p;
   };
-  const bool fused_ub = getenv("ITERCUR_NO_FUSED_UBLOCK") == nullptr && [&] {
+  const bool fused_ub = !env_flag("ITERCUR_NO_FUSED_UBLOCK") && [&] {
     IterState* slot0 = reinterpret_cast<IterState*>(slots);
     TsGemmParams p = ublock_params(run->capL, slot0, iter_arrays(slot0, B));
     p.norm_part = reinterpret_cast<double*>(16);  // placeholder: allocated below
@@ -514,7 +514,7 @@ void run_iterative_cur(itercur_run* run) {
   const uint8_t epoch = 2;  // the global-memory LUPP clears its in-call marks, so one epoch suffices
   static uint32_t run_counter = 0;
   const uint32_t gen_base = ((++run_counter) & 0x3FFu) << 21;  // LUPP slot-tag generations
-  const bool use_graph = !evs.on && getenv("ITERCUR_NO_GRAPH") == nullptr;
+  const bool use_graph = !evs.on && !env_flag("ITERCUR_NO_GRAPH");
   cudaGraphExec_t graph_exec = nullptr;
   int64_t graph_cap = -1;
   struct ExecGuard {
@@ -528,7 +528,7 @@ void run_iterative_cur(itercur_run* run) {
   int64_t ev_i = 2;
   std::vector<size_t> iter_events;
   bool done = false;
-  static const bool host_trace = getenv("ITERCUR_HOST_TRACE") != nullptr;
+  static const bool host_trace = env_flag("ITERCUR_HOST_TRACE");
   if (host_trace)
     fprintf(stderr, "[itercur setup] %.0fus before the iteration loop (sketch %.0fus)\n",
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count(),
@@ -554,11 +554,11 @@ void run_iterative_cur(itercur_run* run) {
     // iteration-begin + gathers folded into the cluster LUPP kernels: measured slightly slower
     // than separate grid-wide gather launches inside the batch graphs (config 2: 39.4 vs
     // 38.8 ms; the strided gathers then run on the cluster's 16 SMs only), so opt-in
-    static const bool fuse_off = getenv("ITERCUR_LUPP_FUSION") == nullptr;
+    static const bool fuse_off = !env_flag("ITERCUR_LUPP_FUSION");
     auto enqueue_batch = [&]() {
       // programmatic dependent launch along the iteration's kernel chain: measured neutral to
       // slightly slower inside the batch graphs on B200 (config 2: 38.5 vs 38.3 ms), so opt-in
-      static const bool pdl = getenv("ITERCUR_PDL") != nullptr;
+      static const bool pdl = env_flag("ITERCUR_PDL");
       PdlScope pdl_scope(pdl && !evs.on);
       batch_launches = 0;
       for (int j = 0; j < kBatch; ++j) {
@@ -686,7 +686,8 @@ void run_iterative_cur(itercur_run* run) {
 
         // (4) core step: LU of D_k = S_row(I_k, 0:w); U_k^T = A(I_k,:)^T - Rt^T L(I_k,:)^T;
         //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
-        if (row_lupp_path >= 0)  // the cluster LUPP emitted the factors of D_k itself
+        static const bool force_cross_lu = env_flag("ITERCUR_FORCE_CROSS_LU");  // A/B check
+        if (row_lupp_path >= 0 || force_cross_lu)  // the cluster / panel LUPP emitted D_k's factors itself
           CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
         if (!row_fused)
           CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
@@ -1414,7 +1415,7 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
     set_lupp_force_path(0);
     // one traced launch: per-step phase cycles of CTA 0 (the cluster kernel records them only
     // in an instrumented build: ITERCUR_NVCC_EXTRA=-DITERCUR_LUPP_INSTRUMENT)
-    if (getenv("ITERCUR_LUPP_TRACE")) {
+    if (env_flag("ITERCUR_LUPP_TRACE")) {
       DevBuf<long long> tr;
       tr.alloc(static_cast<size_t>(steps) * 16);
       CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * 16, st));
@@ -1427,7 +1428,15 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
       std::vector<long long> h(static_cast<size_t>(steps) * 16);
       CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 16, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      if (used <= -100) {  // cluster v2 layout (16 slots per step)
+      if (used <= -200000) {  // panel kernel (8 slots per step)
+        for (int q = 0; q + 1 < steps; ++q) {
+          const long long* v = h.data() + q * 8;
+          fprintf(stderr,
+                  "lupp panel step %d: reduce %lld pivot-row %lld rows %lld panel-end %lld cand %lld barrier %lld "
+                  "step %lld\n",
+                  q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[4] - v[3], v[5] - v[4], v[8] - v[5], v[8] - v[0]);
+        }
+      } else if (used <= -100) {  // cluster v2 layout (16 slots per step)
         for (int q = 0; q + 1 < steps; ++q) {
           const long long* v = h.data() + q * 16;
           fprintf(stderr,

@@ -3,9 +3,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <utility>
 
 namespace itercur_b200 {
+
+// A/B and tuning switches: set, non-empty and not "0"
+inline bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] && !(e[0] == '0' && e[1] == 0);
+}
 
 constexpr uint32_t kStreamSketch = 1;      // RngStream::Sketch, proj/include/itercur/rng.hpp:13
 constexpr uint32_t kStreamSluppSketch = 2; // RngStream::SluppSketch (the s-LUPP baseline, baselines.cpp:44-46)

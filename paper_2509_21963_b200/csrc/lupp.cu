@@ -113,6 +113,7 @@ struct LuppKernelArgs {
   LuppArgs a;
   Cand* cand;           // [2][gridDim.x]
   double* norm_part;    // [gridDim.x]
+  long long* dbg;       // optional per-step clock64() trace of CTA 0 (panel kernel; benchmarking)
 };
 
 __global__ void __launch_bounds__(kLuppThreads) lupp_kernel(LuppKernelArgs ka) {
@@ -1305,7 +1306,7 @@ static cudaError_t try_lupp_cluster_v2(const LuppArgs& a, cudaStream_t st, int* 
   ka.a = a;
   ka.dbg = g_lupp_dbg;
   ka.skeleton = getenv("ITERCUR_LUPP_SKELETON") ? atoi(getenv("ITERCUR_LUPP_SKELETON")) : 0;
-  ka.serial_exchange = getenv("ITERCUR_LUPP_SERIAL") != nullptr;
+  ka.serial_exchange = env_flag("ITERCUR_LUPP_SERIAL");
   ka.rows_per_cta = pl.Rb;
   ka.smax = std::max(a.cols_max, 1);
   ka.slot = pl.slot;
@@ -1328,8 +1329,8 @@ static V2Plan plan_lupp_cluster_v2(const LuppArgs& a) {
   if (ready < 0)
     ready = (prepare_cluster_v2<512, 4>(budget) ? 1 : 0) |
             (prepare_cluster_v2<768, 2>(budget) && prepare_cluster_v2<768, 1>(budget) ? 2 : 0);
-  static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;
-  static const bool v1 = getenv("ITERCUR_LUPP_CLUSTER_V1") != nullptr;  // A/B switch
+  static const bool disabled = env_flag("ITERCUR_LUPP_NO_CLUSTER");
+  static const bool v1 = env_flag("ITERCUR_LUPP_CLUSTER_V1");  // A/B switch
   static const int force_threads = [] {
     const char* e = getenv("ITERCUR_LUPP_THREADS");
     return e ? atoi(e) : 0;
@@ -1395,7 +1396,7 @@ static cudaError_t try_lupp_cluster(const LuppArgs& a, cudaStream_t st, int* gri
     if (usable && cluster_capacity_ok(max_cl, budget) < 1) usable = false;
     cudaGetLastError();
   }
-  static const bool disabled = getenv("ITERCUR_LUPP_NO_CLUSTER") != nullptr;  // tuning switch
+  static const bool disabled = env_flag("ITERCUR_LUPP_NO_CLUSTER");  // tuning switch
   if (disabled || !usable || a.rows >= (1ll << 31) - 1) return cudaErrorNotSupported;
   // smallest cluster whose slabs fit
   for (int cl = 1; cl <= max_cl; cl *= 2) {
@@ -1427,6 +1428,237 @@ static cudaError_t try_lupp_cluster(const LuppArgs& a, cudaStream_t st, int* gri
     return cudaLaunchKernelEx(&cfg, lupp_cluster_kernel, ka);
   }
   return cudaErrorNotSupported;
+}
+
+// ---------------------------------------------------------------------------------
+// Grid-wide LUPP with panel-blocked updates, for slabs too large for shared memory (configs
+// 4/5: 100000-200000 rows). The right-looking kernel above rewrites every remaining column
+// of every row per pivot step — HBM-bound at these sizes. Here a thread keeps its rows'
+// current column and the open panel's multipliers in registers: per step it reads one column
+// and writes its multiplier; the later columns receive the panel's kPanelG rank-1 updates in
+// one pass at the panel end (each element read and written once per panel). The pivot row
+// for step s is rebuilt by every CTA from the winner's row in W (current through the last
+// panel end), its stored multipliers and the panel's previous pivot rows (same operations in
+// the same order as right-looking, so identical pivots). In-call bans live in registers;
+// the pivot rows' LU factors are emitted for the row selection (no separate factorisation).
+// ---------------------------------------------------------------------------------
+// Panel-kernel candidate exchange. Merge of one candidate into a running one with the
+// reference's rule (larger |value|, ties -> lower row index; the loser's magnitude feeds the
+// runner-up).
+__device__ __forceinline__ void wcand_merge(WCand& c, uint64_t key, int32_t idx, double second) {
+  if (key > c.key || (key == c.key && key != 0 && idx < c.idx)) {
+    c.second = fmax(second, key_mag(c.key));
+    c.key = key;
+    c.idx = idx;
+  } else {
+    c.second = fmax(c.second, key_mag(key));
+  }
+}
+// Every warp reduces all G CTA candidates (lane-strided loads, then redux.sync).
+__device__ __forceinline__ Cand panel_reduce_list(const Cand* cs, int G) {
+  WCand c{0ull, 0x7fffffff, -1.0};
+  constexpr int B = 8;  // loads of a batch issued together (one L2 round trip per batch)
+  for (int q0 = threadIdx.x & 31; q0 < G; q0 += 32 * B) {
+    Cand x[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) x[u] = q0 + 32 * u < G ? cs[q0 + 32 * u] : cand_empty();
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (x[u].idx >= 0) wcand_merge(c, mag_key(x[u].mag), static_cast<int32_t>(x[u].idx), x[u].second);
+  }
+  const WCand w = warp_argmax(c);
+  return w.key ? Cand{key_mag(w.key), w.second, static_cast<int64_t>(w.idx)} : cand_empty();
+}
+// This CTA's candidate to global: warp argmax, then thread 0 merges the warps.
+__device__ __forceinline__ void panel_publish(const Cand& local, WCand* sw, Cand* out) {
+  WCand c{0ull, 0x7fffffff, -1.0};
+  if (local.idx >= 0) wcand_merge(c, mag_key(local.mag), static_cast<int32_t>(local.idx), local.second);
+  const WCand w = warp_argmax(c);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    WCand r = sw[0];
+    for (int q = 1; q < kLuppThreads / 32; ++q)
+      if (sw[q].key) wcand_merge(r, sw[q].key, sw[q].idx, sw[q].second);
+    *out = r.key ? Cand{key_mag(r.key), r.second, static_cast<int64_t>(r.idx)} : cand_empty();
+  }
+}
+
+// PG: panel width (8; 4 for the 8-rows-per-thread variant, whose multipliers must still fit
+// in registers at 512 threads per CTA)
+template <int RMAX, int PG>
+__global__ void __launch_bounds__(kLuppThreads, 2) lupp_panel_kernel(LuppKernelArgs ka) {
+  cg::grid_group grid = cg::this_grid();
+  const LuppArgs& a = ka.a;
+  extern __shared__ double sm[];  // P [smax] + U [PG][smax] + F [PG][RMAX][threads]
+  __shared__ Cand sc[kLuppThreads / 32 + 1];
+  __shared__ double sred[kLuppThreads / 32];
+  __shared__ WCand sw[kLuppThreads / 32];
+  const int smax = a.cols_max;
+  double* P = sm;
+  double* U = sm + smax;
+  double* F = U + PG * smax;  // this thread's panel multipliers: F[(j * RMAX + k) * threads + tid]
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kLuppThreads + threadIdx.x;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * kLuppThreads;
+  const int G = gridDim.x;
+  double* W = a.W;
+  const int64_t ldw = a.ldw;
+  int steps = a.cols_max;
+  if (a.d_steps) steps = min(steps, *a.d_steps);
+  if (steps <= 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *a.d_count = 0;
+      if (a.d_width_out) *a.d_width_out = 0;
+    }
+    return;
+  }
+  double nsq;
+  if (a.d_norm_sq) {
+    nsq = *a.d_norm_sq;
+  } else {
+    double sq = 0.0;
+    for (int t = 0; t < steps; ++t)
+      for (int64_t i = gtid; i < a.rows; i += gstride) {
+        const double v = W[i + t * ldw];
+        sq = fma(v, v, sq);
+      }
+    const double b = block_sum<kLuppThreads>(sq, sred);
+    if (threadIdx.x == 0) ka.norm_part[blockIdx.x] = b;
+    grid.sync();
+    nsq = 0.0;
+    for (int q = 0; q < G; ++q) nsq += ka.norm_part[q];
+  }
+  const double abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(nsq);
+  double* lu_blk = a.lu_out ? a.lu_out + (a.d_lu_r ? *a.d_lu_r : 0) * a.lu_ld : nullptr;
+
+  // this thread's rows i = gtid + k*gstride; live bits; current column; panel multipliers
+  uint32_t live = 0;
+  double cur[RMAX], nxt[RMAX];  // nxt: W(i, s+1) through the last panel end (prefetched)
+  Cand local = cand_empty();
+#pragma unroll
+  for (int k = 0; k < RMAX; ++k) {
+    const int64_t i = gtid + k * gstride;
+    cur[k] = 0.0;
+    nxt[k] = 0.0;
+    if (i < a.rows) {
+      const uint8_t mk = a.mask[i];
+      if (!(mk == 1 || mk == a.epoch)) {
+        live |= 1u << k;
+        cur[k] = W[i];
+        if (steps > 1) nxt[k] = W[i + ldw];
+        local = cand_merge(local, Cand{fabs(cur[k]), -1.0, i});
+      }
+    }
+  }
+  Cand bc = block_reduce_cand(local, sc);
+  if (threadIdx.x == 0) ka.cand[blockIdx.x] = bc;
+  grid.sync();
+
+  int count = 0;
+  double first = 0.0;
+  long long* const dbg = (ka.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? ka.dbg : nullptr;
+  for (int s = 0; s < steps; ++s) {
+    if (dbg) dbg[s * 8 + 0] = clock64();
+    // every warp reduces the whole CTA-candidate list itself: no block barrier on this path
+    const Cand best = panel_reduce_list(ka.cand + (s & 1) * G, G);
+    if (best.idx < 0 || best.mag <= abs_floor) break;
+    if (s == 0)
+      first = best.mag;
+    else if (best.mag < a.pivot_floor * first)
+      break;
+    if (dbg) dbg[s * 8 + 1] = clock64();
+    const int jp = s % PG, s0 = s - jp;
+    // pivot row: the winner's row through the last panel end, then this panel's steps (all the
+    // loads of the winner's row — values and panel multipliers — in one round trip)
+    if (s + threadIdx.x < steps) {
+      double mult[PG - 1];
+#pragma unroll
+      for (int j = 0; j < PG - 1; ++j) mult[j] = j < jp ? W[best.idx + (s0 + j) * ldw] : 0.0;
+      for (int t = s + threadIdx.x; t < steps; t += kLuppThreads) {
+        double x = W[best.idx + t * ldw];
+#pragma unroll
+        for (int j = 0; j < PG - 1; ++j)
+          if (j < jp) x = __dsub_rn(x, __dmul_rn(mult[j], U[j * smax + t]));
+        P[t] = x;
+        U[jp * smax + t] = x;
+      }
+    }
+    __syncthreads();
+    if (dbg) dbg[s * 8 + 2] = clock64();
+    if (blockIdx.x == 0) {
+      if (threadIdx.x == 0) {
+        a.d_idx[s] = best.idx;
+        a.d_best[s] = best.mag;
+        a.d_second[s] = best.second;
+      }
+      if (lu_blk)  // LU row s of D_k: multipliers (stored in W) then U(s, s:)
+        for (int t = threadIdx.x; t < steps; t += kLuppThreads)
+          lu_blk[s + t * a.lu_ld] = t < s ? W[best.idx + t * ldw] : P[t];
+    }
+    ++count;
+    if (s + 1 >= steps) break;
+    const double pivot = P[s], y = __drcp_rn(pivot);
+    const bool p_ok = fabs(pivot) > 0x1p-968 && fabs(pivot) < 0x1p968;
+    // (the panel must close exactly every PG steps: the pivot rows are rebuilt with the
+    // open panel's terms, so a column may never receive them from a trailing update as well)
+    const bool panel_end = jp == PG - 1;
+    local = cand_empty();
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) {
+      if (!(live >> k & 1)) continue;
+      const int64_t i = gtid + k * gstride;
+      if (i == best.idx) {
+        live &= ~(1u << k);
+        continue;
+      }
+      const double f = div_by_pivot(cur[k], pivot, y, p_ok);
+      F[(jp * RMAX + k) * kLuppThreads + threadIdx.x] = f;
+      W[i + s * ldw] = f;  // column s is dead for this row: its multiplier (LU factors, pivot rows)
+      double v = nxt[k];
+      for (int j = 0; j < jp; ++j)
+        v = __dsub_rn(v, __dmul_rn(F[(j * RMAX + k) * kLuppThreads + threadIdx.x], U[j * smax + s + 1]));
+      v = __dsub_rn(v, __dmul_rn(f, U[jp * smax + s + 1]));
+      cur[k] = v;
+      if (!panel_end && s + 2 < steps) nxt[k] = W[i + (s + 2) * ldw];  // raw next column, in flight across the barrier
+      local = cand_merge(local, Cand{fabs(v), -1.0, i});
+    }
+    if (dbg) dbg[s * 8 + 3] = clock64();
+    if (panel_end) {
+      // close the panel: columns s+1.. of this thread's rows receive the panel's updates in one
+      // pass, a chunk of C columns loaded together (latency bound otherwise)
+#pragma unroll
+      for (int k = 0; k < RMAX; ++k) {
+        if (!(live >> k & 1)) continue;
+        const int64_t i = gtid + k * gstride;
+        double fr[PG];
+#pragma unroll
+        for (int j = 0; j < PG; ++j) fr[j] = F[(j * RMAX + k) * kLuppThreads + threadIdx.x];
+        W[i + (s + 1) * ldw] = cur[k];
+        constexpr int C = 8;
+        for (int t0 = s + 2; t0 < steps; t0 += C) {
+          double x[C];
+#pragma unroll
+          for (int u = 0; u < C; ++u) x[u] = t0 + u < steps ? W[i + (t0 + u) * ldw] : 0.0;
+#pragma unroll
+          for (int u = 0; u < C; ++u) {
+            const int t = min(t0 + u, steps - 1);
+#pragma unroll
+            for (int j = 0; j < PG; ++j) x[u] = __dsub_rn(x[u], __dmul_rn(fr[j], U[j * smax + t]));
+            if (t0 + u < steps) W[i + (t0 + u) * ldw] = x[u];
+          }
+          if (t0 == s + 2) nxt[k] = x[0];
+        }
+      }
+    }
+    if (dbg) dbg[s * 8 + 4] = clock64();
+    panel_publish(local, sw, ka.cand + ((s + 1) & 1) * G + blockIdx.x);
+    if (dbg) dbg[s * 8 + 5] = clock64();
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.d_count = count;
+    if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+  }
 }
 
 // Clear in-call ban marks (any value other than 1) when the epoch counter wraps.
@@ -1519,15 +1751,46 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
     cudaFuncSetAttribute(lupp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024);
     attr_set = true;
   }
-  const size_t smem = sizeof(double) * static_cast<size_t>(steps);
-  const int64_t want = std::max<int64_t>(1, ceil_div(a.rows, kLuppThreads));  // one row per thread
-  const int maxb = lupp_max_blocks(reinterpret_cast<const void*>(lupp_kernel), smem);
-  int grid = static_cast<int>(std::min<int64_t>(want, std::min(maxb, kMaxLuppGrid)));
   LuppKernelArgs ka;
   ka.a = a;
   ka.cand = cand;
   ka.norm_part = norm_part;
+  ka.dbg = g_lupp_dbg;
   void* params[] = {&ka};
+  static const bool right_looking = env_flag("ITERCUR_LUPP_RIGHT_LOOKING");  // A/B switch
+  if (!right_looking && steps <= 2048) {
+    // panel-blocked grid kernel: the fewest rows per thread whose co-resident grid covers the
+    // slab (occupancy per variant: they differ in registers)
+    struct Variant {
+      const void* fn;
+      int rmax, pg;
+    };
+    static const Variant variants[4] = {{reinterpret_cast<const void*>(lupp_panel_kernel<1, 8>), 1, 8},
+                                        {reinterpret_cast<const void*>(lupp_panel_kernel<2, 8>), 2, 8},
+                                        {reinterpret_cast<const void*>(lupp_panel_kernel<4, 8>), 4, 8},
+                                        {reinterpret_cast<const void*>(lupp_panel_kernel<8, 4>), 8, 4}};
+    static size_t pattr[4] = {0, 0, 0, 0};
+    for (int v = 0; v < 4; ++v) {
+      const size_t psmem = sizeof(double) * (static_cast<size_t>(steps) * (1 + variants[v].pg) +
+                                             static_cast<size_t>(variants[v].pg) * variants[v].rmax * kLuppThreads);
+      if (psmem > 48 * 1024 && psmem > pattr[v]) {
+        cudaError_t e = cudaFuncSetAttribute(variants[v].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(psmem));
+        if (e != cudaSuccess) return e;
+        pattr[v] = psmem;
+      }
+      const int maxb = std::min(lupp_max_blocks(variants[v].fn, psmem), kMaxLuppGrid);
+      const int64_t need = ceil_div(a.rows, static_cast<int64_t>(variants[v].rmax) * kLuppThreads);
+      if (maxb <= 0 || need > maxb) continue;
+      const int grid = static_cast<int>(std::max<int64_t>(1, need));
+      if (grid_used) *grid_used = -(200000 + grid);  // negative: emits the LU factors itself
+      return cudaLaunchCooperativeKernel(variants[v].fn, dim3(grid), dim3(kLuppThreads), params, psmem, st);
+    }
+  }
+  const size_t smem = sizeof(double) * static_cast<size_t>(steps);
+  const int64_t want = std::max<int64_t>(1, ceil_div(a.rows, kLuppThreads));  // one row per thread
+  const int maxb = lupp_max_blocks(reinterpret_cast<const void*>(lupp_kernel), smem);
+  int grid = static_cast<int>(std::min<int64_t>(want, std::min(maxb, kMaxLuppGrid)));
   if (grid_used) *grid_used = 1000000 + grid;
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lupp_kernel), dim3(grid), dim3(kLuppThreads),
                                      params, smem, st);

@@ -89,7 +89,8 @@ def test_sketch_non_tma_path_odd_lda(engine, oracle):
 
 @pytest.mark.parametrize("rows,cols,b,is_columns", [(11, 2000, 10, True), (22, 777, 20, True),
                                                     (5000, 20, 20, False), (50, 5, 5, False),
-                                                    (64, 40000, 50, True)])
+                                                    (64, 40000, 50, True), (70000, 64, 64, False),
+                                                    (64, 90000, 50, True)])
 def test_lupp_bit_exact_vs_oracle(engine, oracle, rows, cols, b, is_columns):
     """Same input bits -> the same pivot sequence and bit-identical pivot magnitudes."""
     S = _stages()
