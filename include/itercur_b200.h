@@ -17,6 +17,8 @@
  *       CurFactors.c_matrix/r_matrix/core_matrix  proj/bindings/python/module.cpp:60-68
  *   itercur_true_relative_error_device
  *       itercur::true_relative_error      proj/include/itercur/driver.hpp:85 (driver.cpp:169-190)
+ *   itercur_sketched_residual_device
+ *       make_sketch + downdate_col_residual  proj/src/sketch.cpp:10-41 (as run_threshold, bench.cpp:171-174)
  *   itercur_adjusted_threshold / itercur_gratton_tail
  *       proj/include/itercur/driver.hpp:64,68 (driver.cpp:28-46)
  *   itercur_sketch_device
@@ -48,7 +50,7 @@
 extern "C" {
 #endif
 
-#define ITERCUR_B200_ABI_VERSION 2
+#define ITERCUR_B200_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define ITERCUR_API __attribute__((visibility("default")))
@@ -153,6 +155,13 @@ ITERCUR_API int itercur_run_r_matrix(const itercur_run* run, double* out);
 ITERCUR_API int itercur_run_core_matrix(const itercur_run* run, double* out);
 /* ||A - CUR||_F / ||A||_F evaluated on the device over column panels. */
 ITERCUR_API int itercur_true_relative_error_device(const itercur_run* run, double* out);
+/* make_sketch(seed, b, A) then downdate_col_residual(estimator, factors) for the run's factors
+ * (proj/src/sketch.cpp:10-41; used by run_threshold, proj/src/bench.cpp:171-174, to score the
+ * s-LUPP baseline with the adaptive run's estimator): out = ||GA - GA(:,J) X^{-1} R||_F / ||GA||_F. */
+/* ||A||_F of a device matrix (proj/src/matrix.cpp:297-302 fro_norm), fixed-order reduction. */
+ITERCUR_API int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda, void* stream, double* out);
+ITERCUR_API int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind,
+                                                 int32_t sparse_nnz, double* out);
 ITERCUR_API void itercur_run_free(itercur_run* run);
 
 /* ---- helpers ---- */

@@ -152,6 +152,17 @@ class MatrixHandle:
         return self._tensor.detach().cpu().numpy()
 
     def fro_norm(self) -> float:
+        """||A||_F (proj/src/matrix.cpp:297-302); device handles reduce on the device."""
+        if self._tensor is not None:
+            import torch
+
+            t = self._tensor
+            out = C.c_double()
+            with torch.cuda.device(t.device):
+                stream = torch.cuda.current_stream(t.device).cuda_stream
+                _check(_lib().itercur_fro_norm_device(C.c_void_p(t.data_ptr()), self.rows, self.cols, self.lda,
+                                                      C.c_void_p(stream), C.byref(out)))
+            return out.value
         return float(np.linalg.norm(self.to_numpy()))
 
     def __repr__(self) -> str:
@@ -382,6 +393,28 @@ def true_relative_error(a, factors: CurFactors) -> float:
     return out.value
 
 
+def sketched_relative_error(a, factors: CurFactors, b: int, seed: int = 0, sketch: str = "gaussian",
+                            sparse_nnz: int = 8) -> float:
+    """make_sketch(seed, b, A) then downdate_col_residual(estimator, factors)
+    (proj/src/sketch.cpp:10-41): ||GA - GA(:,J) core R||_F / ||GA||_F for any finished run's
+    factors — how run_threshold scores the s-LUPP baseline with the adaptive run's estimator
+    (proj/src/bench.cpp:171-174). Raises ValueError for b < 1 or b > m, as make_sketch does."""
+    if factors._run is None:
+        h = _as_handle(a)
+        b = int(b)
+        if b < 1:
+            raise ValueError("block size must be at least 1")
+        if b > h.rows:
+            raise ValueError("block exceeds row count")
+        return 0.0 if h.fro_norm() == 0.0 else 1.0
+    if sketch not in _SKETCHES:
+        raise ValueError(f"unknown sketch '{sketch}'")
+    out = C.c_double()
+    _check(_lib().itercur_sketched_residual_device(factors._run.ptr, int(b), int(seed), _SKETCHES[sketch],
+                                                   int(sparse_nnz), C.byref(out)))
+    return out.value
+
+
 def adjusted_threshold(epsilon, delta, alpha, c) -> float:
     """proj/src/driver.cpp:28-39."""
     out = C.c_double()
@@ -403,5 +436,5 @@ def sketch_rows_for_block(b: int) -> int:
 
 __all__ = [
     "CurFactors", "IterationRecord", "MatrixHandle", "RunTrace", "__version__", "adjusted_threshold", "slupp_cur",
-    "gratton_tail", "iterative_cur", "sketch_rows_for_block", "true_relative_error",
+    "gratton_tail", "iterative_cur", "sketch_rows_for_block", "sketched_relative_error", "true_relative_error",
 ]

@@ -24,7 +24,8 @@ EXPORTED = [
     "itercur_run_final_rho", "itercur_run_threshold", "itercur_run_sketch_seconds", "itercur_run_total_seconds",
     "itercur_run_ga_norm", "itercur_run_note", "itercur_run_num_iterations", "itercur_run_iterations",
     "itercur_run_kernel_launches", "itercur_run_num_steps", "itercur_run_steps", "itercur_run_c_matrix", "itercur_run_r_matrix",
-    "itercur_run_core_matrix", "itercur_true_relative_error_device", "itercur_run_free",
+    "itercur_run_core_matrix", "itercur_true_relative_error_device", "itercur_sketched_residual_device", "itercur_fro_norm_device",
+    "itercur_run_free",
     "itercur_adjusted_threshold", "itercur_gratton_tail", "itercur_sketch_rows_for_block",
     "itercur_gaussian_matrix_device", "itercur_sketch_device", "itercur_select_device",
     "itercur_time_sketch_kernel", "itercur_time_lupp", "itercur_time_gemm",
@@ -94,6 +95,8 @@ def lib() -> C.CDLL:
         "itercur_run_r_matrix": (C.c_int, [runp, dp]),
         "itercur_run_core_matrix": (C.c_int, [runp, dp]),
         "itercur_true_relative_error_device": (C.c_int, [runp, dp]),
+        "itercur_fro_norm_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, dp]),
+        "itercur_sketched_residual_device": (C.c_int, [runp, C.c_int64, C.c_uint64, C.c_int32, C.c_int32, dp]),
         "itercur_run_free": (None, [runp]),
         "itercur_adjusted_threshold": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int64, dp]),
         "itercur_gratton_tail": (C.c_int, [C.c_int64, C.c_double, dp]),

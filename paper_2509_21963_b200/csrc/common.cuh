@@ -63,6 +63,20 @@ __device__ __forceinline__ double uniform_at_dev(uint64_t seed, uint32_t stream,
 // ascending with a strict '>' so ties go to the lowest index. `second` tracks the
 // runner-up magnitude for the parity checker's margin log.
 // ---------------------------------------------------------------------------------
+// a / p correctly rounded from a precomputed y = RN(1/p) (Markstein: q0 = RN(a y), r = a - q0 p
+// exactly, q = RN(q0 + r y)); outside the exponent range where the theorem holds (or for a = 0)
+// the IEEE division itself. p_ok: |p| inside [2^-968, 2^968].
+static __device__ __noinline__ double ieee_div(double a, double p) { return __ddiv_rn(a, p); }
+__device__ __forceinline__ double div_by_pivot(double a, double p, double y, bool p_ok) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = __fma_rn(-q0, p, a);
+  const double q = __fma_rn(r, y, q0);
+  const double aq = fabs(q), aa = fabs(a);
+  if (p_ok && aq > 0x1p-968 && aq < 0x1p968 && aa > 0x1p-968 && aa < 0x1p968) return q;
+  return ieee_div(a, p);
+}
+__device__ __forceinline__ bool pivot_in_range(double p) { return fabs(p) > 0x1p-968 && fabs(p) < 0x1p968; }
+
 struct Cand {
   double mag;
   double second;

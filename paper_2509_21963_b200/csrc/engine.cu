@@ -248,6 +248,8 @@ struct Workspace {
   DevBuf<uint8_t> col_mask, row_mask;
   DevBuf<char> state, lupp_scratch, qrcp_scratch;
   DevBuf<double> Wq;  // Y copy for the QRCP column selection (qrcp_pivot_cols takes W by value)
+  DevBuf<double> At;  // row-major copy of A (n x m column-major, ld ldAt) for the row gathers A(I_k, :)
+  int64_t ldAt = 0;
   DevBuf<double> scal;  // [0] asq, [1] ysq
   DevBuf<unsigned long long> nonfinite;
   char* h_state = nullptr;  // pinned mirror (thread-local cache, see pinned_state)
@@ -465,6 +467,32 @@ void run_iterative_cur(itercur_run* run) {
     grow_factors(run, first, st);
   }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+  // row-major copy of A (when it is a modest share of free HBM): the U block's base A(I_k, :)
+  // then reads |I_k| contiguous rows instead of one DRAM burst per element. Made once the run
+  // has shown it is long enough to repay the transpose (measured at config 2: ~8 us per
+  // iteration saved for a 0.5 ms transpose; at config 3, 8 iterations, it would not pay).
+  static const bool at_off = env_flag("ITERCUR_NO_ROWMAJOR_A"), at_eager = env_flag("ITERCUR_ROWMAJOR_A");
+  const int64_t at_after_iters = at_eager ? 0 : 3 * kBatch;
+  auto maybe_make_rowmajor_a = [&](int64_t iters_done) -> bool {
+    if (at_off || ws.At.p || iters_done < at_after_iters) return false;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double bytes = 8.0 * static_cast<double>(ldn) * static_cast<double>(m);
+    if (bytes > 0.3 * static_cast<double>(free_b)) return false;
+    ws.At.alloc(static_cast<size_t>(ldn) * m);
+    ws.ldAt = ldn;
+    CK(launch_transpose(A, m, n, lda, ws.At.p, ldn, st));
+    run->launches += 1;
+    return true;
+  };
+  // optional U-block trace (ITERCUR_UB_TRACE=k: phases and CTA spans at iteration k)
+  const char* ub_trace_env = getenv("ITERCUR_UB_TRACE");
+  const int64_t ub_trace_k = ub_trace_env ? atoll(ub_trace_env) : 0;
+  DevBuf<long long> ub_dbg;
+  if (ub_trace_env) {
+    ub_dbg.alloc(32 + 2 * 8192);
+    CK(cudaMemsetAsync(ub_dbg.p, 0, sizeof(long long) * (32 + 2 * 8192), st));
+  }
   // the fused U-block kernel (GEMM2 + solves + downdate) when the shape qualifies
   auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
     TsGemmParams p;
@@ -479,9 +507,15 @@ void run_iterative_cur(itercur_run* run) {
     p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
     p.bsk = 1;
     p.bsn = ldbg;
-    p.base_mode = kBaseGatherRowsT;
-    p.src = A;
-    p.lds = lda;
+    if (ws.At.p) {  // A(I_k[q], j) = At(j, I_k[q])
+      p.base_mode = kBaseGatherCols;
+      p.src = ws.At.p;
+      p.lds = ws.ldAt;
+    } else {
+      p.base_mode = kBaseGatherRowsT;
+      p.src = A;
+      p.lds = lda;
+    }
     p.idx = arr.row_idx;
     p.alpha = -1.0;
     p.out_mode = kOutNone;
@@ -496,6 +530,8 @@ void run_iterative_cur(itercur_run* run) {
     p.ldwc = ldn;
     p.wc_rows = B;
     p.norm_part = ws.part.p;
+    p.dbg = ub_dbg.p;
+    p.dbg_k = ub_trace_k;
     return p;
   };
   const bool fused_ub = !env_flag("ITERCUR_NO_FUSED_UBLOCK") && [&] {
@@ -547,6 +583,7 @@ void run_iterative_cur(itercur_run* run) {
       ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
       t_grow = us_since(tb0);
     }
+    const bool at_new = maybe_make_rowmajor_a(k_host);  // (re-capture: the U block's base changes)
     const int64_t ldbg = run->capL;
     // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
@@ -718,9 +755,15 @@ void run_iterative_cur(itercur_run* run) {
           p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
           p.bsk = 1;
           p.bsn = ldbg;
-          p.base_mode = kBaseGatherRowsT;
-          p.src = A;
-          p.lds = lda;
+          if (ws.At.p) {
+            p.base_mode = kBaseGatherCols;
+            p.src = ws.At.p;
+            p.lds = ws.ldAt;
+          } else {
+            p.base_mode = kBaseGatherRowsT;
+            p.src = A;
+            p.lds = lda;
+          }
           p.idx = arr.row_idx;
           p.alpha = -1.0;
           p.out_mode = kOutColMajor;
@@ -767,7 +810,7 @@ void run_iterative_cur(itercur_run* run) {
     };
     const auto tc0 = hclock::now();
     if (use_graph) {
-      if (!graph_exec || graph_cap != run->capL) {
+      if (!graph_exec || graph_cap != run->capL || at_new) {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         graph_exec = nullptr;
         cudaGraph_t g = nullptr;
@@ -860,6 +903,36 @@ void run_iterative_cur(itercur_run* run) {
       rec.select_rows_s = elapsed_s(evs.get(e0 + 2), evs.get(e0 + 3));
       rec.core_s = elapsed_s(evs.get(e0 + 3), evs.get(e0 + 4));
       rec.downdate_s = elapsed_s(evs.get(e0 + 4), evs.get(e0 + 5));
+    }
+  }
+  if (ub_trace_env) {
+    std::vector<long long> h(32 + 2 * 8192);
+    CK(cudaMemcpyAsync(h.data(), ub_dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "[ub trace k=%lld] CTA0 cycles: main %lld exchange %lld fills %lld fwd %lld back %lld rt %lld dmma+y %lld "
+            "norm %lld total %lld\n",
+            static_cast<long long>(ub_trace_k), h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
+            h[6] - h[5], h[7] - h[6], h[8] - h[7], h[8] - h[0]);
+    long long t0 = 0, t1 = 0, e_fin = 0;
+    int n = 0;
+    std::vector<long long> starts, ends;
+    for (int c = 0; c < 8192; ++c) {
+      const long long a = h[32 + 2 * c], b2 = h[32 + 2 * c + 1];
+      if (!a) continue;
+      starts.push_back(a);
+      ends.push_back(b2);
+      ++n;
+    }
+    if (n) {
+      t0 = *std::min_element(starts.begin(), starts.end());
+      t1 = *std::max_element(starts.begin(), starts.end());
+      e_fin = *std::max_element(ends.begin(), ends.end());
+      std::vector<long long> dur(n);
+      for (int c = 0; c < n; ++c) dur[c] = ends[c] - starts[c];
+      std::sort(dur.begin(), dur.end());
+      fprintf(stderr, "[ub trace] %d CTAs: last start +%lld ns, last end +%lld ns; CTA span ns min %lld median %lld max %lld\n",
+              n, t1 - t0, e_fin - t0, dur[0], dur[n / 2], dur[n - 1]);
     }
   }
   run->final_rho = rho;
@@ -987,6 +1060,64 @@ double true_error_impl(const itercur_run* run) {
   CK(cudaMemcpyAsync(&sq, outd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return std::sqrt(sq) / a_norm;
+}
+
+// make_sketch(seed, b, A) + downdate_col_residual(estimator, factors) (proj/src/sketch.cpp:10-41)
+// for a finished run's factors: rho = ||G A - G (C core R)|| / ||G A||. With the incremental
+// form C core R = L R~, so G C core R = (G L) R~: the sketch operator is applied to L (m x r) by
+// the same kernel, then Y^T -= R~^T (G L)^T on the engine's GEMM with ||Y||^2 fused.
+double sketched_residual_impl(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind, int32_t sparse_nnz) {
+  cudaStream_t st = run->stream;
+  const int64_t m = run->m, n = run->n;
+  if (b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
+  if (b > m) fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
+  const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
+  const int k = kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
+  double scale = 1.0;
+  if (k == kSketchSparseSign)
+    scale = 1.0 / std::sqrt(static_cast<double>(std::min<int64_t>(std::max(sparse_nnz, 1), c)));
+  DevBuf<double> S, Y, GL, wsb, scal, part, outd;
+  S.alloc(static_cast<size_t>(cp) * ldg);
+  Y.alloc(static_cast<size_t>(cp) * n);
+  scal.alloc(4);
+  CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, seed, k, sparse_nnz, st));
+  const int64_t r = run->r;
+  const int64_t wse = std::max(sketch_workspace_elems(m, n, cp), r > 0 ? sketch_workspace_elems(m, r, cp) : 0);
+  wsb.alloc(wse);
+  CK(run_sketch_apply(run->A, m, n, run->lda, S.p, ldg, cp, scale, Y.p, wsb.p, wse, SketchStats{scal.p, scal.p + 1},
+                      st, nullptr));
+  double h[2];
+  CK(cudaMemcpyAsync(h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double ga_norm = std::sqrt(h[1]);
+  if (r == 0 || ga_norm == 0.0) return ga_norm > 0.0 ? 1.0 : 0.0;  // sketch.cpp:27-30
+  GL.alloc(static_cast<size_t>(cp) * r);
+  CK(run_sketch_apply(run->L.p, m, r, run->ldL, S.p, ldg, cp, scale, GL.p, wsb.p, wse,
+                      SketchStats{scal.p + 2, scal.p + 3}, st, nullptr));
+  TsGemmParams p;
+  p.M = n;
+  p.K = r;
+  p.N = static_cast<int>(c);
+  p.A = run->Rt.p;  // R~^T (n x r), column-major with ld ldR
+  p.lda = run->ldR;
+  p.B = GL.p;       // B(q, h) = (G L)(h, q)
+  p.bsk = cp;
+  p.bsn = 1;
+  p.base_mode = kBaseInPlaceRowMajor;
+  p.C0 = Y.p;       // Y^T(j, h) = Y[h + j * cp]
+  p.ldc0 = cp;
+  p.out_mode = kOutRowMajor;
+  p.alpha = -1.0;
+  const int64_t parts = ts_gemm_grid_size(p.M, p.N);
+  part.alloc(parts);
+  outd.alloc(1);
+  p.norm_part = part.p;
+  CK(run_ts_gemm(p, st));
+  CK(launch_sum_partials(part.p, parts, outd.p, st));
+  double ysq = 0.0;
+  CK(cudaMemcpyAsync(&ysq, outd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return std::sqrt(ysq) / ga_norm;
 }
 
 void require_device() {
@@ -1139,6 +1270,24 @@ int itercur_true_relative_error_device(const itercur_run* run, double* out) {
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     *out = true_error_impl(run);
+  });
+}
+int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind,
+                                     int32_t sparse_nnz, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
+    *out = sketched_residual_impl(run, b, seed, kind, sparse_nnz);
+  });
+}
+int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda, void* stream, double* out) {
+  return guarded([&] {
+    require_device();
+    if (m < 0 || n < 0 || (m > 0 && n > 0 && lda < m)) fail(ITERCUR_E_INVALID_ARGUMENT, "fro_norm: invalid shape");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    g_alloc_stream = st;
+    *out = (m == 0 || n == 0) ? 0.0 : std::sqrt(device_sumsq(dA, m, n, lda, st));
   });
 }
 void itercur_run_free(itercur_run* run) { delete run; }

@@ -105,6 +105,19 @@ __device__ __forceinline__ void gemm_load_stage(const TsGemmParams& p, double* s
   }
 }
 
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ub_stamp(const TsGemmParams& p, int slot) {
+  if (p.dbg && blockIdx.x == 0 && blockIdx.z == 0 && threadIdx.x == 0) p.dbg[slot] = clock64();
+}
+__device__ __forceinline__ void cta_stamp(const TsGemmParams& p, int which) {
+  if (p.dbg && threadIdx.x == 0) p.dbg[32 + 2 * (blockIdx.x * gridDim.z + blockIdx.z) + which] = gtimer();
+}
+
 // Split-K cluster reduction (when gridDim.z > 1) and the fused epilogue: base + alpha * acc
 // written per out_mode, with the per-CTA sum of squares of C.
 template <int NT, int WARPS>
@@ -150,8 +163,26 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
         bv[nt][dr * 2 + dq] = (finisher && ql < nvalid && i < p.M) ? gemm_base(p, i, q0 + ql) : 0.0;
       }
   double* s_lu = gsm + NT * 4 * THREADS;  // past the split-K exchange buffer
-  double* s_yg = s_lu + W * W;
+  double* s_yg = s_lu + W * W + W;  // (W reciprocals behind the LU block)
   if constexpr (UB) {
+    if (finisher) {
+      // D_k's LU factors and Y(:,J_k)^T staged by cp.async now (the ring is drained): their
+      // latency overlaps the split-K exchange
+      __syncthreads();
+      const int64_t rr = p.ctl ? p.ctl->r : 0;
+      const double* lu = p.lu + rr * p.ldd;
+      for (int e = threadIdx.x; e < W * W; e += THREADS) {
+        const int a = e % W, b = e / W;
+        const bool in = a < nvalid && b < nvalid;
+        cp_async_8(s_lu + e, in ? lu + a + b * p.ldd : lu, in ? 8 : 0);
+      }
+      for (int e = threadIdx.x; e < NTY * 8 * W; e += THREADS) {
+        const int h = e / W, q = e % W;
+        const bool in = q < nvalid && h < p.ycp;
+        cp_async_8(s_yg + h * YP + q, in ? p.yg + h + q * p.ycp : p.yg, in ? 8 : 0);
+      }
+      cp_async_commit();
+    }
 #pragma unroll
     for (int ny = 0; ny < NTY; ++ny)
 #pragma unroll
@@ -163,6 +194,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
           yv[ny][dr * 2 + dq] = (finisher && h < p.ycp && j < p.M) ? p.y[j * p.ycp + h] : 0.0;
         }
   }
+  if constexpr (UB) ub_stamp(p, 1);
   if (splits > 1) {
     // fixed-order reduction over the cluster: rank z publishes its fragments in its own
     // shared memory, rank 0 adds ranks 1..S-1 in order (deterministic for a given S)
@@ -186,22 +218,22 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
       }
     }
     cl.sync();
-    if (blockIdx.z != 0) return;
+    if (blockIdx.z != 0) {
+      if constexpr (UB) cta_stamp(p, 1);
+      return;
+    }
   }
   if constexpr (UB) {
-    __syncthreads();  // the ring (and the split exchange buffer) is drained: reuse it
-    const int64_t rr = p.ctl ? p.ctl->r : 0;
-    const double* lu = p.lu + rr * p.ldd;
-    for (int e = threadIdx.x; e < W * W; e += THREADS) {
-      const int a = e % W, b = e / W;
-      s_lu[e] = (a < nvalid && b < nvalid) ? lu[a + b * p.ldd] : 0.0;
-    }
-    for (int e = threadIdx.x; e < NTY * 8 * W; e += THREADS) {
-      const int h = e / W, q = e % W;
-      s_yg[h * YP + q] = (q < nvalid && h < p.ycp) ? p.yg[h + q * p.ycp] : 0.0;
-    }
+    ub_stamp(p, 2);
+    cp_async_wait<0>();
     __syncthreads();
+    // reciprocals of U's diagonal, behind the LU block
+    if (threadIdx.x < W) s_lu[W * W + threadIdx.x] = threadIdx.x < nvalid ? __drcp_rn(s_lu[threadIdx.x * (W + 1)]) : 0.0;
+    __syncthreads();
+    ub_stamp(p, 3);
     ublock_epilogue<NT, WARPS>(p, acc, bv, yv, s_lu, s_yg, i0, nvalid);
+    ub_stamp(p, 8);
+    cta_stamp(p, 1);
     return;
   }
 
@@ -296,14 +328,34 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
         }
       }
   }
+  ub_stamp(p, 4);
   // back substitution with U: x[p] /= U(p, p), then x[q] -= U(q, p) x[p] for q < p
 #pragma unroll
   for (int pp = W - 1; pp >= 0; --pp) {
     if (pp >= w) continue;
     const int ntp = pp / 8, tp = (pp % 8) / 2, dqp = pp % 2;
     const double upp = s_lu[pp + pp * W];
-    const double x0 = __shfl_sync(0xffffffffu, acc[ntp][dqp], qbase | tp) / upp;
-    const double x1 = __shfl_sync(0xffffffffu, acc[ntp][2 + dqp], qbase | tp) / upp;
+    const double a0 = __shfl_sync(0xffffffffu, acc[ntp][dqp], qbase | tp);
+    const double a1 = __shfl_sync(0xffffffffu, acc[ntp][2 + dqp], qbase | tp);
+    // x = a / U(p, p) by Markstein's sequence from the precomputed reciprocal (the IEEE quotient
+    // when a, x and U(p, p) lie inside [2^-968, 2^968] or a = 0); the IEEE division for the
+    // whole warp otherwise (a warp-uniform branch keeps the chain short)
+    const double yrc = s_lu[W * W + pp];
+    double x0 = __dmul_rn(a0, yrc), x1 = __dmul_rn(a1, yrc);
+    x0 = __fma_rn(__fma_rn(-x0, upp, a0), yrc, x0);
+    x1 = __fma_rn(__fma_rn(-x1, upp, a1), yrc, x1);
+    // in range: zero, or biased exponent in [56, 1990] (inside 2^-968 .. 2^968); branch-free
+    auto out_of_range = [](double v) {
+      const unsigned hi = static_cast<unsigned>(__double_as_longlong(v) >> 32) & 0x7fffffffu;
+      const unsigned e = hi >> 20;
+      return static_cast<unsigned>((e - 56u) > (1990u - 56u)) & static_cast<unsigned>(v != 0.0);
+    };
+    const unsigned bad = out_of_range(a0) | out_of_range(a1) | out_of_range(x0) | out_of_range(x1) |
+                         static_cast<unsigned>(!pivot_in_range(upp));
+    if (__any_sync(0xffffffffu, bad)) {
+      x0 = ieee_div(a0, upp);
+      x1 = ieee_div(a1, upp);
+    }
     if (t == tp) {
       acc[ntp][dqp] = x0;
       acc[ntp][2 + dqp] = x1;
@@ -320,6 +372,7 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
         }
       }
   }
+  ub_stamp(p, 5);
   // R~ rows r .. r+w
   double* rt = p.rt + r * p.ldr;
 #pragma unroll
@@ -334,6 +387,7 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
         if (j < p.M) rt[q * p.ldr + j] = acc[nt][dr * 2 + dq];
       }
     }
+  ub_stamp(p, 6);
   // downdate MMA: D(j, h) = sum_q x_j[q] Yg(h, q)
   double yacc[NTY][4];
 #pragma unroll
@@ -365,6 +419,7 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
         if (h < p.wc_rows) p.Wc[j + h * p.ldwc] = v;
       }
     }
+  ub_stamp(p, 7);
   sq = warp_sum(sq);
   if (lane == 0) red[warp] = sq;
   __syncthreads();
@@ -492,6 +547,11 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   griddep_wait();
+  if constexpr (UB) {
+    if (p.dbg && p.ctl && p.ctl->k != p.dbg_k) p.dbg = nullptr;
+    cta_stamp(p, 0);
+    ub_stamp(p, 0);
+  }
   if (p.ctl) {
     if (p.ctl->done) return;
     const int64_t r = p.ctl->r;
@@ -636,7 +696,7 @@ static cudaError_t launch_cfg(const TsGemmParams& p, cudaStream_t st) {
 template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
 static cudaError_t launch_lean(const TsGemmParams& p, cudaStream_t st) {
   using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
-  static_assert(!UB || (NT * 4 * Cfg::THREADS + NT * 8 * NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
+  static_assert(!UB || (NT * 4 * Cfg::THREADS + NT * 8 * NT * 8 + NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
                         STAGES * Cfg::STAGE_ELEMS), "U-block epilogue buffers must fit the ring");
   static bool attr_set = false;
   if (!attr_set) {
@@ -678,7 +738,8 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
 }
 
 bool ts_gemm_ublock_supported(const TsGemmParams& p) {
-  return p.N >= 1 && p.N <= 32 && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) && p.base_mode == kBaseGatherRowsT &&
+  return p.N >= 1 && p.N <= 32 && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) &&
+         (p.base_mode == kBaseGatherRowsT || p.base_mode == kBaseGatherCols) &&
          p.norm_part && p.y && p.rt && p.lu && p.yg && p.ctl;
 }
 

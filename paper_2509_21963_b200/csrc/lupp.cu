@@ -819,17 +819,6 @@ __device__ __forceinline__ long long clock_after(unsigned long long dep) {
 
 // out-of-line IEEE division: the rare fallback stays out of the (instruction-cache
 // sensitive) step loop
-__device__ __noinline__ double ieee_div(double a, double p) { return __ddiv_rn(a, p); }
-
-__device__ __forceinline__ double div_by_pivot(double a, double p, double y, bool p_ok) {
-  const double q0 = __dmul_rn(a, y);
-  const double r = __fma_rn(-q0, p, a);
-  const double q = __fma_rn(r, y, q0);
-  const double aq = fabs(q), aa = fabs(a);
-  if (p_ok && aq > 0x1p-968 && aq < 0x1p968 && aa > 0x1p-968 && aa < 0x1p968) return q;
-  return ieee_div(a, p);
-}
-
 template <int THREADS, int RMAX>
 __global__ void __launch_bounds__(THREADS, 1) lupp_cluster_v2_kernel(LuppClusterV2Args ka) {
   // warp roles: warps 0..3 (one per scheduler sub-partition) are service warps — each reduces

@@ -62,6 +62,9 @@ inline IterArrays iter_arrays(void* base, int b) {
 
 cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int rows, double* Wc, int64_t ldwc,
                                   cudaStream_t st);
+// At(j, i) = A(i, j) (At column-major n x m, ld ldt): the engine's row-major copy of A
+cudaError_t launch_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* At, int64_t ldt,
+                             cudaStream_t st);
 // out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < min(*d_w, w_max), zero for
 // q >= w. With ctl: skipped when ctl->done, and K = ctl->r when k_from_r.
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,

@@ -110,3 +110,76 @@ def generate(cfg: int, device="cuda") -> torch.Tensor:
             at[j0:j0 + chunk] += ys[j0:j0 + chunk] @ xsig.t()
         return a
     raise ValueError(f"unknown config {cfg}")
+
+
+# ------------------------------------------------------------------ reference generator kinds
+# proj/src/testmat.cpp:19-132 (GeneratorSpec::low_rank / low_rank_pd / lehmer / exp_decay and
+# generate()), formed on the device. Entries come from the engine's normal_at on the
+# reference's stream tags; the products and the QR are input formation (not the timed path).
+def _check_dims(m, n, r=None):
+    if m < 1 or n < 1:
+        raise ValueError("generator dimensions must be positive")
+    if r is not None and (r < 1 or r > min(m, n)):
+        raise ValueError("generator rank must lie in [1, min(m, n)]")
+
+
+def _low_rank_product(m, n, r, seed, device):
+    left = stages.gaussian_matrix(m, r, seed, GEN_LEFT, device=device)
+    right = stages.gaussian_matrix(n, r, seed, GEN_RIGHT, device=device)
+    a = _colmajor_empty(m, n, device)
+    torch.matmul(right, left.t(), out=a.t())
+    return a
+
+
+def low_rank(m: int, n: int, r: int, seed: int = 0, device="cuda") -> torch.Tensor:
+    """left(m x r, GenLeft) * right(n x r, GenRight)^T (testmat.cpp:68-74, 87-90)."""
+    _check_dims(m, n, r)
+    return _low_rank_product(m, n, r, seed, device)
+
+
+def low_rank_pd(m: int, n: int, r: int, decay: float = 0.0, seed: int = 0, device="cuda") -> torch.Tensor:
+    """low_rank plus a geometric diagonal 1, d, d^2, ... (testmat.cpp:91-106); decay <= 0
+    selects d with D(last)/D(first) = 1e-12."""
+    _check_dims(m, n, r)
+    d = min(m, n)
+    ratio = float(decay)
+    if ratio <= 0.0:
+        ratio = math.pow(1e-12, 1.0 / float(d - 1)) if d > 1 else 1.0
+    if ratio >= 1.0:
+        raise ValueError("diagonal decay must lie in (0, 1)")
+    a = _low_rank_product(m, n, r, seed, device)
+    diag = np.empty(d)
+    entry = 1.0
+    for i in range(d):  # running product, as the reference accumulates it
+        diag[i] = entry
+        entry *= ratio
+    idx = torch.arange(d, device=a.device)
+    a[idx, idx] += torch.from_numpy(diag).to(a.device)
+    return a
+
+
+def lehmer(n: int, device="cuda") -> torch.Tensor:
+    """A(i, j) = (min(i, j) + 1) / (max(i, j) + 1) (testmat.cpp:107-115)."""
+    _check_dims(n, n)
+    i = torch.arange(n, dtype=torch.float64, device=device)
+    a = _colmajor_empty(n, n, device)
+    a.copy_((torch.minimum(i[:, None], i[None, :]) + 1.0) / (torch.maximum(i[:, None], i[None, :]) + 1.0))
+    return a
+
+
+def exp_decay(n: int, ratio: float = 0.5, seed: int = 0, device="cuda") -> torch.Tensor:
+    """Q1 diag(1, ratio, ratio^2, ...) Q2^T with Q1, Q2 the Householder-QR factors of n x n
+    Gaussians on GenLeft / GenRight (testmat.cpp:76-80, 116-129)."""
+    _check_dims(n, n)
+    if not (ratio > 0.0 and ratio < 1.0):
+        raise ValueError("singular-value ratio must lie in (0, 1)")
+    q1, _ = torch.linalg.qr(stages.gaussian_matrix(n, n, seed, GEN_LEFT, device=device).contiguous())
+    q2, _ = torch.linalg.qr(stages.gaussian_matrix(n, n, seed, GEN_RIGHT, device=device).contiguous())
+    sigma = np.empty(n)
+    value = 1.0
+    for i in range(n):
+        sigma[i] = value
+        value *= ratio
+    a = _colmajor_empty(n, n, device)
+    torch.matmul(q2, (q1 * torch.from_numpy(sigma).to(q1.device)).t(), out=a.t())
+    return a
