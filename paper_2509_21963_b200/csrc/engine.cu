@@ -493,6 +493,14 @@ void run_iterative_cur(itercur_run* run) {
     ub_dbg.alloc(32 + 2 * 8192);
     CK(cudaMemsetAsync(ub_dbg.p, 0, sizeof(long long) * (32 + 2 * 8192), st));
   }
+  // the same trace for the row-residual GEMM (ITERCUR_G1_TRACE=k)
+  const char* g1_trace_env = getenv("ITERCUR_G1_TRACE");
+  const int64_t g1_trace_k = g1_trace_env ? atoll(g1_trace_env) : 0;
+  DevBuf<long long> g1_dbg;
+  if (g1_trace_env) {
+    g1_dbg.alloc(32 + 2 * 8192);
+    CK(cudaMemsetAsync(g1_dbg.p, 0, sizeof(long long) * (32 + 2 * 8192), st));
+  }
   // the fused U-block kernel (GEMM2 + solves + downdate) when the shape qualifies
   auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
     TsGemmParams p;
@@ -678,6 +686,8 @@ void run_iterative_cur(itercur_run* run) {
           p.ldc0 = run->ldL;
           p.C1 = ws.Wr.p;
           p.ldc1 = ldm;
+          p.dbg = g1_dbg.p;
+          p.dbg_k = g1_trace_k;
           CK(run_ts_gemm(p, st));
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
@@ -905,36 +915,35 @@ void run_iterative_cur(itercur_run* run) {
       rec.downdate_s = elapsed_s(evs.get(e0 + 4), evs.get(e0 + 5));
     }
   }
-  if (ub_trace_env) {
+  auto print_trace = [&](const char* name, const DevBuf<long long>& buf, int64_t k) {
     std::vector<long long> h(32 + 2 * 8192);
-    CK(cudaMemcpyAsync(h.data(), ub_dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h.data(), buf.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     fprintf(stderr,
-            "[ub trace k=%lld] CTA0 cycles: main %lld exchange %lld fills %lld fwd %lld back %lld rt %lld dmma+y %lld "
-            "norm %lld total %lld\n",
-            static_cast<long long>(ub_trace_k), h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
+            "[%s trace k=%lld] CTA0 cycles: main %lld exchange %lld fills %lld fwd %lld back %lld rt %lld "
+            "dmma+y %lld norm %lld total %lld\n",
+            name, static_cast<long long>(k), h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
             h[6] - h[5], h[7] - h[6], h[8] - h[7], h[8] - h[0]);
-    long long t0 = 0, t1 = 0, e_fin = 0;
-    int n = 0;
     std::vector<long long> starts, ends;
-    for (int c = 0; c < 8192; ++c) {
-      const long long a = h[32 + 2 * c], b2 = h[32 + 2 * c + 1];
-      if (!a) continue;
-      starts.push_back(a);
-      ends.push_back(b2);
-      ++n;
-    }
+    for (int c = 0; c < 8192; ++c)
+      if (h[32 + 2 * c]) {
+        starts.push_back(h[32 + 2 * c]);
+        ends.push_back(h[32 + 2 * c + 1]);
+      }
+    const int n = static_cast<int>(starts.size());
     if (n) {
-      t0 = *std::min_element(starts.begin(), starts.end());
-      t1 = *std::max_element(starts.begin(), starts.end());
-      e_fin = *std::max_element(ends.begin(), ends.end());
+      const long long t0 = *std::min_element(starts.begin(), starts.end());
+      const long long t1 = *std::max_element(starts.begin(), starts.end());
+      const long long e_fin = *std::max_element(ends.begin(), ends.end());
       std::vector<long long> dur(n);
       for (int c = 0; c < n; ++c) dur[c] = ends[c] - starts[c];
       std::sort(dur.begin(), dur.end());
-      fprintf(stderr, "[ub trace] %d CTAs: last start +%lld ns, last end +%lld ns; CTA span ns min %lld median %lld max %lld\n",
-              n, t1 - t0, e_fin - t0, dur[0], dur[n / 2], dur[n - 1]);
+      fprintf(stderr, "[%s trace] %d CTAs: last start +%lld ns, last end +%lld ns; CTA span ns min %lld median %lld max %lld\n",
+              name, n, t1 - t0, e_fin - t0, dur[0], dur[n / 2], dur[n - 1]);
     }
-  }
+  };
+  if (ub_trace_env) print_trace("ub", ub_dbg, ub_trace_k);
+  if (g1_trace_env) print_trace("g1", g1_dbg, g1_trace_k);
   run->final_rho = rho;
   run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   if (host_trace) fprintf(stderr, "[itercur done] total %.0fus\n", run->total_s * 1e6);

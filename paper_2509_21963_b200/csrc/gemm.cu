@@ -194,7 +194,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
           yv[ny][dr * 2 + dq] = (finisher && h < p.ycp && j < p.M) ? p.y[j * p.ycp + h] : 0.0;
         }
   }
-  if constexpr (UB) ub_stamp(p, 1);
+  ub_stamp(p, 1);
   if (splits > 1) {
     // fixed-order reduction over the cluster: rank z publishes its fragments in its own
     // shared memory, rank 0 adds ranks 1..S-1 in order (deterministic for a given S)
@@ -219,7 +219,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
     }
     cl.sync();
     if (blockIdx.z != 0) {
-      if constexpr (UB) cta_stamp(p, 1);
+      cta_stamp(p, 1);
       return;
     }
   }
@@ -237,6 +237,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
     return;
   }
 
+  ub_stamp(p, 2);
   // ---------------- epilogue: physical rows (2g, 2g+1), columns (2t, 2t+1) ----------
   double sq = 0.0;
 #pragma unroll
@@ -272,6 +273,8 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
       p.norm_part[blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
   }
+  ub_stamp(p, 8);
+  cta_stamp(p, 1);
 }
 
 
@@ -547,8 +550,8 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   griddep_wait();
-  if constexpr (UB) {
-    if (p.dbg && p.ctl && p.ctl->k != p.dbg_k) p.dbg = nullptr;
+  if (p.dbg) {
+    if (p.ctl && p.ctl->k != p.dbg_k) p.dbg = nullptr;
     cta_stamp(p, 0);
     ub_stamp(p, 0);
   }
@@ -727,6 +730,8 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
     switch (lean) {
       case 1: return launch_lean<NT, 4, 16, 4>(p, st);
       case 2: return launch_lean<NT, 4, 32, 3>(p, st);
+      case 4: return launch_lean<NT, 4, 16, 3>(p, st);
+      case 5: return launch_lean<NT, 4, 32, 2>(p, st);
       default: return launch_lean<NT, 4, 32, 4>(p, st);
     }
   }
@@ -750,7 +755,11 @@ static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
   static const int forced = env_int("ITERCUR_UB_LEAN", env_int("ITERCUR_GEMM_LEAN", -1));
   static const int ub_splits = env_int("ITERCUR_UB_SPLITS", 0);
   const int lean = forced > 0 ? forced : (p.M >= 16000 ? 2 : 1);
-  g_splits_override = ub_splits;
+  // at most 2 K-splits: only the split-0 CTA runs the (serial) epilogue while its peers wait at
+  // the cluster barrier, so deeper splits cost more than they save (config 2, profile-mode
+  // phase sums: 7.64 ms at 2 splits vs 7.68 at 3 and 7.99 at 4)
+  const int64_t tiles = ceil_div(p.M, 64);
+  g_splits_override = ub_splits > 0 ? ub_splits : std::min(2, gemm_splits(tiles, p.K, lean == 2 ? 32 : 16));
   const cudaError_t e = lean == 2 ? launch_lean<NT, 4, 32, 3, true>(p, st) : launch_lean<NT, 4, 16, 4, true>(p, st);
   g_splits_override = 0;
   return e;
