@@ -243,6 +243,53 @@ double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cud
   return h;
 }
 
+// ---- the sketch apply (make_sketch, sketch.cpp:10-24), shared by the run and the stage entries.
+// The sparse-sign operator can also be applied as a sparse operator (8 adds per element of A,
+// sketch.cu sparse_sketch_kernel; bitwise equal to the oracle's sparse loop). Measured on B200
+// it is slower than the DMMA contraction over the materialised +-1 operator at every shape
+// tried (40000 x 20000, c = 55: 3.9 ms vs 2.7 ms; its list walk is bound by the shared-memory
+// read of every (row, target) pair and a serial add chain per sketch row), so it is opt-in:
+// ITERCUR_SPARSE_SKETCH=1.
+constexpr int64_t kSparseSketchMinCp = 1 << 30;
+struct SketchBuffers {
+  DevBuf<double> S, ws;
+};
+static bool sparse_sketch_path(int kind, int64_t c, int64_t cp, int zeta_eff) {
+  if (kind != kSketchSparseSign || !sparse_sketch_supported(c, zeta_eff)) return false;
+  const char* e = getenv("ITERCUR_SPARSE_SKETCH");
+  if (e && e[0]) return e[0] != '0';
+  return cp >= kSparseSketchMinCp;
+}
+static int zeta_effective(int kind, int sparse_nnz, int64_t c) {
+  return kind == kSketchSparseSign ? static_cast<int>(std::min<int64_t>(std::max(sparse_nnz, 1), c)) : 0;
+}
+// Y (cp x n, ld cp) = scale * S * A, ||A||^2 -> stats.d_asq, ||Y||^2 -> stats.d_ysq. Returns the
+// number of kernel launches.
+static int apply_sketch(const double* A, int64_t m, int64_t n, int64_t lda, int kind, int sparse_nnz, uint64_t seed,
+                        uint32_t stream_tag, int64_t c, int64_t cp, double* Y, const SketchStats& stats,
+                        SketchBuffers& buf, cudaStream_t st, SketchLaunchInfo* info = nullptr,
+                        bool operator_ready = false) {
+  const int ze = zeta_effective(kind, sparse_nnz, c);
+  const double scale = kind == kSketchSparseSign ? 1.0 / std::sqrt(static_cast<double>(ze)) : 1.0;
+  if (sparse_sketch_path(kind, c, cp, ze)) {
+    const int64_t wse = sparse_sketch_workspace_elems(m, n, cp, ze);
+    if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
+    CK(run_sketch_apply_sparse(A, m, n, lda, seed, c, cp, ze, scale, Y, buf.ws.p, wse, stats, st, info));
+    return 4;
+  }
+  const int64_t ldg = round_up(m, 32);
+  int launches = 0;
+  if (!operator_ready) {
+    buf.S.alloc(static_cast<size_t>(cp) * ldg);
+    CK(launch_gen_sketch_operator(buf.S.p, cp, ldg, c, m, seed, kind, sparse_nnz, st, stream_tag));
+    launches += 1;
+  }
+  const int64_t wse = sketch_workspace_elems(m, n, cp);
+  if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
+  CK(run_sketch_apply(A, m, n, lda, buf.S.p, ldg, cp, scale, Y, buf.ws.p, wse, stats, st, info));
+  return launches + 4;
+}
+
 struct Workspace {
   DevBuf<double> Y, Wc, Wr, Bg, Ut, Yg, lu, part, sk_ws, S;
   DevBuf<uint8_t> col_mask, row_mask;
@@ -351,24 +398,12 @@ void run_iterative_cur(itercur_run* run) {
   cudaEvent_t e_sk0 = evs.get(0), e_sk1 = evs.get(1);
   CK(cudaEventRecord(e_sk0, st));
   {
-    const int64_t ldg = round_up(m, 32);
-    ws.S.alloc(static_cast<size_t>(cp) * ldg);
-    CK(launch_gen_sketch_operator(ws.S.p, cp, ldg, c, m, cfg.seed, cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN
-                                                                       ? kSketchSparseSign
-                                                                       : kSketchGaussian,
-                                  cfg.sparse_nnz, st,
-                                  cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch));
-    run->launches += 1;
-    const int64_t wse = sketch_workspace_elems(m, n, cp);
-    ws.sk_ws.alloc(wse);
-    double scale = 1.0;
-    if (cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN) {
-      const int ze = static_cast<int>(std::min<int64_t>(std::max(cfg.sparse_nnz, 1), c));
-      scale = 1.0 / std::sqrt(static_cast<double>(ze));
-    }
+    const int kind = cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
+    SketchBuffers sb;
     SketchStats stats{ws.scal.p + 0, ws.scal.p + 1};
-    CK(run_sketch_apply(A, m, n, lda, ws.S.p, ldg, cp, scale, ws.Y.p, ws.sk_ws.p, wse, stats, st, nullptr));
-    run->launches += 4;
+    run->launches += apply_sketch(A, m, n, lda, kind, cfg.sparse_nnz, cfg.seed,
+                                  cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch, c,
+                                  cp, ws.Y.p, stats, sb, st);
   }
   CK(cudaEventRecord(e_sk1, st));
   double hs[2] = {0, 0};
@@ -1080,29 +1115,24 @@ double sketched_residual_impl(const itercur_run* run, int64_t b, uint64_t seed, 
   const int64_t m = run->m, n = run->n;
   if (b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
   if (b > m) fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
-  const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
+  const int64_t c = sketch_rows(b), cp = round_up(c, 8);
   const int k = kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
-  double scale = 1.0;
-  if (k == kSketchSparseSign)
-    scale = 1.0 / std::sqrt(static_cast<double>(std::min<int64_t>(std::max(sparse_nnz, 1), c)));
-  DevBuf<double> S, Y, GL, wsb, scal, part, outd;
-  S.alloc(static_cast<size_t>(cp) * ldg);
+  DevBuf<double> Y, GL, scal, part, outd;
+  SketchBuffers sb;
   Y.alloc(static_cast<size_t>(cp) * n);
   scal.alloc(4);
-  CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, seed, k, sparse_nnz, st));
   const int64_t r = run->r;
-  const int64_t wse = std::max(sketch_workspace_elems(m, n, cp), r > 0 ? sketch_workspace_elems(m, r, cp) : 0);
-  wsb.alloc(wse);
-  CK(run_sketch_apply(run->A, m, n, run->lda, S.p, ldg, cp, scale, Y.p, wsb.p, wse, SketchStats{scal.p, scal.p + 1},
-                      st, nullptr));
+  apply_sketch(run->A, m, n, run->lda, k, sparse_nnz, seed, kStreamSketch, c, cp, Y.p, SketchStats{scal.p, scal.p + 1},
+               sb, st);
   double h[2];
   CK(cudaMemcpyAsync(h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double ga_norm = std::sqrt(h[1]);
   if (r == 0 || ga_norm == 0.0) return ga_norm > 0.0 ? 1.0 : 0.0;  // sketch.cpp:27-30
   GL.alloc(static_cast<size_t>(cp) * r);
-  CK(run_sketch_apply(run->L.p, m, r, run->ldL, S.p, ldg, cp, scale, GL.p, wsb.p, wse,
-                      SketchStats{scal.p + 2, scal.p + 3}, st, nullptr));
+  // the same operator on L (the dense operator, if any, is reused)
+  apply_sketch(run->L.p, m, r, run->ldL, k, sparse_nnz, seed, kStreamSketch, c, cp, GL.p,
+               SketchStats{scal.p + 2, scal.p + 3}, sb, st, nullptr, sb.S.p != nullptr);
   TsGemmParams p;
   p.M = n;
   p.K = r;
@@ -1329,20 +1359,14 @@ int itercur_sketch_device(const double* dA, int64_t m, int64_t n, int64_t lda, i
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     configure_mempool_once();
     g_alloc_stream = st;
-    const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
-    DevBuf<double> S, Yp, wsb, scal;
-    S.alloc(static_cast<size_t>(cp) * ldg);
+    const int64_t c = sketch_rows(b), cp = round_up(c, 8);
+    DevBuf<double> Yp, scal;
+    SketchBuffers sb;
     Yp.alloc(static_cast<size_t>(cp) * n);
-    const int64_t wse = sketch_workspace_elems(m, n, cp);
-    wsb.alloc(wse);
     scal.alloc(2);
     const int k = kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
-    CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, seed, k, sparse_nnz, st));
-    double scale = 1.0;
-    if (k == kSketchSparseSign)
-      scale = 1.0 / std::sqrt(static_cast<double>(std::min<int64_t>(std::max(sparse_nnz, 1), c)));
     SketchStats stats{scal.p, scal.p + 1};
-    CK(run_sketch_apply(dA, m, n, lda, S.p, ldg, cp, scale, Yp.p, wsb.p, wse, stats, st, nullptr));
+    apply_sketch(dA, m, n, lda, k, sparse_nnz, seed, kStreamSketch, c, cp, Yp.p, stats, sb, st);
     // compact to ld = c
     CK(cudaMemcpy2DAsync(dY, sizeof(double) * c, Yp.p, sizeof(double) * cp, sizeof(double) * c, n,
                          cudaMemcpyDeviceToDevice, st));
@@ -1492,21 +1516,33 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     configure_mempool_once();
     g_alloc_stream = st;
     const int64_t c = sketch_rows(b), cp = round_up(c, 8), ldg = round_up(m, 32);
-    DevBuf<double> S, Y, wsb;
-    S.alloc(static_cast<size_t>(cp) * ldg);
+    const int k = kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
+    DevBuf<double> S, Y, wsb, scal;
     Y.alloc(static_cast<size_t>(cp) * n);
-    const int64_t wse = sketch_workspace_elems(m, n, cp);
-    wsb.alloc(wse);
-    CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, 0, kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign
-                                                                                          : kSketchGaussian,
-                                  8, st));
+    scal.alloc(2);
     SketchLaunchInfo info;
-    CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, wse, st, &info));  // warm-up
+    const bool sparse = sparse_sketch_path(k, c, cp, zeta_effective(k, 8, c));
+    SketchBuffers sb;
+    if (!sparse) {
+      S.alloc(static_cast<size_t>(cp) * ldg);
+      const int64_t wse = sketch_workspace_elems(m, n, cp);
+      wsb.alloc(wse);
+      CK(launch_gen_sketch_operator(S.p, cp, ldg, c, m, 0, k, 8, st));
+    }
+    // the sparse path is timed whole (operator lists + apply + norm reductions); the dense
+    // path times its DMMA kernel alone
+    auto once = [&]() {
+      if (sparse)
+        apply_sketch(dA, m, n, lda, k, 8, 0, kStreamSketch, c, cp, Y.p, SketchStats{scal.p, scal.p + 1}, sb, st, &info);
+      else
+        CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, static_cast<int64_t>(wsb.count), st, &info));
+    };
+    once();  // warm-up
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, st));
-    for (int q = 0; q < reps; ++q) CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, wse, st, &info));
+    for (int q = 0; q < reps; ++q) once();
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
     float ms = 0.f;

@@ -89,6 +89,13 @@ cudaError_t run_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
                              int64_t c_pad, double scale, double* Y, double* workspace, int64_t workspace_elems,
                              const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info);
 int64_t sketch_workspace_elems(int64_t m, int64_t n, int64_t c_pad);
+// Sparse-sign sketch as a sparse operator (no dense Omega): Y (c_pad x n, ld c_pad) =
+// scale * Omega * A generated from (seed, c, zeta) on the fly, ||A||^2 and ||Y||^2 as above.
+bool sparse_sketch_supported(int64_t c, int zeta);
+int64_t sparse_sketch_workspace_elems(int64_t m, int64_t n, int64_t c_pad, int zeta);
+cudaError_t run_sketch_apply_sparse(const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed, int64_t c,
+                                    int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
+                                    const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info);
 // Stand-alone timing hook: the DMMA kernel only (for roofline measurement).
 cudaError_t run_sketch_dmma_only(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
                                  int64_t c_pad, double* Y, double* workspace, int64_t workspace_elems, cudaStream_t st,

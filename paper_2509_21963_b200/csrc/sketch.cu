@@ -461,4 +461,242 @@ cudaError_t run_sketch_dmma_only(const double* A, int64_t m, int64_t n, int64_t 
   return launch_dmma(p, A, m, n, lda, S, ldg, c_pad, out, n * c_pad, ws + part_elems, st);
 }
 
+
+// ------------------------------------------------------------------ sparse-sign sketch
+// Y = Omega * A with Omega's zeta nonzeros (+-1) per column applied as a
+// sparse operator: 8 adds per element of A instead of 2 * c_pad DMMA flops. A is streamed
+// once in 256-row x 32-column tiles (coalesced 8-byte loads, register-prefetched one tile
+// ahead, staged in shared memory with an odd pitch); the operator is kept transposed per
+// 256-row tile: for each sketch row h, the tile rows it touches in ascending order with
+// their signs (16-bit entries). Warp q owns sketch rows h = q, q + 16, ..; lane j owns
+// column j of the tile, so every list entry is one broadcast 16-bit load plus one
+// conflict-free 256-byte row read per warp. Each Y(h, j) is a running sum over ascending
+// rows i from 0 with the sign applied as add / subtract, then scaled once: the same
+// operations in the same order as the oracle's sparse loop (bitwise-identical Y).
+constexpr int kSpTI = 256;   // rows per tile
+constexpr int kSpTJ = 32;    // columns per CTA
+constexpr int kSpThreads = 512;
+constexpr int kSpMaxC = 128;  // sketch rows supported (8 accumulators per lane)
+// per-tile list capacity: zeta entries per row plus up to 3 padding entries per sketch row
+__host__ __device__ constexpr int sp_list_cap(int zeta, int c_pad) { return zeta * kSpTI + 4 * c_pad; }
+
+constexpr int kSpTJP = kSpTJ + 1;  // odd tile pitch: a lane-per-row store hits distinct bank pairs
+// lists of tile t: entries[t * zeta * 256 + off[t * (c_pad + 1) + h] ...]; an entry is the row's
+// byte offset in the tile (row * kSpTJP * 8) with the sign in bit 31 (xor into the value's sign)
+__global__ void __launch_bounds__(kSpTI) sparse_lists_kernel(uint64_t seed, int64_t m, int c, int c_pad, int zeta,
+                                                             uint32_t* __restrict__ entries, int* __restrict__ offs) {
+  __shared__ int cnt[kSpTI / 32][kSpMaxC];
+  __shared__ int base[kSpTI / 32][kSpMaxC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kSpTI + threadIdx.x;
+  int32_t rows[16];
+  int8_t signs[16];
+  uint32_t hit[kSpMaxC / 32] = {0, 0, 0, 0}, neg[kSpMaxC / 32] = {0, 0, 0, 0};
+  if (i < m) {
+    sparse_sign_slots(seed, i, c, zeta, rows, signs);
+    for (int t = 0; t < zeta; ++t) {
+      hit[rows[t] >> 5] |= 1u << (rows[t] & 31);
+      if (signs[t] < 0) neg[rows[t] >> 5] |= 1u << (rows[t] & 31);
+    }
+  }
+  for (int h = 0; h < c; ++h) {
+    const unsigned bal = __ballot_sync(0xffffffffu, hit[h >> 5] >> (h & 31) & 1u);
+    if (lane == 0) cnt[warp][h] = __popc(bal);
+  }
+  __syncthreads();
+  __shared__ int pad_from[kSpMaxC], pad_to[kSpMaxC];
+  if (threadIdx.x == 0) {
+    int run = 0;
+    int* o = offs + static_cast<int64_t>(blockIdx.x) * (c_pad + 1);
+    for (int h = 0; h < c_pad; ++h) {
+      o[h] = run;
+      for (int w = 0; w < kSpTI / 32; ++w) {
+        base[w][h] = run;
+        run += h < c ? cnt[w][h] : 0;
+      }
+      pad_from[h] = run;
+      run = (run + 3) & ~3;  // every list a multiple of 4 entries
+      pad_to[h] = run;
+    }
+    o[c_pad] = run;
+  }
+  __syncthreads();
+  uint32_t* e = entries + static_cast<int64_t>(blockIdx.x) * sp_list_cap(zeta, c_pad);
+  for (int h = threadIdx.x; h < c_pad; h += kSpTI)
+    for (int q = pad_from[h]; q < pad_to[h]; ++q) e[q] = static_cast<uint32_t>(kSpTI * kSpTJP * 8);  // zero row
+  for (int h = 0; h < c; ++h) {
+    const bool mine = hit[h >> 5] >> (h & 31) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+    if (mine) {
+      const int pos = base[warp][h] + __popc(bal & ((1u << lane) - 1u));
+      e[pos] = static_cast<uint32_t>(threadIdx.x * kSpTJP * 8) | ((neg[h >> 5] >> (h & 31) & 1u) << 31);
+    }
+  }
+}
+
+template <int NH>  // accumulators per lane: sketch rows q, q + 16, .. (NH * 16 >= c_pad)
+__global__ void __launch_bounds__(kSpThreads, 1)
+    sparse_sketch_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                         const uint32_t* __restrict__ entries, const int* __restrict__ offs, int c, int c_pad,
+                         int zeta, double scale, double* __restrict__ Y, double* __restrict__ asq_part,
+                         double* __restrict__ ysq_part, int mode) {
+  constexpr int TJP = kSpTJP;
+  extern __shared__ __align__(16) double sps[];
+  double* tile = sps;                                                    // [kSpTI + 1][TJP], last row 0
+  uint32_t* lst = reinterpret_cast<uint32_t*>(tile + (kSpTI + 1) * TJP + 1);  // [list cap], 16-byte aligned
+  int* off = reinterpret_cast<int*>(lst + sp_list_cap(16, kSpMaxC));     // [c_pad + 1]
+  __shared__ double red[kSpThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kSpTJ;
+  const int ntiles = static_cast<int>((m + kSpTI - 1) / kSpTI);
+  // loader: warp w reads columns w and w + 16, lane l rows l + 32u of the tile
+  const int64_t jl0 = j0 + warp, jl1 = j0 + warp + 16;
+  const bool c0ok = jl0 < n, c1ok = jl1 < n;
+  const double* a0 = A + (c0ok ? jl0 : 0) * lda;
+  const double* a1 = A + (c1ok ? jl1 : 0) * lda;
+  double pre[16];
+  constexpr int kLpre = (sp_list_cap(16, kSpMaxC) / 4 + kSpThreads - 1) / kSpThreads;
+  uint4 lpre[kLpre];  // this tile's operator lists
+  int opre = 0;       // and one list offset
+  const int nent4 = sp_list_cap(zeta, c_pad) / 4;
+  if (threadIdx.x < TJP) tile[kSpTI * TJP + threadIdx.x] = 0.0;  // the zero row (padding entries)
+  double asq = 0.0;
+  auto fetch = [&](int t) {
+    const int64_t i0 = static_cast<int64_t>(t) * kSpTI;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + lane + 32 * u;
+      pre[u] = (c0ok && i < m) ? __ldcs(a0 + i) : 0.0;
+      pre[8 + u] = (c1ok && i < m) ? __ldcs(a1 + i) : 0.0;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(entries) + static_cast<int64_t>(t) * nent4;
+#pragma unroll
+    for (int k = 0; k < kLpre; ++k) {
+      const int q = threadIdx.x + k * kSpThreads;
+      lpre[k] = q < nent4 ? src[q] : make_uint4(0, 0, 0, 0);
+    }
+    opre = threadIdx.x <= c_pad ? offs[static_cast<int64_t>(t) * (c_pad + 1) + threadIdx.x] : 0;
+  };
+  double acc[NH];
+#pragma unroll
+  for (int q = 0; q < NH; ++q) acc[q] = 0.0;
+  fetch(0);
+  for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      tile[(lane + 32 * u) * TJP + warp] = pre[u];
+      tile[(lane + 32 * u) * TJP + warp + 16] = pre[8 + u];
+      asq = fma(pre[u], pre[u], asq);
+      asq = fma(pre[8 + u], pre[8 + u], asq);
+    }
+#pragma unroll
+    for (int k = 0; k < kLpre; ++k) {
+      const int q = threadIdx.x + k * kSpThreads;
+      if (q < nent4) reinterpret_cast<uint4*>(lst)[q] = lpre[k];
+    }
+    if (threadIdx.x <= c_pad) off[threadIdx.x] = opre;
+    __syncthreads();
+    if (t + 1 < ntiles && !(mode & 2)) fetch(t + 1);  // next tile in flight during the list walk
+    const uint32_t col = smem_u32(tile) + lane * 8;
+    auto add_entry = [&](double v, uint32_t u) {
+      // v + (x with its sign flipped when u's bit 31 is set) == v -/+ x exactly
+      double x;
+      asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(col + (u & 0x7fffffffu)));  // (not volatile: the 4 loads batch)
+      const int hi = __double2hiint(x) ^ static_cast<int>(u & 0x80000000u);
+      return __dadd_rn(v, __hiloint2double(hi, __double2loint(x)));
+    };
+    // Every list is padded to a multiple of 4 entries that read the tile's zero row (adding
+    // +0.0 leaves a running sum that started at +0.0 unchanged, so Y stays bitwise the oracle's),
+    // so 4 entries arrive per broadcast 16-byte load: one shared-memory wavefront per 4.
+#pragma unroll
+    for (int q = 0; q < NH; ++q) {
+      const int h = warp + 16 * q;
+      if (h >= c || (mode & 1)) continue;
+      const int e0 = off[h], e1 = off[h + 1];
+      double v = acc[q];
+      for (int e = e0; e < e1; e += 8) {
+        const uint4 ua = *reinterpret_cast<const uint4*>(lst + e);
+        const uint4 ub = e + 4 < e1 ? *reinterpret_cast<const uint4*>(lst + e + 4) : make_uint4(0, 0, 0, 0);
+        v = add_entry(v, ua.x);
+        v = add_entry(v, ua.y);
+        v = add_entry(v, ua.z);
+        v = add_entry(v, ua.w);
+        if (e + 4 < e1) {
+          v = add_entry(v, ub.x);
+          v = add_entry(v, ub.y);
+          v = add_entry(v, ub.z);
+          v = add_entry(v, ub.w);
+        }
+      }
+      acc[q] = v;
+    }
+    __syncthreads();
+  }
+  double ysq = 0.0;
+  const int64_t j = j0 + lane;
+#pragma unroll
+  for (int q = 0; q < NH; ++q) {
+    const int h = warp + 16 * q;
+    if (h < c_pad && j < n) {
+      const double v = h < c ? acc[q] * scale : 0.0;
+      Y[h + j * c_pad] = v;
+      ysq = fma(v, v, ysq);
+    }
+  }
+  const double bs = block_sum<kSpThreads>(asq, red);
+  if (threadIdx.x == 0) asq_part[blockIdx.x] = bs;
+  __syncthreads();
+  const double by = block_sum<kSpThreads>(ysq, red);
+  if (threadIdx.x == 0) ysq_part[blockIdx.x] = by;
+}
+
+int64_t sparse_sketch_workspace_elems(int64_t m, int64_t n, int64_t c_pad, int zeta) {
+  const int64_t tiles = ceil_div(m, kSpTI);
+  const int64_t ent_bytes = tiles * sp_list_cap(zeta, static_cast<int>(c_pad)) * 4, off_bytes = tiles * (c_pad + 1) * 4;
+  return ceil_div(ent_bytes + off_bytes, 8) + 2 * ceil_div(n, kSpTJ) + 16;
+}
+
+bool sparse_sketch_supported(int64_t c, int zeta) { return c >= 1 && c <= kSpMaxC && zeta >= 1 && zeta <= 16; }
+
+cudaError_t run_sketch_apply_sparse(const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed, int64_t c,
+                                    int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
+                                    const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info) {
+  if (!sparse_sketch_supported(c, zeta) || c_pad > kSpMaxC) return cudaErrorInvalidValue;
+  if (sparse_sketch_workspace_elems(m, n, c_pad, zeta) > ws_elems) return cudaErrorInvalidValue;
+  const int64_t tiles = ceil_div(m, kSpTI), ctas = ceil_div(n, kSpTJ);
+  uint32_t* entries = reinterpret_cast<uint32_t*>(ws);
+  const int64_t cap = sp_list_cap(zeta, static_cast<int>(c_pad));
+  int* offs = reinterpret_cast<int*>(entries + tiles * cap);
+  double* asq_part = ws + ceil_div(tiles * cap * 4 + tiles * (c_pad + 1) * 4, 8);
+  double* ysq_part = asq_part + ctas;
+  sparse_lists_kernel<<<static_cast<unsigned>(tiles), kSpTI, 0, st>>>(seed, m, static_cast<int>(c),
+                                                                     static_cast<int>(c_pad), zeta, entries, offs);
+  const size_t smem = sizeof(double) * ((kSpTI + 1) * kSpTJP + 1) + 4 * sp_list_cap(16, kSpMaxC) + 4 * (kSpMaxC + 1);
+  auto launch = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    static const int mode = getenv("ITERCUR_SPARSE_MODE") ? atoi(getenv("ITERCUR_SPARSE_MODE")) : 0;  // ablation
+    kern<<<static_cast<unsigned>(ctas), kSpThreads, smem, st>>>(A, m, n, lda, entries, offs, static_cast<int>(c),
+                                                                static_cast<int>(c_pad), zeta, scale, Y, asq_part,
+                                                                ysq_part, mode);
+    return cudaGetLastError();
+  };
+  cudaError_t e;
+  if (c_pad <= 16) e = launch(sparse_sketch_kernel<1>);
+  else if (c_pad <= 32) e = launch(sparse_sketch_kernel<2>);
+  else if (c_pad <= 64) e = launch(sparse_sketch_kernel<4>);
+  else e = launch(sparse_sketch_kernel<8>);
+  if (e != cudaSuccess) return e;
+  reduce_partials_kernel<<<1, 256, 0, st>>>(ysq_part, static_cast<int>(ctas), stats.d_ysq);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(asq_part, static_cast<int>(ctas), stats.d_asq);
+  if (info) {
+    info->splits = 1;
+    info->ctas = static_cast<int>(ctas);
+    info->nt = 0;
+    info->tma = false;
+    info->dominant_launches = 1;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace itercur_b200

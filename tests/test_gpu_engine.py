@@ -22,8 +22,8 @@ def low_rank_plus_noise(oracle, m, n, r, rel_noise, seed):
     return a + (rel_noise * np.linalg.norm(a) / np.linalg.norm(noise)) * noise
 
 
-@pytest.mark.parametrize("case", ["expdecay600", "lowrank_noise", "rbf1500", "sparse_sign", "odd_shape", "b64",
-                                  "b1"])
+@pytest.mark.parametrize("case", ["expdecay600", "lowrank_noise", "rbf1500", "sparse_sign", "sparse_sign_b40",
+                                  "odd_shape", "b64", "b1"])
 def test_engine_matches_oracle(engine, oracle, case):
     rng = np.random.default_rng(11)
     kw = dict(epsilon=1e-6, b=10, seed=0)
@@ -42,6 +42,12 @@ def test_engine_matches_oracle(engine, oracle, case):
         v, _ = np.linalg.qr(rng.standard_normal((400, 400)))
         a = (u * (np.arange(1, 401) ** -2.0)) @ v.T
         kw.update(epsilon=1e-4, b=20, seed=2, sketch="sparse_sign")
+    elif case == "sparse_sign_b40":  # c_pad = 48, through the opt-in sparse-operator sketch kernel
+        import os
+
+        os.environ["ITERCUR_SPARSE_SKETCH"] = "1"
+        a = low_rank_plus_noise(oracle, 900, 700, 120, 1e-9, 13)
+        kw.update(epsilon=1e-7, b=40, seed=5, sketch="sparse_sign")
     elif case == "b64":  # wide blocks: block-level LU and 64-wide solves (configs 4/5 use b = 50 / 64)
         a = low_rank_plus_noise(oracle, 700, 520, 150, 1e-10, 21)
         kw.update(epsilon=1e-8, b=64, seed=6)
@@ -51,7 +57,12 @@ def test_engine_matches_oracle(engine, oracle, case):
     else:
         a = low_rank_plus_noise(oracle, 333, 217, 25, 1e-11, 9)
         kw.update(epsilon=1e-9, b=7, seed=4)
-    f, t = engine.iterative_cur(a, **kw)
+    try:
+        f, t = engine.iterative_cur(a, **kw)
+    finally:
+        import os
+
+        os.environ.pop("ITERCUR_SPARSE_SKETCH", None)
     o = oracle.iterative_cur(a, **kw)
     v = compare_runs(o, f, t)
     assert v["status_equal"], (o.status, t.status)

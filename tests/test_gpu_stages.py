@@ -71,6 +71,31 @@ def test_sketch_matches_oracle(engine, oracle, m, n, b, kind):
     assert abs(ga - ga_or) <= 1e-12 * ga_or and abs(an - an_or) <= 1e-12 * an_or
 
 
+@pytest.mark.parametrize("m,n,b", [(513, 300, 40), (800, 901, 50), (1000, 64, 100), (257, 33, 1), (700, 1000, 20),
+                                   (300, 1, 30), (4099, 257, 58), (600, 70, 16)])
+def test_sparse_sign_operator_path_bit_exact(engine, oracle, monkeypatch, m, n, b):
+    """The sparse-operator kernel sums each Y(h, j) over ascending rows with the sign as
+    add/subtract and scales once — the oracle's loop — so Y is bitwise equal (not just close)."""
+    monkeypatch.setenv("ITERCUR_SPARSE_SKETCH", "1")  # opt-in path
+    S = _stages()
+    a = oracle.random_gaussian(m, n, 99 + m)
+    y, ga, an = S.sketch(S.colmajor(a), b, 7, kind="sparse_sign")
+    y_or, ga_or, an_or = oracle.sketch(a, b, 7, kind="sparse_sign")
+    assert np.array_equal(y.cpu().numpy(), y_or)
+    assert abs(ga - ga_or) <= 1e-13 * ga_or and abs(an - an_or) <= 1e-13 * an_or
+
+
+def test_sparse_sign_dense_and_sparse_paths_agree(engine, oracle, monkeypatch):
+    S = _stages()
+    a = S.colmajor(oracle.random_gaussian(600, 500, 5))
+    monkeypatch.setenv("ITERCUR_SPARSE_SKETCH", "0")
+    y_dense, _, _ = S.sketch(a, 40, 2, kind="sparse_sign")
+    monkeypatch.setenv("ITERCUR_SPARSE_SKETCH", "1")
+    y_sparse, _, _ = S.sketch(a, 40, 2, kind="sparse_sign")
+    d, sp = y_dense.cpu().numpy(), y_sparse.cpu().numpy()
+    assert np.linalg.norm(d - sp) <= 1e-13 * np.linalg.norm(sp)
+
+
 def test_sketch_non_tma_path_odd_lda(engine, oracle):
     """lda odd -> the A tile cannot be described to TMA; the generic staging path runs."""
     import torch
