@@ -91,7 +91,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kernel_substr, profile="profiles/ncu_full_r01_cfg2.txt"):
+def ncu_traffic(kernel_substr, profile="profiles/ncu_full_r01_cfg2_v4.txt"):
     """DRAM bytes (read + write) per launch of a kernel from the committed `ncu --set full`
     summary (tools/summarize_ncu.py), or None when no capture is on file."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), profile)
@@ -394,7 +394,7 @@ def main():
         roof = {"bound": "hbm", "achieved": bytes_alg / t_k / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": hbm_src}
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": ncu_traffic("sketch_dmma_kernel"),
-                 "traffic_source": "profiles/ncu_full_r01_cfg2.txt (dram__bytes_read + dram__bytes_write, one launch)",
+                 "traffic_source": "profiles/ncu_full_r01_cfg2_v4.txt (dram__bytes_read + dram__bytes_write, one launch)",
                  "kernel": "sketch_dmma_kernel",
                  "ms_per_launch": sk["ms"], "ctas": sk["ctas"], "splits": sk["splits"], "tma": sk["tma"],
                  "algorithmic_bytes": bytes_alg, "algorithmic_flops": flops_alg})
