@@ -295,6 +295,7 @@ struct Workspace {
   DevBuf<uint8_t> col_mask, row_mask;
   DevBuf<char> state, lupp_scratch, qrcp_scratch;
   DevBuf<double> Wq;  // Y copy for the QRCP column selection (qrcp_pivot_cols takes W by value)
+  DevBuf<int> commit_counter;  // arrivals of the U block's CTAs (fused commit), reset by the last
   DevBuf<double> At;  // row-major copy of A (n x m column-major, ld ldAt) for the row gathers A(I_k, :)
   int64_t ldAt = 0;
   DevBuf<double> scal;  // [0] asq, [1] ysq
@@ -585,6 +586,8 @@ void run_iterative_cur(itercur_run* run) {
   }();
   const int64_t y_parts = fused_ub ? ts_gemm_ublock_parts(n) : ts_gemm_grid_size(n, static_cast<int>(cp));
   ws.part.alloc(std::max<int64_t>(y_parts, 1));
+  ws.commit_counter.alloc(1);
+  CK(cudaMemsetAsync(ws.commit_counter.p, 0, sizeof(int), st));
 
   // initial Wc = Y^T(:, 0:b)
   CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, ldn, st));
@@ -653,7 +656,7 @@ void run_iterative_cur(itercur_run* run) {
         // (1) column selection: LUPP on W = Y^T (select_columns, select.cpp:121-139); on the
         //     cluster path the same kernel also opens the iteration (iter_begin) and, after its
         //     last pivot, gathers R~(:,J_k) (GEMM1's B) and Y(:,J_k) (the downdate's B)
-        bool col_fused = false;
+        bool col_fused = false, begin_fused = false;
         {
           LuppArgs la{};
           la.W = ws.Wc.p;
@@ -672,14 +675,21 @@ void run_iterative_cur(itercur_run* run) {
           la.d_gen_k = &d_ctl->k;
           la.gen_base = gen_base;
           la.gen_which = 0;
-          col_fused = !col_qrcp && fused_ub && !fuse_off && lupp_fuses_iteration_work(la);
-          if (col_fused) {
+          const bool fusable = !col_qrcp && fused_ub && lupp_fuses_iteration_work(la);
+          col_fused = fusable && !fuse_off;
+          // the iteration begin alone (no gathers) folded into the cluster LUPP
+          // (measured: column-selection phase 6.90 -> 6.57 ms at config 2; ITERCUR_NO_LUPP_FUSE_BEGIN)
+          static const bool begin_only = !env_flag("ITERCUR_NO_LUPP_FUSE_BEGIN");
+          if (col_fused || (fusable && begin_only)) {
             la.begin_ctl = d_ctl;
             la.begin_slot = slot;
-            la.post[0] = {run->Rt.p, run->ldR, 1, ldbg, &d_ctl->r, ws.Bg.p, ldbg, B};
-            la.post[1] = {ws.Y.p, 1, cp, cp, nullptr, ws.Yg.p, cp, B};
+            begin_fused = true;
           } else {
             CK(launch_iter_begin(d_ctl, slot, st));
+          }
+          if (col_fused) {
+            la.post[0] = {run->Rt.p, run->ldR, 1, ldbg, &d_ctl->r, ws.Bg.p, ldbg, B};
+            la.post[1] = {ws.Y.p, 1, cp, cp, nullptr, ws.Yg.p, cp, B};
           }
           if (col_qrcp) {  // QRCP over the c-row columns of (a copy of) Y, select.cpp:79-117,121-139
             CK(cudaMemcpyAsync(ws.Wq.p, ws.Y.p, sizeof(double) * cp * n, cudaMemcpyDeviceToDevice, st));
@@ -779,12 +789,32 @@ void run_iterative_cur(itercur_run* run) {
           if (!col_fused)
             CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
           TsGemmParams p = ublock_params(ldbg, slot, arr);
+          // the commit in the U block's last CTA instead of its own kernel: measured slower
+          // (config 2 phase sums 32.17 vs 31.60 ms: every CTA's release fence before its arrival
+          // lengthens the kernel more than the launch it saves), so opt-in: ITERCUR_FUSED_COMMIT
+          static const bool fused_commit = env_flag("ITERCUR_FUSED_COMMIT");
+          if (fused_commit) {
+            p.commit.ctl = d_ctl;
+            p.commit.slot = slot;
+            p.commit.row_idx = arr.row_idx;
+            p.commit.col_idx = arr.col_idx;
+            p.commit.I_all = run->dI.p;
+            p.commit.J_all = run->dJ.p;
+            p.commit.row_mask = ws.row_mask.p;
+            p.commit.col_mask = ws.col_mask.p;
+            p.commit.counter = ws.commit_counter.p;
+          }
           CK(run_ts_gemm_ublock(p, st));
-          batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0) - (col_fused ? 3 : 0) - (row_fused ? 1 : 0);
+          batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0) - (col_fused ? 2 : 0) - (begin_fused ? 1 : 0) -
+                            (row_fused ? 1 : 0);
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));  // downdate fused into the core step
-          CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p,
-                           y_parts, st));
+          if (!fused_commit) {
+            CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p,
+                             y_parts, st));
+          } else {
+            batch_launches -= 1;
+          }
           continue;
         }
         {

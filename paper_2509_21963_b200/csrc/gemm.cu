@@ -431,6 +431,21 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
     for (int q = 0; q < WARPS; ++q) s += red[q];
     p.norm_part[blockIdx.x] = s;
   }
+  if (p.commit.ctl) {
+    // the last finishing CTA commits the iteration (replaces the commit kernel's launch): every
+    // CTA's partial is published before its arrival, so the fixed-order sum sees all of them
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(p.commit.counter, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      commit_body<WARPS * 32>(p.commit, p.norm_part, gridDim.x, red);
+      if (threadIdx.x == 0) *p.commit.counter = 0;
+    }
+  }
 }
 
 static int ts_gemm_nt_host(int n) { return n <= 8 ? 1 : (n <= 16 ? 2 : (n <= 24 ? 3 : (n <= 32 ? 4 : 9))); }

@@ -51,6 +51,7 @@ struct TsGemmParams {
   // device-resident loop control: skip when ctl->done; K = min(K, ctl->r) when k_from_r;
   // A += ctl->r * a_off_per_r and C0 += ctl->r * c0_off_per_r (elements)
   const IterCtl* ctl = nullptr;
+  CommitArgs commit;        // U block: when commit.ctl is set, the last CTA also commits the iteration
   int64_t dbg_k = 0;         // ... recorded at iteration ctl->k == dbg_k
   long long* dbg = nullptr;  // optional trace (U block): [0..15] clock64 phases of CTA (0,0,0); [32+2c] globaltimer entry/exit of CTA c
   int k_from_r = 0;

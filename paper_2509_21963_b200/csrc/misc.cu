@@ -427,58 +427,27 @@ cudaError_t launch_width(IterState* slot, const IterCtl* ctl, cudaStream_t st) {
 }
 
 // Iteration commit (driver.cpp:102-159).
-__global__ void commit_kernel(IterCtl* ctl, IterState* slot, IterArrays arr, int64_t* __restrict__ I_all,
-                              int64_t* __restrict__ J_all, uint8_t* __restrict__ row_mask,
-                              uint8_t* __restrict__ col_mask, const double* __restrict__ y_partials,
-                              int64_t y_parts) {
-  __shared__ int s_stop;
+__global__ void commit_kernel(CommitArgs c, const double* __restrict__ y_partials, int64_t y_parts) {
   __shared__ double red[8];
   griddep_wait();
   griddep_launch_dependents();
-  if (ctl->done) return;
-  {  // ||Y||^2 of the downdated residual: fixed-order sum of the GEMM's per-CTA partials
-    double sq = 0.0;
-    for (int64_t i = threadIdx.x; i < y_parts; i += blockDim.x) sq += y_partials[i];
-    const double tot = block_sum<256>(sq, red);
-    if (threadIdx.x == 0) ctl->ysq = tot;
-  }
-  const int width = min(slot->ncols, slot->nrows);
-  const int64_t r = ctl->r;
-  if (threadIdx.x == 0) s_stop = (slot->ncols == 0 || slot->nrows == 0) ? 1 : 0;
-  __syncthreads();
-  if (s_stop) {  // empty column or row selection -> ResidualExhausted, factors unchanged
-    if (threadIdx.x == 0) {
-      ctl->done = 1;
-      ctl->status = 2;
-    }
-    return;
-  }
-  for (int q = threadIdx.x; q < width; q += blockDim.x) {
-    I_all[r + q] = arr.row_idx[q];
-    J_all[r + q] = arr.col_idx[q];
-    row_mask[arr.row_idx[q]] = 1;
-    col_mask[arr.col_idx[q]] = 1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const double rho = ctl->ga_norm > 0.0 ? sqrt(ctl->ysq) / ctl->ga_norm : 0.0;
-    slot->width = width;
-    slot->ysq = ctl->ysq;
-    slot->rho = rho;
-    ctl->rho = rho;
-    ctl->r = r + width;
-    ctl->k += 1;
-    if (rho <= ctl->threshold) {
-      ctl->done = 1;
-      ctl->status = 0;  // Converged
-    }
-  }
+  if (c.ctl->done) return;
+  commit_body<256>(c, y_partials, y_parts, red);
 }
+
 cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, int64_t* I_all, int64_t* J_all,
                           uint8_t* row_mask, uint8_t* col_mask, const double* y_partials, int64_t y_parts,
                           cudaStream_t st) {
-  return launch_ex(commit_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), ctl, slot, arr, I_all, J_all, row_mask,
-                   col_mask, y_partials, y_parts);
+  CommitArgs c;
+  c.ctl = ctl;
+  c.slot = slot;
+  c.row_idx = arr.row_idx;
+  c.col_idx = arr.col_idx;
+  c.I_all = I_all;
+  c.J_all = J_all;
+  c.row_mask = row_mask;
+  c.col_mask = col_mask;
+  return launch_ex(commit_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), c, y_partials, y_parts);
 }
 
 }  // namespace itercur_b200

@@ -47,6 +47,71 @@ struct IterArrays {
   double* row_best;
   double* row_second;
 };
+// Everything an iteration commit touches (driver.cpp:102-159): run by commit_kernel, or by the
+// last CTA of the fused U-block kernel (CommitArgs::counter, reset by that CTA).
+struct CommitArgs {
+  IterCtl* ctl = nullptr;
+  IterState* slot = nullptr;
+  const int64_t* row_idx = nullptr;
+  const int64_t* col_idx = nullptr;
+  int64_t* I_all = nullptr;
+  int64_t* J_all = nullptr;
+  uint8_t* row_mask = nullptr;
+  uint8_t* col_mask = nullptr;
+  int* counter = nullptr;  // fused form only
+};
+#ifdef __CUDACC__
+}  // namespace itercur_b200
+#include "common.cuh"
+namespace itercur_b200 {
+// One CTA of THREADS threads: ||Y||^2 from the per-CTA partials in a fixed order, the stop
+// tests, the index append and the masks. `red` holds THREADS / 32 doubles.
+template <int THREADS>
+__device__ inline void commit_body(const CommitArgs& c, const double* __restrict__ y_partials, int64_t y_parts,
+                                   double* red) {
+  __shared__ int s_stop;
+  IterCtl* ctl = c.ctl;
+  IterState* slot = c.slot;
+  {  // ||Y||^2 of the downdated residual: fixed-order sum of the GEMM's per-CTA partials
+    double sq = 0.0;
+    for (int64_t i = threadIdx.x; i < y_parts; i += THREADS) sq += y_partials[i];
+    const double tot = block_sum<THREADS>(sq, red);
+    if (threadIdx.x == 0) ctl->ysq = tot;
+  }
+  const int width = min(slot->ncols, slot->nrows);
+  const int64_t r = ctl->r;
+  if (threadIdx.x == 0) s_stop = (slot->ncols == 0 || slot->nrows == 0) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) {  // empty column or row selection -> ResidualExhausted, factors unchanged
+    if (threadIdx.x == 0) {
+      ctl->done = 1;
+      ctl->status = 2;
+    }
+    return;
+  }
+  for (int q = threadIdx.x; q < width; q += THREADS) {
+    c.I_all[r + q] = c.row_idx[q];
+    c.J_all[r + q] = c.col_idx[q];
+    c.row_mask[c.row_idx[q]] = 1;
+    c.col_mask[c.col_idx[q]] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double rho = ctl->ga_norm > 0.0 ? sqrt(ctl->ysq) / ctl->ga_norm : 0.0;
+    slot->width = width;
+    slot->ysq = ctl->ysq;
+    slot->rho = rho;
+    ctl->rho = rho;
+    ctl->r = r + width;
+    ctl->k += 1;
+    if (rho <= ctl->threshold) {
+      ctl->done = 1;
+      ctl->status = 0;  // Converged
+    }
+  }
+}
+#endif
+
 inline size_t iter_state_bytes(int b) { return sizeof(IterState) + 6 * sizeof(double) * static_cast<size_t>(b); }
 inline IterArrays iter_arrays(void* base, int b) {
   char* p = static_cast<char*>(base) + sizeof(IterState);
