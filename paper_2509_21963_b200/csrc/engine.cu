@@ -87,6 +87,21 @@ cudaStream_t work_stream() {
   return s;
 }
 
+// A second work stream for graph branches off the iteration's critical path, with its two events.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  thread_local SideStream ss;
+  if (!ss.s) {
+    CK(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  return ss;
+}
+
 void configure_mempool_once() {
   static bool done = false;
   if (done) return;
@@ -707,6 +722,19 @@ void run_iterative_cur(itercur_run* run) {
         //     the GEMM loader would re-fetch one 32-B sector per element in every CTA)
         if (!col_fused)
           CK(launch_gather(run->Rt.p, run->ldR, 1, ldbg, arr.col_idx, &slot->ncols, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        // Y(:, J_k) for the U block's downdate on a side branch: it needs only J_k, so it can run
+        // beside the row residual and the row selection (joined before the U block). Measured
+        // slower inside the batch graphs (config 2: 35.6 vs 32.6 ms; the concurrent kernel delays
+        // the cluster launches), so opt-in: ITERCUR_SIDE_GATHER
+        static const bool y_branch = env_flag("ITERCUR_SIDE_GATHER");
+        const bool y_side = fused_ub && !col_fused && y_branch;
+        if (y_side) {
+          SideStream& ss = side_stream();
+          CK(cudaEventRecord(ss.fork, st));
+          CK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->ncols, B, ws.Yg.p, cp, ss.s, d_ctl, false));
+          CK(cudaEventRecord(ss.join, ss.s));
+        }
         {
           TsGemmParams p;
           p.M = m;
@@ -786,7 +814,9 @@ void run_iterative_cur(itercur_run* run) {
         if (fused_ub) {
           // Y(:, J_k) before the downdate, then one kernel: U_k^T, the solves against D_k,
           // R~ rows, Y^T -= R~_k^T Y(:, J_k)^T, ||Y||^2 partials and Wc
-          if (!col_fused)
+          if (y_side)
+            CK(cudaStreamWaitEvent(st, side_stream().join, 0));
+          else if (!col_fused)
             CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
           TsGemmParams p = ublock_params(ldbg, slot, arr);
           // the commit in the U block's last CTA instead of its own kernel: measured slower
