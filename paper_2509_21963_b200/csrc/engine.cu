@@ -519,16 +519,19 @@ void run_iterative_cur(itercur_run* run) {
   }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
   // row-major copy of A (when it is a modest share of free HBM): the U block's base A(I_k, :)
-  // then reads |I_k| contiguous rows instead of one DRAM burst per element. Made once the run
-  // has shown it is long enough to repay the transpose (measured at config 2: ~8 us per
-  // iteration saved for a 0.5 ms transpose; at config 3, 8 iterations, it would not pay).
-  static const bool at_off = env_flag("ITERCUR_NO_ROWMAJOR_A"), at_eager = env_flag("ITERCUR_ROWMAJOR_A");
-  const int64_t at_after_iters = at_eager ? 0 : 3 * kBatch;
+  // then reads |I_k| contiguous rows instead of one DRAM burst per element (~8 us per
+  // iteration at config 2).
+  // Made up front for A <= 2 GB (transpose <= ~0.6 ms; config 2: 32.3 ms eager vs 33.1 lazy after
+  // 24 iterations — the lazy path's 1.6 GB pool allocation stalls the host between batches);
+  // larger matrices skip it unless forced (config 3, 8 iterations, would pay 6 ms for 20 GB).
+  // ITERCUR_ROWMAJOR_A=1 forces it, ITERCUR_NO_ROWMAJOR_A=1 disables it.
+  static const bool at_off = env_flag("ITERCUR_NO_ROWMAJOR_A"), at_force = env_flag("ITERCUR_ROWMAJOR_A");
   auto maybe_make_rowmajor_a = [&](int64_t iters_done) -> bool {
-    if (at_off || ws.At.p || iters_done < at_after_iters) return false;
+    if (at_off || ws.At.p || iters_done > 0) return false;
+    const double bytes = 8.0 * static_cast<double>(ldn) * static_cast<double>(m);
+    if (!at_force && bytes > 2e9) return false;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const double bytes = 8.0 * static_cast<double>(ldn) * static_cast<double>(m);
     if (bytes > 0.3 * static_cast<double>(free_b)) return false;
     ws.At.alloc(static_cast<size_t>(ldn) * m);
     ws.ldAt = ldn;
@@ -552,6 +555,35 @@ void run_iterative_cur(itercur_run* run) {
     g1_dbg.alloc(32 + 2 * 8192);
     CK(cudaMemsetAsync(g1_dbg.p, 0, sizeof(long long) * (32 + 2 * 8192), st));
   }
+  // the row-residual GEMM: S_row = A(:,J_k) - L * Rt(:,J_k) into L's next columns and the row LUPP input
+  auto gemm1_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
+    TsGemmParams p;
+    p.M = m;
+    p.K = ldbg;
+    p.ctl = d_ctl;
+    p.k_from_r = 1;
+    p.N = B;
+    p.d_n = &slot->ncols;
+    p.A = run->L.p;
+    p.lda = run->ldL;
+    p.B = ws.Bg.p;  // B(k, q) = Rt(k, J_k[q])
+    p.bsk = 1;
+    p.bsn = ldbg;
+    p.base_mode = kBaseGatherCols;
+    p.src = A;
+    p.lds = lda;
+    p.idx = arr.col_idx;
+    p.alpha = -1.0;
+    p.out_mode = kOutColMajor;
+    p.C0 = run->L.p;
+    p.c0_off_per_r = run->ldL;
+    p.ldc0 = run->ldL;
+    p.C1 = ws.Wr.p;
+    p.ldc1 = ldm;
+    p.dbg = g1_dbg.p;
+    p.dbg_k = g1_trace_k;
+    return p;
+  };
   // the fused U-block kernel (GEMM2 + solves + downdate) when the shape qualifies
   auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
     TsGemmParams p;
@@ -612,16 +644,28 @@ void run_iterative_cur(itercur_run* run) {
   static uint32_t run_counter = 0;
   const uint32_t gen_base = ((++run_counter) & 0x3FFu) << 21;  // LUPP slot-tag generations
   const bool use_graph = !evs.on && !env_flag("ITERCUR_NO_GRAPH");
-  cudaGraphExec_t graph_exec = nullptr;
-  int64_t graph_cap = -1;
-  struct ExecGuard {
-    cudaGraphExec_t* e;
-    ~ExecGuard() {
-      if (*e) cudaGraphExecDestroy(*e);
+  // batch graphs by split plan (they differ only in the GEMMs' K-split counts), valid for one
+  // factor capacity and one U-block base; the next batch's graph is captured while the current
+  // one runs on the device
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+  };
+  struct GraphCache {
+    std::vector<std::pair<int, GraphEntry>> v;
+    GraphEntry* find(int sig) {
+      for (auto& e : v)
+        if (e.first == sig) return &e.second;
+      return nullptr;
     }
-  } exec_guard{&graph_exec};
+    void clear() {
+      for (auto& e : v) cudaGraphExecDestroy(e.second.exec);
+      v.clear();
+    }
+    ~GraphCache() { clear(); }
+  } graphs;
+  int64_t graph_cap = -1;
   int64_t k_host = 0, r_host = 0;
-  int64_t graph_batch_launches = 0;  // kernels per replayed batch graph
   int64_t ev_i = 2;
   std::vector<size_t> iter_events;
   bool done = false;
@@ -646,6 +690,27 @@ void run_iterative_cur(itercur_run* run) {
     }
     const bool at_new = maybe_make_rowmajor_a(k_host);  // (re-capture: the U block's base changes)
     const int64_t ldbg = run->capL;
+    // the GEMMs' K-split counts are planned for the largest K this batch can reach (the kernels
+    // take K from the device loop control): few splits while the factors are thin. The batch
+    // graph is re-captured only when a planned count changes.
+    auto k_plan_for = [&](int64_t r0) {
+      return std::max<int64_t>(1, std::min<int64_t>(ldbg, r0 + static_cast<int64_t>(kBatch) * b));
+    };
+    auto plan_sig_for = [&](int64_t kp) {
+      IterState* slot0 = reinterpret_cast<IterState*>(slots);
+      const IterArrays arr0 = iter_arrays(slot0, B);
+      TsGemmParams g1 = gemm1_params(ldbg, slot0, arr0);
+      g1.k_plan = kp;
+      int sig = ts_gemm_planned_splits(g1, false);
+      if (fused_ub) {
+        TsGemmParams ub = ublock_params(ldbg, slot0, arr0);
+        ub.k_plan = kp;
+        sig = sig * 64 + ts_gemm_planned_splits(ub, true);
+      }
+      return sig;
+    };
+    int64_t k_plan = k_plan_for(r_host);
+    const int plan_sig = plan_sig_for(k_plan);
     // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
     int64_t batch_launches = 0;
@@ -736,31 +801,8 @@ void run_iterative_cur(itercur_run* run) {
           CK(cudaEventRecord(ss.join, ss.s));
         }
         {
-          TsGemmParams p;
-          p.M = m;
-          p.K = ldbg;
-          p.ctl = d_ctl;
-          p.k_from_r = 1;
-          p.N = B;
-          p.d_n = &slot->ncols;
-          p.A = run->L.p;
-          p.lda = run->ldL;
-          p.B = ws.Bg.p;  // B(k, q) = Rt(k, J_k[q])
-          p.bsk = 1;
-          p.bsn = ldbg;
-          p.base_mode = kBaseGatherCols;
-          p.src = A;
-          p.lds = lda;
-          p.idx = arr.col_idx;
-          p.alpha = -1.0;
-          p.out_mode = kOutColMajor;
-          p.C0 = run->L.p;
-          p.c0_off_per_r = run->ldL;
-          p.ldc0 = run->ldL;
-          p.C1 = ws.Wr.p;
-          p.ldc1 = ldm;
-          p.dbg = g1_dbg.p;
-          p.dbg_k = g1_trace_k;
+          TsGemmParams p = gemm1_params(ldbg, slot, arr);
+          p.k_plan = k_plan;
           CK(run_ts_gemm(p, st));
         }
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 2), st));
@@ -819,6 +861,7 @@ void run_iterative_cur(itercur_run* run) {
           else if (!col_fused)
             CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
           TsGemmParams p = ublock_params(ldbg, slot, arr);
+          p.k_plan = k_plan;
           // the commit in the U block's last CTA instead of its own kernel: measured slower
           // (config 2 phase sums 32.17 vs 31.60 ms: every CTA's release fence before its arrival
           // lengthens the kernel more than the launch it saves), so opt-in: ITERCUR_FUSED_COMMIT
@@ -914,36 +957,56 @@ void run_iterative_cur(itercur_run* run) {
       }
     };
     const auto tc0 = hclock::now();
+    auto capture = [&](int64_t kp) {
+      k_plan = kp;
+      GraphEntry e;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_batch();
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CK(cudaStreamEndCapture(st, &g));
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      e.launches = batch_launches;
+      return e;
+    };
     if (use_graph) {
-      if (!graph_exec || graph_cap != run->capL || at_new) {
-        if (graph_exec) cudaGraphExecDestroy(graph_exec);
-        graph_exec = nullptr;
-        cudaGraph_t g = nullptr;
-        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-          enqueue_batch();
-        } catch (...) {
-          cudaStreamEndCapture(st, &g);
-          if (g) cudaGraphDestroy(g);
-          throw;
-        }
-        CK(cudaStreamEndCapture(st, &g));
-        const cudaError_t ie = cudaGraphInstantiate(&graph_exec, g, 0);
-        cudaGraphDestroy(g);
-        CK(ie);
+      if (graph_cap != run->capL || at_new) {
+        graphs.clear();
         graph_cap = run->capL;
+      }
+      GraphEntry* ge = graphs.find(plan_sig);
+      if (!ge) {
+        graphs.v.emplace_back(plan_sig, capture(k_plan));
+        ge = &graphs.v.back().second;
         t_capture = us_since(tc0);
       }
-      CK(cudaGraphLaunch(graph_exec, st));
+      CK(cudaGraphLaunch(ge->exec, st));
+      batch_launches = ge->launches;
     } else {
       enqueue_batch();
     }
     t_launch = us_since(tc0) - t_capture;
-    if (use_graph && batch_launches == 0) batch_launches = graph_batch_launches;
-    graph_batch_launches = batch_launches;
     run->launches += batch_launches;
     // one D2H read per batch: the batch's records + the loop control
     CK(cudaMemcpyAsync(ws.h_state, ws.state.p, slot_bytes * kBatch + sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+    // while the device runs this batch: the graph of the next batch's plan (its K bound is at
+    // most r + 2 batches of b), if the capacity will not have to grow first
+    if (use_graph && std::min(r_host + 2 * static_cast<int64_t>(kBatch) * b, max_rank + b) <= run->capL) {
+      const int64_t kn = k_plan_for(r_host + static_cast<int64_t>(kBatch) * b);
+      const int sn = plan_sig_for(kn);
+      if (!graphs.find(sn)) {
+        const auto tp = hclock::now();
+        graphs.v.emplace_back(sn, capture(kn));
+        t_capture += us_since(tp);
+      }
+    }
     const auto ts0 = hclock::now();
     CK(cudaStreamSynchronize(st));
     t_sync = us_since(ts0);

@@ -687,12 +687,18 @@ static int gemm_splits(int64_t tiles, int64_t K, int kt) {
   const int forced = g_splits_override > 0 ? g_splits_override : forced_env;
   const int64_t stages = ceil_div(K, kt);
   int s = forced > 0 ? forced : static_cast<int>(ceil_div(4 * kNumSMs, std::max<int64_t>(tiles, 1)));
-  s = static_cast<int>(std::min<int64_t>(s, std::max<int64_t>(1, stages / 4)));
+  // a split must own >= 10 k-stages: below that one wave of unsplit CTAs is faster (row-residual
+  // shape 20000 x 20, B200: K = 400 -> 26.8 us unsplit vs 28.9 at 2 splits; K = 1600 -> 86 vs 76)
+  s = static_cast<int>(std::min<int64_t>(s, std::max<int64_t>(1, stages / 10)));
   return std::max(1, std::min(s, 8));
 }
 
+static thread_local bool g_plan_only = false;  // ts_gemm_planned_splits: compute the grid, do not launch
+static thread_local int g_planned_z = 0;
 template <typename Kern>
 static cudaError_t launch_split(Kern kern, dim3 grid, int threads, int bytes, const TsGemmParams& p, cudaStream_t st) {
+  g_planned_z = static_cast<int>(grid.z);
+  if (g_plan_only) return cudaSuccess;
   return launch_ex(kern, grid, dim3(threads), bytes, st, dim3(grid.z > 1 ? 1 : 0, 1, grid.z), p);
 }
 
@@ -707,7 +713,7 @@ static cudaError_t launch_cfg(const TsGemmParams& p, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, Cfg::BM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
-  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.K, kGemmKT));
+  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.k_plan > 0 ? p.k_plan : p.K, kGemmKT));
   return launch_split(ts_gemm_kernel<NT, WARPS>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
 }
 
@@ -724,7 +730,7 @@ static cudaError_t launch_lean(const TsGemmParams& p, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, Cfg::BM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
-  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.K, KT));
+  grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.k_plan > 0 ? p.k_plan : p.K, KT));
   return launch_split(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
 }
 
@@ -774,7 +780,8 @@ static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
   // the cluster barrier, so deeper splits cost more than they save (config 2, profile-mode
   // phase sums: 7.64 ms at 2 splits vs 7.68 at 3 and 7.99 at 4)
   const int64_t tiles = ceil_div(p.M, 64);
-  g_splits_override = ub_splits > 0 ? ub_splits : std::min(2, gemm_splits(tiles, p.K, lean == 2 ? 32 : 16));
+  g_splits_override =
+      ub_splits > 0 ? ub_splits : std::min(2, gemm_splits(tiles, p.k_plan > 0 ? p.k_plan : p.K, lean == 2 ? 32 : 16));
   const cudaError_t e = lean == 2 ? launch_lean<NT, 4, 32, 3, true>(p, st) : launch_lean<NT, 4, 16, 4, true>(p, st);
   g_splits_override = 0;
   return e;
@@ -796,6 +803,17 @@ int ts_gemm_nt(int n) { return static_cast<int>(std::min<int64_t>(9, std::max<in
 int64_t ts_gemm_grid_size(int64_t M, int N) {
   const int nt = ts_gemm_nt(N);
   return ceil_div(M, gemm_warps(M) * 16) * ceil_div(N, nt * 8);
+}
+
+int ts_gemm_planned_splits(const TsGemmParams& p, bool ublock) {
+  g_plan_only = true;
+  g_planned_z = 0;
+  if (ublock)
+    run_ts_gemm_ublock(p, nullptr);
+  else
+    run_ts_gemm(p, nullptr);
+  g_plan_only = false;
+  return g_planned_z;
 }
 
 cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st) {

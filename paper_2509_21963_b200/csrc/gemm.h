@@ -52,6 +52,7 @@ struct TsGemmParams {
   // A += ctl->r * a_off_per_r and C0 += ctl->r * c0_off_per_r (elements)
   const IterCtl* ctl = nullptr;
   CommitArgs commit;        // U block: when commit.ctl is set, the last CTA also commits the iteration
+  int64_t k_plan = 0;        // host-side hint: the K the split count is planned for (0: K)
   int64_t dbg_k = 0;         // ... recorded at iteration ctl->k == dbg_k
   long long* dbg = nullptr;  // optional trace (U block): [0..15] clock64 phases of CTA (0,0,0); [32+2c] globaltimer entry/exit of CTA c
   int k_from_r = 0;
@@ -73,6 +74,8 @@ struct TsGemmParams {
 
 cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st);
 int64_t ts_gemm_grid_size(int64_t M, int N);
+// grid.z (K splits) the launch of these parameters would use (no launch)
+int ts_gemm_planned_splits(const TsGemmParams& p, bool ublock);
 // the fused U-block GEMM: returns cudaErrorNotSupported when the shape / layout does not
 // qualify (the caller then runs GEMM + rows_lu_solve + downdate GEMM separately)
 bool ts_gemm_ublock_supported(const TsGemmParams& p);
