@@ -221,7 +221,7 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
     shard = a[:, lo:hi].t().contiguous().t()
     del a
     torch.cuda.synchronize()
-    run = dict(run_cfg)
+    run = dict(run_cfg, column_exchange=args.exchange)
     res = None
     for _ in range(args.warmup):
         res = iterative_cur_sharded(shard, lo, n, **run)
@@ -255,7 +255,8 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
         line = {"metric": METRIC, "value": m * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
-                "config": {**cfg_line, "parallelism": f"column-sharded x{world}"},
+                "config": {**cfg_line, "parallelism": f"column-sharded x{world}",
+                           "column_exchange": args.exchange},
                 "e2e": {"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
                         "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms},
                 "clocks": clk.summary(),
@@ -278,6 +279,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="CPU sample budget (s)")
     ap.add_argument("--ref-iters", type=int, default=0, help="iterations to tolerance for the CPU estimate")
+    ap.add_argument("--exchange", default="sketch", choices=["sketch", "candidates"],
+                    help="--sharded column selection: replicate Y per iteration, or exchange pivot candidates per step")
     ap.add_argument("--sharded", action="store_true",
                     help="N > 1: one matrix column-sharded over the GPUs (strong scaling) instead of N replicas")
     args = ap.parse_args()

@@ -259,21 +259,23 @@ double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cud
 }
 
 // ---- the sketch apply (make_sketch, sketch.cpp:10-24), shared by the run and the stage entries.
-// The sparse-sign operator can also be applied as a sparse operator (8 adds per element of A,
-// sketch.cu sparse_sketch_kernel; bitwise equal to the oracle's sparse loop). Measured on B200
-// it is slower than the DMMA contraction over the materialised +-1 operator at every shape
-// tried (40000 x 20000, c = 55: 3.9 ms vs 2.7 ms; its list walk is bound by the shared-memory
-// read of every (row, target) pair and a serial add chain per sketch row), so it is opt-in:
-// ITERCUR_SPARSE_SKETCH=1.
-constexpr int64_t kSparseSketchMinCp = 1 << 30;
+// Sparse-sign operator, three kernels (ITERCUR_SPARSE_SKETCH selects; default: the integer path):
+//   2  sliced-integer tensor path (sketch.cu sparse_sketch_imma_kernel): A as 7 int8 slices of a
+//      56-bit fixed-point form x the int8 +-1 operator on mma.sync s8 — HBM-bound at c_pad <= 64;
+//   0  FP64 DMMA contraction over the materialised +-1 operator (FP64-bound once c_pad > ~24);
+//   1  the sparse list walk (bitwise equal to the oracle's sparse loop; bound by shared-memory
+//      reads of every (row, target) pair: 3.9 ms vs DMMA 2.7 ms at 40000 x 20000, c = 55).
 struct SketchBuffers {
   DevBuf<double> S, ws;
 };
-static bool sparse_sketch_path(int kind, int64_t c, int64_t cp, int zeta_eff) {
-  if (kind != kSketchSparseSign || !sparse_sketch_supported(c, zeta_eff)) return false;
+enum SparseMode { kSparseDense = 0, kSparseList = 1, kSparseImma = 2 };
+static int sparse_sketch_mode(int kind, int64_t c, int64_t cp, int zeta_eff, const double* A, int64_t lda) {
+  if (kind != kSketchSparseSign) return kSparseDense;
   const char* e = getenv("ITERCUR_SPARSE_SKETCH");
-  if (e && e[0]) return e[0] != '0';
-  return cp >= kSparseSketchMinCp;
+  const int want = (e && e[0]) ? atoi(e) : kSparseImma;
+  if (want == kSparseList && sparse_sketch_supported(c, zeta_eff)) return kSparseList;
+  if (want == kSparseImma && sparse_sketch_imma_supported(A, lda, cp)) return kSparseImma;
+  return kSparseDense;
 }
 static int zeta_effective(int kind, int sparse_nnz, int64_t c) {
   return kind == kSketchSparseSign ? static_cast<int>(std::min<int64_t>(std::max(sparse_nnz, 1), c)) : 0;
@@ -286,11 +288,19 @@ static int apply_sketch(const double* A, int64_t m, int64_t n, int64_t lda, int 
                         bool operator_ready = false) {
   const int ze = zeta_effective(kind, sparse_nnz, c);
   const double scale = kind == kSketchSparseSign ? 1.0 / std::sqrt(static_cast<double>(ze)) : 1.0;
-  if (sparse_sketch_path(kind, c, cp, ze)) {
+  const int mode = sparse_sketch_mode(kind, c, cp, ze, A, lda);
+  if (mode == kSparseList) {
     const int64_t wse = sparse_sketch_workspace_elems(m, n, cp, ze);
     if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
     CK(run_sketch_apply_sparse(A, m, n, lda, seed, c, cp, ze, scale, Y, buf.ws.p, wse, stats, st, info));
     return 4;
+  }
+  if (mode == kSparseImma) {
+    // the int8 operator lives in the workspace; it is regenerated per call (m threads)
+    const int64_t wse = sparse_sketch_imma_workspace_elems(m, n, cp);
+    if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
+    CK(run_sketch_apply_sparse_imma(A, m, n, lda, seed, c, cp, ze, scale, Y, buf.ws.p, wse, stats, st, info, false));
+    return 6;
   }
   const int64_t ldg = round_up(m, 32);
   int launches = 0;
@@ -1644,9 +1654,15 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     Y.alloc(static_cast<size_t>(cp) * n);
     scal.alloc(2);
     SketchLaunchInfo info;
-    const bool sparse = sparse_sketch_path(k, c, cp, zeta_effective(k, 8, c));
+    const int smode = sparse_sketch_mode(k, c, cp, zeta_effective(k, 8, c), dA, lda);
+    const bool sparse = smode == kSparseList;
     SketchBuffers sb;
-    if (!sparse) {
+    if (smode == kSparseImma) {
+      wsb.alloc(sparse_sketch_imma_workspace_elems(m, n, cp));
+      CK(run_sketch_apply_sparse_imma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
+                                      static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
+                                      false, false));
+    } else if (!sparse) {
       S.alloc(static_cast<size_t>(cp) * ldg);
       const int64_t wse = sketch_workspace_elems(m, n, cp);
       wsb.alloc(wse);
@@ -1655,7 +1671,11 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     // the sparse path is timed whole (operator lists + apply + norm reductions); the dense
     // path times its DMMA kernel alone
     auto once = [&]() {
-      if (sparse)
+      if (smode == kSparseImma)  // the integer-path kernel alone (operator already generated)
+        CK(run_sketch_apply_sparse_imma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
+                                        static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
+                                        true, true));
+      else if (sparse)
         apply_sketch(dA, m, n, lda, k, 8, 0, kStreamSketch, c, cp, Y.p, SketchStats{scal.p, scal.p + 1}, sb, st, &info);
       else
         CK(run_sketch_dmma_only(dA, m, n, lda, S.p, ldg, cp, Y.p, wsb.p, static_cast<int64_t>(wsb.count), st, &info));

@@ -699,4 +699,406 @@ cudaError_t run_sketch_apply_sparse(const double* A, int64_t m, int64_t n, int64
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ sparse-sign sketch, sliced-integer form
+// Y = Omega * A for the sparse-sign operator (+-1 at zeta positions per column of Omega, SURVEY.md
+// A.8; the scale 1/sqrt(zeta) is applied once by the reduce). The +-1 entries are exact in int8,
+// so the contraction runs on the integer tensor path (mma.sync m16n8k32 s8 x u8/s8 -> s32,
+// measured 1.1 POP/s on B200, tools/microbench/sparse_dispatch.cu) instead of FP64 DMMA: every
+// element x of A is written as a 56-bit two's-complement fixed-point integer relative to a
+// running per-column exponent E (the largest exponent seen so far in that column of this CTA's
+// row range): w = rint(x * 2^(1076 - E)), |w| < 2^54, and its 7 bytes are 7 int8 slices
+// (bytes 0..5 unsigned, byte 6 signed). Each slice is one MMA with the int8 operator tile; the
+// int32 accumulators are exact and are folded into FP64 (sum_t 2^(8t) acc_t * 2^(E - 1076))
+// only when a column's exponent grows (rare: once or twice per column) and at the end. The
+// per-element representation error is <= 2^(E-1077) (half an ulp of a 54-bit mantissa at the
+// column's running maximum), i.e. below FP64's own rounding of the sums.
+// Why: at c_pad = 56 (config 4) the DMMA form needs 112 flop per 8-byte element, 2.4x past the
+// FP64 ridge (37 TF / 6.45 TB/s); the sliced form needs 7 x 128 integer ops per element at
+// 1.1 POP/s, which sits under the HBM time.
+// Tiling: CTA = 4 warps x 8 columns (32 columns of A), K in steps of 32 rows staged by cp.async
+// through a cp.async ring (im_stages) (A tile: 32 columns x 256 B, column pitch 272 B: conflict-free 16-byte
+// fragment loads; operator tile: 16*MT rows x 32 B, pitch 48 B: conflict-free ldmatrix).
+// Warp fragment: A operand = operator tile (16*MT sketch rows x 32 rows of A, row-major, ldmatrix
+// .x4 per 16 sketch rows), B operand = slices of 32 rows x 8 columns (thread: column lane/4,
+// rows 4(lane%4)+{0..3} and +16: two 32-byte runs of its column), C = 16 sketch rows x 8 columns.
+constexpr int kImWarps = 4;
+constexpr int kImThreads = kImWarps * 32;
+constexpr int kImCols = kImWarps * 8;   // columns of A per CTA
+constexpr int kImColPitch = 272;        // bytes per staged column (32 doubles + 16)
+constexpr int kImOmPitch = 48;          // bytes per staged operator row (32 + 16)
+// ring depth: 2 CTAs per SM at MT >= 3 (registers), 3 below; deep enough for ~110 KB of A in
+// flight per SM either way
+template <int MT>
+constexpr int im_stages() { return MT <= 2 ? 6 : 8; }
+constexpr int kImSlices = 7;
+
+template <int MT>
+struct ImCfg {
+  static constexpr int kAStage = kImCols * kImColPitch;       // 8704 B
+  static constexpr int kOStage = 16 * MT * kImOmPitch;        // 768 * MT B
+  static constexpr int kStage = kAStage + kOStage;
+  static constexpr int kYacc = kImWarps * 16 * MT * 8 * 8;    // fp64 accumulators per warp: 16*MT x 8
+  static constexpr int kStages = im_stages<MT>();
+  static constexpr int kSmem = kStages * kStage + kYacc;
+};
+
+__global__ void gen_sparse_sign_i8_kernel(int8_t* O, int64_t ld8, int64_t c, int64_t m, uint64_t seed, int zeta_eff) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    int32_t rows[16];
+    int8_t signs[16];
+    sparse_sign_slots(seed, k, c, zeta_eff, rows, signs);
+    for (int t = 0; t < zeta_eff; ++t) O[rows[t] * ld8 + k] = signs[t];
+  }
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <bool SIGNED_B>
+__device__ __forceinline__ void imma_16x8x32(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (SIGNED_B)
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  else
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// 2^e for e in [-1022, 1023] (exact)
+__device__ __forceinline__ double pow2i(int e) { return __hiloint2double((e + 1023) << 20, 0); }
+
+// bytes t of four 64-bit integers (lo words l0..l3, hi words h0..h3) -> slice registers s[0..6]
+__device__ __forceinline__ void byte_transpose(uint32_t l0, uint32_t l1, uint32_t l2, uint32_t l3, uint32_t h0,
+                                               uint32_t h1, uint32_t h2, uint32_t h3, uint32_t (&s)[kImSlices]) {
+  const uint32_t a = __byte_perm(l0, l1, 0x5140), b = __byte_perm(l2, l3, 0x5140);
+  const uint32_t c = __byte_perm(l0, l1, 0x7362), d = __byte_perm(l2, l3, 0x7362);
+  s[0] = __byte_perm(a, b, 0x5410);
+  s[1] = __byte_perm(a, b, 0x7632);
+  s[2] = __byte_perm(c, d, 0x5410);
+  s[3] = __byte_perm(c, d, 0x7632);
+  const uint32_t e = __byte_perm(h0, h1, 0x5140), f = __byte_perm(h2, h3, 0x5140);
+  const uint32_t g = __byte_perm(h0, h1, 0x7362), h = __byte_perm(h2, h3, 0x7362);
+  s[4] = __byte_perm(e, f, 0x5410);
+  s[5] = __byte_perm(e, f, 0x7632);
+  s[6] = __byte_perm(g, h, 0x5410);
+}
+
+template <int MT, int NS>  // NS slices: bytes 0..NS-1 of w = rint(x * 2^(kSh - E)), top byte signed
+__global__ void __launch_bounds__(kImThreads, (MT <= 2 ? 3 : 2))
+    sparse_sketch_imma_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                              const int8_t* __restrict__ O, int64_t ld8, int64_t kps, int64_t c_pad,
+                              double* __restrict__ part, int64_t split_stride, double* __restrict__ asq_part) {
+  using Cfg = ImCfg<MT>;
+  constexpr int kSh = 1076 - 8 * (7 - NS);  // |w| < 2^(8 NS - 3)
+  extern __shared__ __align__(128) uint8_t ims[];
+  double* yacc = reinterpret_cast<double*>(ims + Cfg::kStages * Cfg::kStage);
+  __shared__ double red[kImWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kImCols;
+  const int64_t kb = static_cast<int64_t>(blockIdx.y) * kps * 32;
+  const int64_t ke = m < kb + kps * 32 ? m : kb + kps * 32;
+  const int nsteps = static_cast<int>(ke > kb ? (ke - kb + 31) / 32 : 0);
+  const uint32_t sbase = smem_u32(ims);
+
+  // producer mapping: A tile = 32 columns x 16 chunks of 16 B (thread: chunk tid & 15 of columns
+  // tid / 16 + 8u, u = 0..3); operator tile = 16*MT rows x 2 chunks (threads < 32*MT). Per-thread
+  // source pointers advance by one k-step (32 rows) per stage; only the last k-steps of the CTA's
+  // row range need the byte counts of a partial tile.
+  const int pcc = tid & 15, pcol = tid >> 4;
+  const double* pa = A + (j0 + pcol < n ? (j0 + pcol) * lda : 0) + kb + 2 * pcc;
+  const int64_t pstride = 8 * lda;  // 8 columns
+  uint32_t pvalid = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) pvalid |= (j0 + pcol + 8 * u < n) ? (1u << u) : 0u;
+  const uint32_t pdst = pcol * kImColPitch + pcc * 16;
+  const int8_t* po = O + (tid >> 1) * ld8 + kb + 16 * (tid & 1);
+  const uint32_t podst = Cfg::kAStage + (tid >> 1) * kImOmPitch + (tid & 1) * 16;
+  const bool all_cols = j0 + kImCols <= n;
+  auto issue = [&](int s, uint32_t st) {
+    const int64_t off = static_cast<int64_t>(s) * 32;
+    if (all_cols && kb + off + 32 <= ke) {  // whole tile in range (all but the CTA's last k-step)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cp_async16(st + pdst + u * (8 * kImColPitch), pa + off + u * pstride, 16);
+    } else {
+      const int64_t rem = ke - (kb + off + 2 * pcc);  // rows left in this thread's chunk column
+      const int full = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int bytes = ((pvalid >> u) & 1u) ? full : 0;
+        cp_async16(st + pdst + u * (8 * kImColPitch), bytes ? pa + off + u * pstride : A, bytes);
+      }
+    }
+    if (tid < 32 * MT) cp_async16(st + podst, po + off, 16);
+  };
+
+  for (int e = tid; e < kImWarps * 16 * MT * 8; e += kImThreads) yacc[e] = 0.0;
+  __syncthreads();
+  int acc[NS][MT][4];
+#pragma unroll
+  for (int t = 0; t < NS; ++t)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[t][mt][v] = 0;
+  int ecol = 0;  // running exponent of this thread's B column (g); 0 = nothing seen yet
+  uint32_t hlim = 1u << 20;  // values with exponent field > ecol have |hi word| >= hlim
+  double asq4[4] = {0.0, 0.0, 0.0, 0.0};
+  // 2^(1076 - E): fone when representable, else fa * fb (E = 1 until the first nonzero exponent:
+  // columns of subnormals still convert exactly)
+  double fa = pow2i((kSh - 1) / 2), fb = pow2i(kSh - 1 - (kSh - 1) / 2), fone = 1.0;
+  bool two_step = true;
+  double* yw = yacc + warp * (16 * MT * 8);  // [col 0..7][row 0..16*MT)
+
+  // fold the int32 slices into the fp64 accumulators: C columns 2q, 2q+1 use their column's E
+  auto flush = [&](int e_old) {
+    const int e0 = max(__shfl_sync(0xffffffffu, e_old, (2 * q) * 4), 1);
+    const int e1 = max(__shfl_sync(0xffffffffu, e_old, (2 * q + 1) * 4), 1);
+    const int sh0 = e0 - kSh, sh1 = e1 - kSh;  // <= 970
+    const double f0a = pow2i(sh0 / 2), f0b = pow2i(sh0 - sh0 / 2), f1a = pow2i(sh1 / 2), f1b = pow2i(sh1 - sh1 / 2);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        double s = static_cast<double>(acc[NS - 1][mt][v]);
+#pragma unroll
+        for (int t = NS - 2; t >= 0; --t) s = fma(s, 256.0, static_cast<double>(acc[t][mt][v]));
+        const bool c1 = v & 1;
+        s = s * (c1 ? f1a : f0a) * (c1 ? f1b : f0b);
+        const int row = mt * 16 + g + 8 * (v >> 1), col = 2 * q + (v & 1);
+        yw[col * (16 * MT) + row] += s;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) acc[t][mt][v] = 0;
+      }
+  };
+
+  uint32_t st_issue = 0, st_cur = 0;  // ring slots (byte offsets) of the next issue / the current k-step
+#pragma unroll
+  for (int s = 0; s < Cfg::kStages - 1; ++s) {
+    if (s < nsteps) issue(s, sbase + st_issue);
+    cp_async_commit();
+    st_issue += Cfg::kStage;
+  }
+  // Software pipeline: the slices of k-step s+1 are formed while the MMAs of k-step s run (the
+  // two instruction streams are independent unless a column's exponent grows, in which case the
+  // MMAs of s complete, the accumulators are folded, then s+1 is converted with the new scale).
+  auto load_x = [&](uint32_t slot, double (&x)[8]) {
+    const double* colp = reinterpret_cast<const double*>(ims + slot + (8 * warp + g) * kImColPitch);
+    const double2 p0 = *reinterpret_cast<const double2*>(colp + 4 * q);
+    const double2 p1 = *reinterpret_cast<const double2*>(colp + 4 * q + 2);
+    const double2 p2 = *reinterpret_cast<const double2*>(colp + 16 + 4 * q);
+    const double2 p3 = *reinterpret_cast<const double2*>(colp + 16 + 4 * q + 2);
+    x[0] = p0.x; x[1] = p0.y; x[2] = p1.x; x[3] = p1.y; x[4] = p2.x; x[5] = p2.y; x[6] = p3.x; x[7] = p3.y;
+    // ||A||^2 and this thread's largest |hi word| (monotone in |x|); the column-wide exponent is
+    // only formed (shuffles) on the rare path where some value reaches the current scale's limit
+    uint32_t hmax = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      asq4[u & 3] = fma(x[u], x[u], asq4[u & 3]);
+      hmax = max(hmax, static_cast<uint32_t>(__double2hiint(x[u])) & 0x7fffffffu);
+    }
+    return hmax;
+  };
+  auto column_emax = [&](uint32_t hmax) {
+    int emax = static_cast<int>(hmax >> 20);
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, 1));
+    return max(emax, __shfl_xor_sync(0xffffffffu, emax, 2));
+  };
+  auto rescale = [&](int emax) {
+    ecol = max(ecol, emax + 1 < 2046 ? emax + 1 : emax);  // one bit of headroom: fewer flushes
+    hlim = static_cast<uint32_t>(ecol + 1) << 20;          // |hi word| >= hlim <=> exponent > ecol
+    const int sh = kSh - max(ecol, 1);
+    fa = pow2i(sh / 2);
+    fb = pow2i(sh - sh / 2);
+    fone = pow2i(sh < 1023 ? sh : 0);
+    two_step = __any_sync(0xffffffffu, sh >= 1023);
+  };
+  // w = rint(x * 2^(kSh - E)) (columns below 2^-969 scale in two exact steps); slices = its bytes
+  auto convert = [&](const double (&x)[8], uint32_t (&b0)[kImSlices], uint32_t (&b1)[kImSlices]) {
+    uint32_t lo[8], hi[8];
+    if (!two_step) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long w = __double2ll_rn(x[u] * fone);
+        lo[u] = static_cast<uint32_t>(w);
+        hi[u] = static_cast<uint32_t>(static_cast<unsigned long long>(w) >> 32);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long w = __double2ll_rn((x[u] * fa) * fb);
+        lo[u] = static_cast<uint32_t>(w);
+        hi[u] = static_cast<uint32_t>(static_cast<unsigned long long>(w) >> 32);
+      }
+    }
+    byte_transpose(lo[0], lo[1], lo[2], lo[3], hi[0], hi[1], hi[2], hi[3], b0);
+    byte_transpose(lo[4], lo[5], lo[6], lo[7], hi[4], hi[5], hi[6], hi[7], b1);
+  };
+  // operator fragments (ldmatrix.x4 of 16 rows x 32 bytes per m-tile) x slices
+  auto mma_step = [&](uint32_t slot, const uint32_t (&b0)[kImSlices], const uint32_t (&b1)[kImSlices]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      uint32_t af[4];
+      const int r = mt * 16 + (lane & 15);
+      const uint32_t addr = sbase + slot + Cfg::kAStage + r * kImOmPitch + (lane >> 4) * 16;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                   : "r"(addr));
+#pragma unroll
+      for (int t = 0; t < NS - 1; ++t) imma_16x8x32<false>(acc[t][mt], af, b0[t], b1[t]);
+      imma_16x8x32<true>(acc[NS - 1][mt], af, b0[NS - 1], b1[NS - 1]);
+    }
+  };
+  auto next_slot = [&](uint32_t v) { return v + Cfg::kStage == Cfg::kStages * Cfg::kStage ? 0u : v + Cfg::kStage; };
+
+  uint32_t bc0[kImSlices], bc1[kImSlices];  // slices of the current k-step
+  if (nsteps > 0) {
+    cp_async_wait<Cfg::kStages - 2>();
+    __syncthreads();
+    double x[8];
+    const uint32_t hmax = load_x(st_cur, x);
+    if (__any_sync(0xffffffffu, hmax >= hlim)) rescale(column_emax(hmax));  // nothing accumulated yet
+    convert(x, bc0, bc1);
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    cp_async_wait<Cfg::kStages - 3>();  // k-step s + 1 has landed
+    __syncthreads();                 // and every warp is done with k-step s - 1's slot
+    if (s + Cfg::kStages - 1 < nsteps) issue(s + Cfg::kStages - 1, sbase + st_issue);
+    cp_async_commit();
+    st_issue = next_slot(st_issue);
+    const uint32_t cur = st_cur;
+    st_cur = next_slot(st_cur);
+    if (s + 1 < nsteps) {
+      double x[8];
+      const uint32_t hmax = load_x(st_cur, x);
+      uint32_t bn0[kImSlices], bn1[kImSlices];
+      if (!__any_sync(0xffffffffu, hmax >= hlim)) {
+        convert(x, bn0, bn1);  // independent of the MMAs below: the scheduler interleaves them
+        mma_step(cur, bc0, bc1);
+      } else {
+        mma_step(cur, bc0, bc1);
+        const int emax = column_emax(hmax);
+        flush(ecol);
+        rescale(emax);
+        convert(x, bn0, bn1);
+      }
+#pragma unroll
+      for (int t = 0; t < kImSlices; ++t) {
+        bc0[t] = bn0[t];
+        bc1[t] = bn1[t];
+      }
+    } else {
+      mma_step(cur, bc0, bc1);
+    }
+  }
+  cp_async_wait<0>();
+  flush(ecol);
+  __syncwarp();
+  // write this split's partial: Y(h, j) at part[split][j * c_pad + h]
+  double* out = part + static_cast<int64_t>(blockIdx.y) * split_stride;
+  for (int e = lane; e < 8 * 16 * MT; e += 32) {
+    const int col = e / (16 * MT), row = e - col * (16 * MT);
+    const int64_t j = j0 + 8 * warp + col;
+    if (j < n && row < c_pad) out[j * c_pad + row] = yw[e];
+  }
+  const double bs = block_sum<kImThreads>((asq4[0] + asq4[1]) + (asq4[2] + asq4[3]), red);
+  if (tid == 0) asq_part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
+}
+
+bool sparse_sketch_imma_supported(const double* A, int64_t lda, int64_t c_pad) {
+  return c_pad <= 64 && (lda % 2) == 0 && (reinterpret_cast<uintptr_t>(A) % 16) == 0;
+}
+
+struct ImPlan {
+  int64_t col_tiles, splits, kps, ld8, mt;
+};
+static ImPlan plan_imma(int64_t m, int64_t n, int64_t c_pad) {
+  ImPlan p{};
+  p.mt = (c_pad + 15) / 16;
+  p.col_tiles = ceil_div(n, kImCols);
+  const int64_t steps = ceil_div(m, 32);
+  // enough CTAs for 2 per SM x a few waves; at least 64 k-steps per split; <= 2^17 k-steps per
+  // split keeps every int32 slice sum exact (|acc| <= 32 * 255 per k-step)
+  const int64_t want = 148 * 2 * 4;
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, p.col_tiles), steps / 64));
+  splits = std::max<int64_t>(splits, ceil_div(steps, int64_t(1) << 17));
+  p.kps = ceil_div(steps, splits);
+  p.splits = ceil_div(steps, p.kps);
+  p.ld8 = round_up(std::max<int64_t>(m, 1) + 32, 32);  // one k-step of zero padding past m
+  return p;
+}
+
+int64_t sparse_sketch_imma_workspace_elems(int64_t m, int64_t n, int64_t c_pad) {
+  const ImPlan p = plan_imma(m, n, c_pad);
+  const int64_t part = p.splits > 1 ? p.splits * n * c_pad : 0;
+  const int64_t om = ceil_div(16 * p.mt * p.ld8, 8);
+  return part + p.col_tiles * p.splits + om + 4096 + 8;
+}
+
+cudaError_t run_sketch_apply_sparse_imma(const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed, int64_t c,
+                                         int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
+                                         const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info,
+                                         bool operator_ready, bool kernel_only) {
+  if (!sparse_sketch_imma_supported(A, lda, c_pad)) return cudaErrorInvalidValue;
+  const ImPlan p = plan_imma(m, n, c_pad);
+  if (sparse_sketch_imma_workspace_elems(m, n, c_pad) > ws_elems) return cudaErrorInvalidValue;
+  const int64_t part_elems = p.splits > 1 ? p.splits * n * c_pad : 0;
+  double* part = ws;
+  double* asq_part = ws + part_elems;
+  int8_t* O = reinterpret_cast<int8_t*>(round_up(reinterpret_cast<uintptr_t>(asq_part + p.col_tiles * p.splits), 64));
+  double* ysq_part = reinterpret_cast<double*>(O + 16 * p.mt * p.ld8);
+  ysq_part = reinterpret_cast<double*>(round_up(reinterpret_cast<uintptr_t>(ysq_part), 16));
+  cudaError_t e;
+  if (!operator_ready) {
+    e = cudaMemsetAsync(O, 0, static_cast<size_t>(16 * p.mt * p.ld8), st);
+    if (e != cudaSuccess) return e;
+    const int ze = static_cast<int>(std::min<int64_t>(zeta, c));
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 148 * 16));
+    gen_sparse_sign_i8_kernel<<<blocks, 256, 0, st>>>(O, p.ld8, c, m, seed, ze);
+  }
+  auto launch = [&](auto kern, int smem) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    dim3 grid(static_cast<unsigned>(p.col_tiles), static_cast<unsigned>(p.splits));
+    kern<<<grid, kImThreads, smem, st>>>(A, m, n, lda, O, p.ld8, p.kps, c_pad, p.splits > 1 ? part : Y, n * c_pad,
+                                         asq_part);
+    return cudaGetLastError();
+  };
+  const int ns_env = getenv("ITERCUR_IMMA_SLICES") ? atoi(getenv("ITERCUR_IMMA_SLICES")) : 0;  // A/B
+  const int ns = ns_env == 6 || ns_env == 7 ? ns_env : (p.mt <= 2 ? 7 : 6);
+  switch (p.mt * 10 + ns) {
+    case 17: e = launch(sparse_sketch_imma_kernel<1, 7>, ImCfg<1>::kSmem); break;
+    case 16: e = launch(sparse_sketch_imma_kernel<1, 6>, ImCfg<1>::kSmem); break;
+    case 27: e = launch(sparse_sketch_imma_kernel<2, 7>, ImCfg<2>::kSmem); break;
+    case 26: e = launch(sparse_sketch_imma_kernel<2, 6>, ImCfg<2>::kSmem); break;
+    case 37: e = launch(sparse_sketch_imma_kernel<3, 7>, ImCfg<3>::kSmem); break;
+    case 36: e = launch(sparse_sketch_imma_kernel<3, 6>, ImCfg<3>::kSmem); break;
+    case 47: e = launch(sparse_sketch_imma_kernel<4, 7>, ImCfg<4>::kSmem); break;
+    default: e = launch(sparse_sketch_imma_kernel<4, 6>, ImCfg<4>::kSmem); break;
+  }
+  if (e != cudaSuccess) return e;
+  if (info) {
+    info->splits = static_cast<int>(p.splits);
+    info->ctas = static_cast<int>(p.col_tiles * p.splits);
+    info->nt = static_cast<int>(p.mt);
+    info->tma = false;
+    info->dominant_launches = 1;
+  }
+  if (kernel_only) return cudaGetLastError();
+  const int64_t total = n * c_pad;
+  const int rblocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 2048));
+  sketch_reduce_kernel<<<rblocks, 256, 0, st>>>(p.splits > 1 ? part : Y, p.splits > 1 ? static_cast<int>(p.splits) : 1,
+                                                n * c_pad, scale, Y, total, ysq_part);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(ysq_part, rblocks, stats.d_ysq);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(asq_part, static_cast<int>(p.col_tiles * p.splits), stats.d_asq);
+  return cudaGetLastError();
+}
+
 }  // namespace itercur_b200

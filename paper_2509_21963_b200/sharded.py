@@ -114,6 +114,10 @@ class DeviceBackend:
                                             C.c_void_p(out.data_ptr()), _ld(out), self._st()))
         return out
 
+    def select_columns(self, Y, b, pivot_floor, exclude):
+        from .stages import select_columns
+        return select_columns(Y, b, pivot_floor=pivot_floor, exclude=exclude).indices
+
     def select_rows(self, S, b, pivot_floor, exclude):
         from .stages import select_rows
         sel = select_rows(S, b, pivot_floor=pivot_floor, exclude=exclude)
@@ -183,12 +187,71 @@ class _Comm:
         return out
 
 
+def _gather_columns(comm, y, widths):
+    """Y_full = [Y_0 | Y_1 | ...] (c_pad x n, column-major) from every rank's c_pad x n_r block:
+    one all_gather of equal-size (padded) flat buffers."""
+    cp = y.shape[0]
+    if comm.world == 1:
+        return y
+    maxn = max(widths)
+    buf = torch.zeros(maxn * cp, dtype=y.dtype, device=y.device)
+    n_r = y.shape[1]
+    if n_r:
+        buf[:n_r * cp].view(n_r, cp).copy_(y.t())
+    g = comm.all_gather(buf)                                  # world x (maxn * cp)
+    parts = [g[q, :widths[q] * cp] for q in range(comm.world)]
+    return torch.cat(parts).view(sum(widths), cp).t()
+
+
+def _dist_column_lupp(be, comm, y, col_live, steps, ynorm, pivot_floor, col_offset, n_r, col_steps):
+    """Distributed LUPP on W = Y^T (select.cpp:34-74, 121-139): every rank eliminates its own rows;
+    one all_gather of the per-rank pivot candidates per step, reduced in rank order (lowest global
+    index on ties)."""
+    dev = y.device
+    W = to_colmajor(y[:steps, :].t())                # n_r x steps
+    live = col_live.clone()
+    cand = torch.zeros(4 + steps, dtype=torch.float64, device=dev)
+    abs_floor = 1e2 * _EPS * ynorm
+    cols, P, piv_local, first = [], None, -1, 0.0
+    for s in range(steps):
+        if n_r:
+            be.lupp_step(W, live, steps, s, P, piv_local, col_offset, cand)
+        else:
+            cand.zero_()
+            cand[0] = -1.0
+        g = comm.all_gather(cand)                     # world x (4 + steps)
+        mags = g[:, 0]
+        wr = int(torch.argmax(mags).item())           # first maximum in rank order
+        best = float(mags[wr])
+        if best < 0.0 or best <= abs_floor:
+            break
+        if s == 0:
+            first = best
+        elif best < pivot_floor * first:
+            break
+        others = torch.cat([mags[:wr], mags[wr + 1:]])
+        second = max(float(g[wr, 1]), float(others.max()) if others.numel() else -1.0)
+        idx = int(g[wr, 2])
+        cols.append(idx)
+        col_steps.append((idx, best, second))
+        P = g[wr, 4:].contiguous()
+        piv_local = idx - col_offset if wr == comm.rank else -1
+    return cols
+
+
 def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, *, epsilon=1e-6, b=50, delta=0.0,
                           alpha=0.05, risk_adjust=False, max_rank=0, max_iters=0, pivot_floor=1e-13, seed=0,
-                          sketch="gaussian", sparse_nnz=8, group=None, backend=None) -> ShardedResult:
+                          sketch="gaussian", sparse_nnz=8, group=None, backend=None,
+                          column_exchange="sketch") -> ShardedResult:
     """IterativeCUR of A = [A_0 | A_1 | ...] with this rank's block `a_shard` = A(:, col_offset :
     col_offset + n_r) (column-major, on this rank's device). Collective: every rank of `group`
-    calls it with its own shard; all ranks return the same indices and trace."""
+    calls it with its own shard; all ranks return the same indices and trace.
+
+    column_exchange: "sketch" (default) replicates the c_pad x n sketch once per iteration and
+    runs the column LUPP whole on every rank (2 collectives per iteration); "candidates" runs
+    the distributed LUPP (one all_gather of pivot candidates per pivot step)."""
+    if column_exchange not in ("sketch", "candidates"):
+        raise ValueError(f"unknown column_exchange '{column_exchange}'")
     comm = _Comm(group)
     dev = a_shard.device
     be = backend if backend is not None else DeviceBackend(dev)
@@ -242,6 +305,8 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
         return ShardedResult([], [], "Converged", rho, threshold, [],
                              "threshold at or above the initial estimate; empty factorization", [], comm.count)
 
+    widths = [sh[2] for sh in shapes]
+    yfull = _gather_columns(comm, y, widths) if column_exchange == "sketch" else None
     cap = max_rank_eff + b
     L = colmajor_empty(m, cap, dev, fill=0.0)             # residual columns, replicated
     Rt = colmajor_empty(cap, n_r, dev, fill=0.0)          # rows of R~ for this shard
@@ -254,54 +319,40 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
             status = "MaxRank"
             break
         block = min(b, max_rank_eff - r)
-        # ---- column selection: distributed LUPP on W = Y^T (select.cpp:121-139) ----
+        # ---- column selection (select.cpp:121-139) ----
         steps = min(block, c)
-        W = to_colmajor(y[:steps, :].t())                # n_r x steps
-        live = col_live.clone()
-        cand = torch.zeros(4 + steps, dtype=torch.float64, device=dev)
-        abs_floor = 1e2 * _EPS * ynorm
-        cols, P, piv_local, first = [], None, -1, 0.0
-        for s in range(steps):
-            if n_r:
-                be.lupp_step(W, live, steps, s, P, piv_local, col_offset, cand)
-            else:
-                cand.zero_()
-                cand[0] = -1.0
-            g = comm.all_gather(cand)                     # world x (4 + steps)
-            mags = g[:, 0]
-            wr = int(torch.argmax(mags).item())           # first maximum in rank order
-            best = float(mags[wr])
-            if best < 0.0 or best <= abs_floor:
-                break
-            if s == 0:
-                first = best
-            elif best < pivot_floor * first:
-                break
-            others = torch.cat([mags[:wr], mags[wr + 1:]])
-            second = max(float(g[wr, 1]), float(others.max()) if others.numel() else -1.0)
-            idx = int(g[wr, 2])
-            cols.append(idx)
-            col_steps.append((idx, best, second))
-            P = g[wr, 4:].contiguous()
-            piv_local = idx - col_offset if wr == comm.rank else -1
+        if column_exchange == "sketch":
+            # Y is replicated once per iteration (one all_gather of c_pad x n_r per rank); every
+            # rank then runs the single-device LUPP on the whole Y^T: same pivots on every rank,
+            # no per-step exchange.
+            sel = be.select_columns(yfull[:c, :], steps, pivot_floor, J)
+            cols = list(sel)[:steps]
+        else:
+            cols = _dist_column_lupp(be, comm, y, col_live, steps, ynorm, pivot_floor, col_offset, n_r, col_steps)
         if not cols:
             status = "ResidualExhausted"
             break
         w_cols = len(cols)
         own = [(q, j - col_offset) for q, j in enumerate(cols) if col_offset <= j < col_offset + n_r]
-        # ---- A(:,J_k), R~(:,J_k), Y(:,J_k) from their owners (disjoint sums) ----
-        Acols = colmajor_empty(m, w_cols, dev, fill=0.0)
-        Rcols = colmajor_empty(max(r, 1), w_cols, dev, fill=0.0)
-        Ycols = colmajor_empty(y.shape[0], w_cols, dev, fill=0.0)
+        # ---- A(:,J_k), R~(:,J_k) (and Y(:,J_k) unless Y is replicated) from their owners: one all_reduce
+        # of disjoint contributions (exact) ----
+        yrows = y.shape[0] if column_exchange != "sketch" else 0
+        pack = torch.zeros(w_cols, _even(m + r + yrows), dtype=torch.float64, device=dev)  # column q = [A; R~; Y](:, J_q)
         for q, jl in own:
-            Acols[:, q] = a[:, jl]
+            pack[q, :m] = a[:, jl]
             if r:
-                Rcols[:r, q] = Rt[:r, jl]
-            Ycols[:, q] = y[:, jl]
-        comm.all_reduce(Acols)
-        if r:
-            comm.all_reduce(Rcols)
-        comm.all_reduce(Ycols)
+                pack[q, m:m + r] = Rt[:r, jl]
+            if yrows:
+                pack[q, m + r:m + r + yrows] = y[:, jl]
+        comm.all_reduce(pack)
+        packT = pack.t()                                  # (m + r + yrows) x w, column-major view
+        Acols = packT[:m, :]
+        Rcols = to_colmajor(packT[m:m + r, :]) if r else colmajor_empty(1, w_cols, dev, fill=0.0)
+        if yrows:
+            Ycols = to_colmajor(packT[m + r:m + r + yrows, :])
+        else:
+            Jk_t = torch.tensor(cols, dtype=torch.int64, device=dev)
+            Ycols = yfull[:, Jk_t]
         # ---- row residual S_row = A(:,J_k) - L R~(:,J_k) (replicated; sketch.cpp:43-60) ----
         S = colmajor_empty(m, w_cols, dev)
         be.gemm(L[:, :r], Rcols[:r, :], Acols, -1.0, S)
@@ -331,14 +382,16 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
             Ynew = colmajor_empty(n_r, y.shape[0], dev)
             be.gemm(Rk, to_colmajor(Ycols[:, :width].t()), Yt, -1.0, Ynew)
             y = to_colmajor(Ynew.t())
-            ysq_r = float((y.double() ** 2).sum().item())
-        else:
-            ysq_r = 0.0
         for q, jl in own:
             if q < width:
                 col_live[jl] = 0
-        ysq_t = comm.all_reduce(torch.tensor([ysq_r], dtype=torch.float64, device=dev))
-        ynorm = math.sqrt(float(ysq_t[0]))
+        if column_exchange == "sketch":
+            yfull = _gather_columns(comm, y, widths)
+            ysq_all = float(torch.sum(yfull[:c, :] * yfull[:c, :]).item())
+        else:
+            ysq_r = float((y.double() ** 2).sum().item()) if n_r else 0.0
+            ysq_all = float(comm.all_reduce(torch.tensor([ysq_r], dtype=torch.float64, device=dev))[0])
+        ynorm = math.sqrt(ysq_all)
         rho = ynorm / ga_norm if ga_norm > 0 else 0.0
         I += Ik
         J += Jk

@@ -57,6 +57,10 @@ class CpuBackend:
         out.copy_((base if base is not None else 0.0) + alpha * prod)
         return out
 
+    def select_columns(self, Y, b, pivot_floor, exclude):
+        return oracle.select_columns(np.asfortranarray(Y.numpy()), b, pivot_floor=pivot_floor,
+                                     exclude=exclude).indices
+
     def select_rows(self, S, b, pivot_floor, exclude):
         return oracle.select_rows(np.asfortranarray(S.numpy()), b, pivot_floor=pivot_floor, exclude=exclude).indices
 

@@ -68,14 +68,15 @@ def test_gemm_block_lu_and_solves():
 
 @pytest.mark.parametrize("kw", [dict(epsilon=1e-8, b=5, seed=2), dict(epsilon=1e-6, b=8, seed=1, sketch="sparse_sign"),
                                 dict(epsilon=0.0, b=4, seed=3, max_rank=10)])
-def test_world_one_on_the_gpu_matches_oracle(oracle, kw):
+@pytest.mark.parametrize("exchange", ["sketch", "candidates"])
+def test_world_one_on_the_gpu_matches_oracle(oracle, kw, exchange):
     from paper_2509_21963_b200.sharded import iterative_cur_sharded, true_relative_error_sharded
     a = oracle.random_gaussian(300, 20, 5) @ oracle.random_gaussian(240, 20, 6).T
     a = a + 1e-9 * np.linalg.norm(a) / 300.0 * oracle.random_gaussian(300, 240, 7)
     o = oracle.iterative_cur(a, **kw)
     t = torch.from_numpy(np.asfortranarray(a)).cuda()
     t = t.t().contiguous().t()
-    res = iterative_cur_sharded(t, 0, a.shape[1], **kw)
+    res = iterative_cur_sharded(t, 0, a.shape[1], column_exchange=exchange, **kw)
     assert res.status == o.status
     assert res.row_indices == list(o.row_indices) and res.col_indices == list(o.col_indices)
     err = true_relative_error_sharded(t, 0, res)

@@ -43,7 +43,7 @@ def _cases(oracle):
     }
 
 
-def _worker(rank, world, port, case, out_q):
+def _worker(rank, world, port, case, out_q, exchange="sketch"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -53,18 +53,18 @@ def _worker(rank, world, port, case, out_q):
         bounds = [round(q * n / world) for q in range(world + 1)]
         lo, hi = bounds[rank], bounds[rank + 1]
         shard = torch.from_numpy(np.asfortranarray(a[:, lo:hi]))
-        res = iterative_cur_sharded(shard, lo, n, backend=CpuBackend(), **kw)
+        res = iterative_cur_sharded(shard, lo, n, backend=CpuBackend(), column_exchange=exchange, **kw)
         err = true_relative_error_sharded(shard, lo, res)
         out_q.put((rank, res.row_indices, res.col_indices, res.status, res.final_rho, err, res.exchanges))
     finally:
         dist.destroy_process_group()
 
 
-def _run(case, world):
+def _run(case, world, exchange="sketch"):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -74,11 +74,12 @@ def _run(case, world):
     return outs
 
 
+@pytest.mark.parametrize("exchange", ["sketch", "candidates"])
 @pytest.mark.parametrize("case", ["lowrank_noise", "expdecay_sparse_sign", "fixed_rank"])
-def test_two_ranks_match_single_process_oracle(oracle, case):
+def test_two_ranks_match_single_process_oracle(oracle, case, exchange):
     a, kw = _cases(oracle)[case]
     o = oracle.iterative_cur(a, **kw)
-    outs = _run(case, 2)
+    outs = _run(case, 2, exchange)
     # every rank returns the same selection
     assert outs[0][1:5] == outs[1][1:5]
     _, I, J, status, rho, err, exchanges = outs[0]
