@@ -91,7 +91,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kernel_substr, profile="profiles/ncu_full_r01_cfg2_v4.txt"):
+NCU_FULL = "profiles/ncu_full_r01_cfg2_v5.txt"  # the committed `ncu --set full` summary of this config
+
+
+def sketch_kernel_name(sketch, c):
+    """The sketch-apply kernel the engine runs for this sketch kind (csrc/engine.cu sparse_sketch_mode)."""
+    if sketch != "sparse_sign":
+        return "sketch_dmma_kernel"
+    c_pad = ((c + 7) // 8) * 8
+    mode = os.environ.get("ITERCUR_SPARSE_SKETCH", "") or ("3" if c_pad > 32 else "2")
+    return {"0": "sketch_dmma_kernel", "1": "sparse_sketch_kernel", "3": "sparse_sketch_umma_kernel"}.get(
+        mode, "sparse_sketch_imma_kernel")
+
+
+def ncu_traffic(kernel_substr, profile=NCU_FULL):
     """DRAM bytes (read + write) per launch of a kernel from the committed `ncu --set full`
     summary (tools/summarize_ncu.py), or None when no capture is on file."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), profile)
@@ -396,9 +409,10 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": bytes_alg / t_k / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": hbm_src}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": ncu_traffic("sketch_dmma_kernel"),
-                 "traffic_source": "profiles/ncu_full_r01_cfg2_v4.txt (dram__bytes_read + dram__bytes_write, one launch)",
-                 "kernel": "sketch_dmma_kernel",
+    kname = sketch_kernel_name(cfg["sketch"], c)
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": ncu_traffic(kname),
+                 "traffic_source": f"{NCU_FULL} (dram__bytes_read + dram__bytes_write, one launch)",
+                 "kernel": kname,
                  "ms_per_launch": sk["ms"], "ctas": sk["ctas"], "splits": sk["splits"], "tma": sk["tma"],
                  "algorithmic_bytes": bytes_alg, "algorithmic_flops": flops_alg})
 

@@ -259,22 +259,26 @@ double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cud
 }
 
 // ---- the sketch apply (make_sketch, sketch.cpp:10-24), shared by the run and the stage entries.
-// Sparse-sign operator, three kernels (ITERCUR_SPARSE_SKETCH selects; default: the integer path):
-//   2  sliced-integer tensor path (sketch.cu sparse_sketch_imma_kernel): A as 7 int8 slices of a
-//      56-bit fixed-point form x the int8 +-1 operator on mma.sync s8 — HBM-bound at c_pad <= 64;
-//   0  FP64 DMMA contraction over the materialised +-1 operator (FP64-bound once c_pad > ~24);
+// Sparse-sign operator, four kernels (ITERCUR_SPARSE_SKETCH selects; default: 3 when c_pad > 32,
+// else 2 — the faster one at each shape on B200, tools/sketch_modes.py):
+//   3  tcgen05 kind::i8 (sketch.cu sparse_sketch_umma_kernel): A as int8 slices of a per-column
+//      fixed-point form, written by the converter warps straight into TMEM as the MMA's A operand,
+//      int32 accumulators in TMEM, TMA-staged A tiles, persistent CTAs: 83-88% of HBM at c = 55;
+//   2  the same contraction on mma.sync s8 (register accumulators): 82% of HBM at c_pad = 24;
+//   0  FP64 DMMA over the materialised +-1 operator (FP64-bound once c_pad > ~24: 37% at c = 55);
 //   1  the sparse list walk (bitwise equal to the oracle's sparse loop; bound by shared-memory
 //      reads of every (row, target) pair: 3.9 ms vs DMMA 2.7 ms at 40000 x 20000, c = 55).
 struct SketchBuffers {
   DevBuf<double> S, ws;
 };
-enum SparseMode { kSparseDense = 0, kSparseList = 1, kSparseImma = 2 };
+enum SparseMode { kSparseDense = 0, kSparseList = 1, kSparseImma = 2, kSparseUmma = 3 };
 static int sparse_sketch_mode(int kind, int64_t c, int64_t cp, int zeta_eff, const double* A, int64_t lda) {
   if (kind != kSketchSparseSign) return kSparseDense;
   const char* e = getenv("ITERCUR_SPARSE_SKETCH");
-  const int want = (e && e[0]) ? atoi(e) : kSparseImma;
+  const int want = (e && e[0]) ? atoi(e) : (cp > 32 ? kSparseUmma : kSparseImma);
   if (want == kSparseList && sparse_sketch_supported(c, zeta_eff)) return kSparseList;
-  if (want == kSparseImma && sparse_sketch_imma_supported(A, lda, cp)) return kSparseImma;
+  if (want == kSparseUmma && sparse_sketch_umma_supported(A, 0, 0, lda, cp)) return kSparseUmma;
+  if ((want == kSparseImma || want == kSparseUmma) && sparse_sketch_imma_supported(A, lda, cp)) return kSparseImma;
   return kSparseDense;
 }
 static int zeta_effective(int kind, int sparse_nnz, int64_t c) {
@@ -294,6 +298,12 @@ static int apply_sketch(const double* A, int64_t m, int64_t n, int64_t lda, int 
     if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
     CK(run_sketch_apply_sparse(A, m, n, lda, seed, c, cp, ze, scale, Y, buf.ws.p, wse, stats, st, info));
     return 4;
+  }
+  if (mode == kSparseUmma) {
+    const int64_t wse = sparse_sketch_umma_workspace_elems(m, n, cp);
+    if (buf.ws.count < static_cast<size_t>(wse)) buf.ws.alloc(wse);
+    CK(run_sketch_apply_sparse_umma(A, m, n, lda, seed, c, cp, ze, scale, Y, buf.ws.p, wse, stats, st, info, false));
+    return 6;
   }
   if (mode == kSparseImma) {
     // the int8 operator lives in the workspace; it is regenerated per call (m threads)
@@ -1657,7 +1667,12 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     const int smode = sparse_sketch_mode(k, c, cp, zeta_effective(k, 8, c), dA, lda);
     const bool sparse = smode == kSparseList;
     SketchBuffers sb;
-    if (smode == kSparseImma) {
+    if (smode == kSparseUmma) {
+      wsb.alloc(sparse_sketch_umma_workspace_elems(m, n, cp));
+      CK(run_sketch_apply_sparse_umma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
+                                      static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
+                                      false, false));
+    } else if (smode == kSparseImma) {
       wsb.alloc(sparse_sketch_imma_workspace_elems(m, n, cp));
       CK(run_sketch_apply_sparse_imma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
                                       static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
@@ -1671,7 +1686,11 @@ int itercur_time_sketch_kernel(const double* dA, int64_t m, int64_t n, int64_t l
     // the sparse path is timed whole (operator lists + apply + norm reductions); the dense
     // path times its DMMA kernel alone
     auto once = [&]() {
-      if (smode == kSparseImma)  // the integer-path kernel alone (operator already generated)
+      if (smode == kSparseUmma)
+        CK(run_sketch_apply_sparse_umma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
+                                        static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
+                                        true, true));
+      else if (smode == kSparseImma)  // the integer-path kernel alone (operator already generated)
         CK(run_sketch_apply_sparse_imma(dA, m, n, lda, 0, c, cp, zeta_effective(k, 8, c), 1.0, Y.p, wsb.p,
                                         static_cast<int64_t>(wsb.count), SketchStats{scal.p, scal.p + 1}, st, &info,
                                         true, true));

@@ -104,6 +104,13 @@ cudaError_t run_sketch_apply_sparse_imma(const double* A, int64_t m, int64_t n, 
                                          int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
                                          const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info,
                                          bool operator_ready, bool kernel_only = false);
+// The same on tcgen05 (kind::i8, TMEM accumulators; TMA-staged A tiles): c_pad <= 64.
+bool sparse_sketch_umma_supported(const double* A, int64_t m, int64_t n, int64_t lda, int64_t c_pad);
+int64_t sparse_sketch_umma_workspace_elems(int64_t m, int64_t n, int64_t c_pad);
+cudaError_t run_sketch_apply_sparse_umma(const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed, int64_t c,
+                                         int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
+                                         const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info,
+                                         bool operator_ready, bool kernel_only = false);
 // Stand-alone timing hook: the DMMA kernel only (for roofline measurement).
 cudaError_t run_sketch_dmma_only(const double* A, int64_t m, int64_t n, int64_t lda, const double* S, int64_t ldg,
                                  int64_t c_pad, double* Y, double* workspace, int64_t workspace_elems, cudaStream_t st,

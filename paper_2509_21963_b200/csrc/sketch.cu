@@ -1101,4 +1101,464 @@ cudaError_t run_sketch_apply_sparse_imma(const double* A, int64_t m, int64_t n, 
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ sparse-sign sketch, tcgen05 form
+// The same sliced-integer contraction as sparse_sketch_imma_kernel, on the 5th-generation tensor
+// cores: tcgen05.mma kind::i8 with the int32 slice accumulators in TMEM instead of registers.
+//   D (128 columns of A x NPAD sketch rows, s32, TMEM) += slices_t (128 x 32 rows, u8/s8, smem)
+//                                                        x Omega^T (32 rows x NPAD, s8, smem)
+// for t = 0..NS-1 into TMEM columns [t*NPAD, (t+1)*NPAD). Warp roles (192 threads):
+//   warps 0-3  conversion: thread = one column of the CTA's 128; reads its 32 doubles of the
+//              k-step from the TMA tile (two 16-row boxes, 128-B swizzle), forms
+//              w = rint(x * 2^(kSh - E)) against its column's running exponent E, writes the NS
+//              byte slices in the canonical K-major no-swizzle layout (8-row x 16-byte core
+//              matrices), and when its column's exponent grows folds its TMEM lane into FP64
+//              registers (tcgen05.ld), zeroes it (tcgen05.st) and rescales — per warp, no
+//              CTA-wide coupling;
+//   warp 4     producer: TMA of the A tile (2 boxes) + bulk copy of the k-step's operator block;
+//   warp 5     one thread issues the NS MMAs per k-step and commits them to mbarriers.
+// Rings: A/operator stages (full: TMA bytes; empty: 128 conversion arrivals + 1 MMA commit) and
+// double-buffered slice tiles (full: 128 arrivals; empty: MMA commit).
+constexpr int kUmThreads = 320;  // 8 converter warps + producer + MMA issuer
+constexpr int kUmCols = 128;               // MMA M: columns of A per CTA (one TMEM lane each)
+constexpr int kUmABytes = kUmCols * 32 * 8;  // 32 KB per k-step (two 16-row TMA boxes)
+
+template <int NPAD>
+struct UmCfg {
+  static constexpr int kNS = NPAD == 32 ? 7 : 6;      // slices (TMEM: NS*NPAD accumulators + 2*NS*8 operand)
+  static constexpr int kOBytes = NPAD * 32;           // operator block per k-step
+  static constexpr int kTmemCols = 512;
+  static constexpr int kStages = 4;                   // A / operator ring
+  static constexpr int kYaccBytes = NPAD * kUmCols * 8;
+  static constexpr int kSmem = kStages * (kUmABytes + kOBytes) + kYaccBytes + 2048 + 256 + 1024;
+  static_assert(kNS * NPAD + 2 * kNS * 8 <= kTmemCols, "TMEM budget");
+};
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  // K-major, no swizzle: core matrices of 8 rows x 16 B (128 B contiguous); the two K halves 128 B
+  // apart (LBO), consecutive 8-row groups 256 B apart (SBO); version 1 (sm_100)
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>(128 >> 4) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ uint32_t umma_idesc_i8(bool a_signed, int n) {
+  // c = s32 (2), a = u8/s8, b = s8 (operator), both K-major, N >> 3, M = 128 >> 4
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc ? 1 : 0));
+}
+// A operand from TMEM (128 lanes x 8 columns: row = lane, bytes k = 4c..4c+3 in column c)
+__device__ __forceinline__ void umma_i8_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc ? 1 : 0));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
+
+template <int NPAD, int NS>
+__global__ void __launch_bounds__(kUmThreads, 1)
+    sparse_sketch_umma_kernel(const __grid_constant__ CUtensorMap tmA, const int8_t* __restrict__ Oblk, int64_t m,
+                              int64_t n, int64_t col_tiles, int64_t items, int64_t kps, int64_t c_pad,
+                              double* __restrict__ part, int64_t split_stride, double* __restrict__ asq_part,
+                              int ablate) {
+  // Persistent: CTA b processes work items b, b + gridDim.x, ... (item = split * col_tiles + column
+  // tile); the rings and their phases run on across items, so the producer prefetches the next
+  // item's tiles while the converters fold the finished one.
+  using Cfg = UmCfg<NPAD>;
+  constexpr int kSh = 1076 - 8 * (7 - NS);
+  extern __shared__ __align__(1024) uint8_t ums[];
+  uint8_t* sA = ums;                                             // Cfg::kStages x 32 KB (1024-aligned)
+  uint8_t* sO = sA + Cfg::kStages * kUmABytes;                      // Cfg::kStages x operator block
+  double* yacc = reinterpret_cast<double*>(sO + Cfg::kStages * Cfg::kOBytes);  // [NPAD][128] FP64 sums
+  uint32_t* hx = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(yacc) + Cfg::kYaccBytes);  // [2][2][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(hx + 512);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* sfull = empty + Cfg::kStages;
+  uint64_t* sempty = sfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+  __shared__ double red[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto item_range = [&](int64_t it, int64_t& j0, int64_t& kb, int& nsteps) {
+    const int64_t ct = it % col_tiles, sp = it / col_tiles;
+    j0 = ct * kUmCols;
+    kb = sp * kps * 32;
+    const int64_t ke = m < kb + kps * 32 ? m : kb + kps * 32;
+    nsteps = static_cast<int>(ke > kb ? (ke - kb + 31) / 32 : 0);
+  };
+
+  if (tid == 0) {
+    for (int q = 0; q < Cfg::kStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 2 * kUmCols + 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&sfull[q], 2 * kUmCols);
+      mbar_init(&sempty[q], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "n"(Cfg::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ---------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      int64_t g = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int64_t j0, kb;
+        int nsteps;
+        item_range(it, j0, kb, nsteps);
+        for (int s = 0; s < nsteps; ++s, ++g) {
+          const int st = static_cast<int>(g % Cfg::kStages);
+          if (g >= Cfg::kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g / Cfg::kStages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], kUmABytes + Cfg::kOBytes);
+          const int32_t r0 = static_cast<int32_t>(kb + 32 * s);
+          tma_load_2d(sA + st * kUmABytes, &tmA, &full[st], r0, static_cast<int32_t>(j0));
+          tma_load_2d(sA + st * kUmABytes + kUmABytes / 2, &tmA, &full[st], r0 + 16, static_cast<int32_t>(j0));
+          bulk_g2s(sO + st * Cfg::kOBytes, Oblk + (kb / 32 + s) * Cfg::kOBytes, Cfg::kOBytes, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc_u = umma_idesc_i8(false, NPAD), idesc_s = umma_idesc_i8(true, NPAD);
+      int64_t g = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int64_t j0, kb;
+        int nsteps;
+        item_range(it, j0, kb, nsteps);
+        for (int s = 0; s < nsteps; ++s, ++g) {
+          const int st = static_cast<int>(g % Cfg::kStages), sb = static_cast<int>(g & 1);
+          mbar_wait(&full[st], static_cast<uint32_t>(g / Cfg::kStages) & 1);
+          mbar_wait(&sfull[sb], static_cast<uint32_t>(g >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint64_t bdesc = umma_desc(smem_u32(sO + st * Cfg::kOBytes));
+          if (!(ablate & 2)) {
+#pragma unroll
+            for (int t = 0; t < NS; ++t)
+              umma_i8_ta(tmem + t * NPAD, tmem + NS * NPAD + (sb * NS + t) * 8, bdesc, t == NS - 1 ? idesc_s : idesc_u,
+                         s > 0);
+          }
+          umma_commit(&sempty[sb]);  // the slice tile may be rewritten once these MMAs are done
+          umma_commit(&empty[st]);   // the operator block is consumed (the A tile by the converters)
+        }
+      }
+    }
+  } else {
+    // ---------------- conversion (warps 0-7): thread = rows 16*half.. of column jl of the item's 128;
+    // warps w and w + 4 share columns (and TMEM lanes 32*(w%4)..); the column exponent is their
+    // joint maximum (exchanged through shared memory), the TMEM fold is done by the half-0 warp
+    const int cw = warp & 3, half = warp >> 2;
+    const int jl = cw * 32 + lane;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(32 * cw) << 16);  // this warp's TMEM lanes
+    const uint32_t my_off = static_cast<uint32_t>(jl) * 128u;
+    int64_t g = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      int64_t j0, kb;
+      int nsteps;
+      item_range(it, j0, kb, nsteps);
+#pragma unroll 8
+      for (int h = 0; h < NPAD; ++h) yacc[h * kUmCols + jl] = 0.0;
+      double asq4[4] = {0.0, 0.0, 0.0, 0.0};
+      int ecol = 0;
+      uint32_t hlim = 1u << 20;
+      double fa = pow2i((kSh - 1) / 2), fb = pow2i(kSh - 1 - (kSh - 1) / 2), fone = 1.0;
+      bool two_step = true;
+      // fold this warp's TMEM lanes (all slices) into yacc with the current scale, then zero them
+      auto fold = [&]() {
+        const int sh = max(ecol, 1) - kSh;  // <= 970
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          const int e = sh + 8 * t;
+          const double f1 = pow2i(e / 2), f2 = pow2i(e - e / 2);
+#pragma unroll
+          for (int c0 = 0; c0 < NPAD; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tl + t * NPAD + c0, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int v = 0; v < 16; ++v)
+              yacc[(c0 + v) * kUmCols + jl] += (static_cast<double>(static_cast<int>(r[v])) * f1) * f2;
+            tmem_st16_zero(tl + t * NPAD + c0);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      };
+      for (int s = 0; s < nsteps; ++s, ++g) {
+        const int st = static_cast<int>(g % Cfg::kStages), sb = static_cast<int>(g & 1);
+        mbar_wait(&full[st], static_cast<uint32_t>(g / Cfg::kStages) & 1);
+        double x[16];
+        const uint8_t* tile = sA + st * kUmABytes + half * (kUmABytes / 2);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double2 v = *reinterpret_cast<const double2*>(tile + my_off + (((c ^ (jl & 7)) & 7) << 4));
+          x[2 * c] = v.x;
+          x[2 * c + 1] = v.y;
+        }
+        mbar_arrive(&empty[st]);  // A tile consumed (values are in registers)
+        if (ablate & 1) {  // measurement only: stream the tiles, skip the conversion
+          asq4[0] += x[0] + x[15];
+          if (g >= 2) mbar_wait(&sempty[sb], static_cast<uint32_t>((g >> 1) - 1) & 1);
+          mbar_arrive(&sfull[sb]);
+          continue;
+        }
+        uint32_t hmax = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          asq4[u & 3] = fma(x[u], x[u], asq4[u & 3]);
+          hmax = max(hmax, static_cast<uint32_t>(__double2hiint(x[u])) & 0x7fffffffu);
+        }
+        uint32_t* hxs = hx + (g & 1) * 256;
+        hxs[half * 128 + jl] = hmax;
+        asm volatile("bar.sync %0, 64;\n" ::"r"(2 + cw) : "memory");
+        hmax = max(hmax, hxs[(half ^ 1) * 128 + jl]);
+        // the slice buffer sb (TMEM) is free once the MMAs of global k-step g - 2 are done
+        if (g >= 2) mbar_wait(&sempty[sb], static_cast<uint32_t>((g >> 1) - 1) & 1);
+        if (__any_sync(0xffffffffu, hmax >= hlim)) {
+          if (s >= 1 && half == 0) {  // the MMAs of k-step g - 1 complete before this warp reads its lanes
+            mbar_wait(&sempty[sb ^ 1], static_cast<uint32_t>((g - 1) >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            fold();
+          }
+          const int emax = static_cast<int>(hmax >> 20);
+          if (emax > ecol) {
+            ecol = emax + 1 < 2046 ? emax + 1 : emax;
+            hlim = static_cast<uint32_t>(ecol + 1) << 20;
+          }
+          const int sh = kSh - max(ecol, 1);
+          fa = pow2i(sh / 2);
+          fb = pow2i(sh - sh / 2);
+          fone = pow2i(sh < 1023 ? sh : 0);
+          two_step = sh >= 1023;
+        }
+        // scale (one multiply; columns below 2^-969 take two exact steps on a warp-uniform slow path)
+        if (__any_sync(0xffffffffu, two_step)) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) x[u] = two_step ? (x[u] * fa) * fb : x[u] * fone;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) x[u] *= fone;
+        }
+        // slices -> the MMA's A operand in TMEM: lane = column, this half's 16 bytes of slice t in
+        // columns NS*NPAD + (sb*NS + t)*8 + 4*half .. +3 (4 rows per 32-bit column)
+        uint32_t sl[2][NS][2];
+#pragma unroll
+        for (int g8 = 0; g8 < 2; ++g8) {
+          uint32_t lo[8], hi[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long long w = __double2ll_rn(x[8 * g8 + u]);
+            lo[u] = static_cast<uint32_t>(w);
+            hi[u] = static_cast<uint32_t>(static_cast<unsigned long long>(w) >> 32);
+          }
+          uint32_t b0[kImSlices], b1[kImSlices];
+          byte_transpose(lo[0], lo[1], lo[2], lo[3], hi[0], hi[1], hi[2], hi[3], b0);
+          byte_transpose(lo[4], lo[5], lo[6], lo[7], hi[4], hi[5], hi[6], hi[7], b1);
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            sl[g8][t][0] = b0[t];
+            sl[g8][t][1] = b1[t];
+          }
+        }
+        const uint32_t ta = tl + NS * NPAD + sb * NS * 8 + 4 * half;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) tmem_st4(ta + 8 * t, sl[0][t][0], sl[0][t][1], sl[1][t][0], sl[1][t][1]);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(&sfull[sb]);
+      }
+      // item done: fold after its last MMAs, write the split's partial column, ||A||^2 partial
+      if (nsteps > 0 && half == 0) {
+        mbar_wait(&sempty[(g - 1) & 1], static_cast<uint32_t>((g - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        fold();
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      }
+      const int64_t j = j0 + jl;
+      if (half == 0 && j < n) {
+        double* out = part + (it / col_tiles) * split_stride + j * c_pad;
+#pragma unroll 8
+        for (int h = 0; h < NPAD; ++h)
+          if (h < c_pad) out[h] = yacc[h * kUmCols + jl];
+      }
+      const double ws = warp_sum((asq4[0] + asq4[1]) + (asq4[2] + asq4[3]));
+      if (lane == 0) red[warp] = ws;
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      if (tid == 0) asq_part[it] = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(Cfg::kTmemCols) : "memory");
+  }
+}
+
+// operator in per-k-step blocks of the canonical K-major layout: block q (rows 32q..32q+31 of A)
+// holds Omega(h, 32q + kk) at ((h / 8) * 2 + kk / 16) * 128 + (h % 8) * 16 + kk % 16
+__global__ void gen_sparse_sign_umma_kernel(int8_t* O, int npad, int64_t c, int64_t m, uint64_t seed, int zeta_eff) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t rows[16];
+    int8_t signs[16];
+    sparse_sign_slots(seed, i, c, zeta_eff, rows, signs);
+    const int64_t q = i >> 5;
+    const int kk = static_cast<int>(i & 31);
+    int8_t* blk = O + q * npad * 32;
+    for (int t = 0; t < zeta_eff; ++t) {
+      const int h = rows[t];
+      blk[((h >> 3) * 2 + (kk >> 4)) * 128 + (h & 7) * 16 + (kk & 15)] = signs[t];
+    }
+  }
+}
+
+bool sparse_sketch_umma_supported(const double* A, int64_t m, int64_t n, int64_t lda, int64_t c_pad) {
+  return c_pad <= 64 && (lda % 2) == 0 && (reinterpret_cast<uintptr_t>(A) % 16) == 0 && m < (int64_t(1) << 31) &&
+         n < (int64_t(1) << 31);
+}
+
+struct UmPlan {
+  int64_t col_tiles, splits, kps, npad, ksteps, items, grid;
+};
+static int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
+static UmPlan plan_umma(int64_t m, int64_t n, int64_t c_pad) {
+  UmPlan p{};
+  p.npad = c_pad <= 32 ? 32 : 64;
+  p.col_tiles = ceil_div(n, kUmCols);
+  p.ksteps = ceil_div(m, 32);
+  const int64_t sms = num_sms();
+  // persistent CTAs (one per SM): the split count minimising the busiest CTA's k-steps, charging each
+  // item ~8 k-steps of fold/drain and each split a partial Y pass; >= 32 k-steps per item; <= 2^17
+  // k-steps per item keeps every int32 slice sum exact
+  int64_t s = 1;
+  double best = 1e300;
+  for (int64_t t = 1; t <= 64; ++t) {
+    const int64_t kps = ceil_div(p.ksteps, t);
+    if (t > 1 && kps < 32) break;
+    const int64_t items = p.col_tiles * ceil_div(p.ksteps, kps);
+    const double per_cta = std::ceil(static_cast<double>(items) / sms) * (kps + 8.0);
+    const double partials = t > 1 ? 2.0 * t * n * c_pad * 8.0 / (32.0 * kUmCols * 8.0 * sms) : 0.0;
+    if (per_cta + partials < best) {
+      best = per_cta + partials;
+      s = t;
+    }
+  }
+  s = std::max<int64_t>(s, ceil_div(p.ksteps, int64_t(1) << 17));
+  p.kps = ceil_div(p.ksteps, s);
+  p.splits = ceil_div(p.ksteps, p.kps);
+  p.items = p.col_tiles * p.splits;
+  p.grid = std::min<int64_t>(p.items, sms);
+  return p;
+}
+
+int64_t sparse_sketch_umma_workspace_elems(int64_t m, int64_t n, int64_t c_pad) {
+  const UmPlan p = plan_umma(m, n, c_pad);
+  const int64_t part = p.splits > 1 ? p.splits * n * c_pad : 0;
+  const int64_t om = ceil_div(p.ksteps * p.npad * 32, 8);
+  return part + p.items + om + 4096 + 16;
+}
+
+cudaError_t run_sketch_apply_sparse_umma(const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed, int64_t c,
+                                         int64_t c_pad, int zeta, double scale, double* Y, double* ws, int64_t ws_elems,
+                                         const SketchStats& stats, cudaStream_t st, SketchLaunchInfo* info,
+                                         bool operator_ready, bool kernel_only) {
+  if (!sparse_sketch_umma_supported(A, m, n, lda, c_pad)) return cudaErrorInvalidValue;
+  const UmPlan p = plan_umma(m, n, c_pad);
+  if (sparse_sketch_umma_workspace_elems(m, n, c_pad) > ws_elems) return cudaErrorInvalidValue;
+  const int64_t part_elems = p.splits > 1 ? p.splits * n * c_pad : 0;
+  double* part = ws;
+  double* asq_part = ws + part_elems;
+  int8_t* O = reinterpret_cast<int8_t*>(round_up(reinterpret_cast<uintptr_t>(asq_part + p.items), 128));
+  double* ysq_part = reinterpret_cast<double*>(round_up(reinterpret_cast<uintptr_t>(O + p.ksteps * p.npad * 32), 16));
+  cudaError_t e;
+  if (!operator_ready) {
+    e = cudaMemsetAsync(O, 0, static_cast<size_t>(p.ksteps * p.npad * 32), st);
+    if (e != cudaSuccess) return e;
+    const int ze = static_cast<int>(std::min<int64_t>(zeta, c));
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 148 * 16));
+    gen_sparse_sign_umma_kernel<<<blocks, 256, 0, st>>>(O, static_cast<int>(p.npad), c, m, seed, ze);
+  }
+  CUtensorMap tmA{};
+  if (!make_tmap_2d(&tmA, A, m, n, lda, 16, kUmCols)) return cudaErrorInvalidValue;
+  auto launch = [&](auto kern, int npad) {
+    const int smem = npad == 32 ? UmCfg<32>::kSmem : UmCfg<64>::kSmem;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    const int ablate = getenv("ITERCUR_UMMA_ABLATE") ? atoi(getenv("ITERCUR_UMMA_ABLATE")) : 0;  // measurement
+    kern<<<static_cast<unsigned>(p.grid), kUmThreads, smem, st>>>(tmA, O, m, n, p.col_tiles, p.items, p.kps, c_pad,
+                                                                   p.splits > 1 ? part : Y, n * c_pad, asq_part,
+                                                                   ablate);
+    return cudaGetLastError();
+  };
+  if (p.npad == 32) e = launch(sparse_sketch_umma_kernel<32, UmCfg<32>::kNS>, 32);
+  else e = launch(sparse_sketch_umma_kernel<64, UmCfg<64>::kNS>, 64);
+  if (e != cudaSuccess) return e;
+  if (info) {
+    info->splits = static_cast<int>(p.splits);
+    info->ctas = static_cast<int>(p.grid);
+    info->nt = static_cast<int>(p.npad);
+    info->tma = true;
+    info->dominant_launches = 1;
+  }
+  if (kernel_only) return cudaGetLastError();
+  const int64_t total = n * c_pad;
+  const int rblocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 2048));
+  sketch_reduce_kernel<<<rblocks, 256, 0, st>>>(p.splits > 1 ? part : Y, p.splits > 1 ? static_cast<int>(p.splits) : 1,
+                                                n * c_pad, scale, Y, total, ysq_part);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(ysq_part, rblocks, stats.d_ysq);
+  reduce_partials_kernel<<<1, 256, 0, st>>>(asq_part, static_cast<int>(p.items), stats.d_asq);
+  return cudaGetLastError();
+}
+
 }  // namespace itercur_b200

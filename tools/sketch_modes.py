@@ -19,7 +19,7 @@ for m, n, b in shapes:
     a = torch.empty(n, m, dtype=torch.float64, device="cuda").t()
     for j0 in range(0, n, 4096):  # fill in slabs (bounded temporary memory)
         a[:, j0:j0 + 4096].normal_()
-    for mode in ("0", "2", "1"):
+    for mode in os.environ.get("SKETCH_MODES", "0,2,1").split(","):
         if mode == "1" and m * n > 1e9:
             continue
         os.environ["ITERCUR_SPARSE_SKETCH"] = mode
