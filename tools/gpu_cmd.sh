@@ -1,1 +1,2 @@
-for mode in 2 3; do SKETCH_MODES=$mode timeout 300 python tools/sketch_modes.py 20000 10000 20 40000 20000 50 100000 50000 50 2000 2000 10 100000 100000 50 2>&1 | sed "s/^/mode=$mode /"; done > gpurun_out/sketch_modes2.txt
+timeout 1500 python tools/config_sweep.py --true-error > gpurun_out/config_sweep.jsonl 2> gpurun_out/config_sweep.err
+ncu --set full --clock-control none --import-source on -k regex:sparse_sketch_umma -c 1 -o gpurun_out/full_v5_umma python tools/sketch_one.py 100000 50000 50 sparse_sign 1 > gpurun_out/ncu_umma.log 2>&1
