@@ -309,7 +309,7 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
     yfull = _gather_columns(comm, y, widths) if column_exchange == "sketch" else None
     cap = max_rank_eff + b
     L = colmajor_empty(m, cap, dev, fill=0.0)             # residual columns, replicated
-    Rt = colmajor_empty(cap, n_r, dev, fill=0.0)          # rows of R~ for this shard
+    RtT = colmajor_empty(n_r, cap, dev, fill=0.0)         # R~^T for this shard (n_r x cap, column-major)
     col_live = torch.ones(n_r, dtype=torch.uint8, device=dev)
     I, J, rhos, col_steps = [], [], [], []
     r, k = 0, 0
@@ -338,12 +338,14 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
         # of disjoint contributions (exact) ----
         yrows = y.shape[0] if column_exchange != "sketch" else 0
         pack = torch.zeros(w_cols, _even(m + r + yrows), dtype=torch.float64, device=dev)  # column q = [A; R~; Y](:, J_q)
-        for q, jl in own:
-            pack[q, :m] = a[:, jl]
+        if own:
+            qs = torch.tensor([q for q, _ in own], dtype=torch.int64, device=dev)
+            js = torch.tensor([jl for _, jl in own], dtype=torch.int64, device=dev)
+            pack[qs, :m] = a.index_select(1, js).t()
             if r:
-                pack[q, m:m + r] = Rt[:r, jl]
+                pack[qs, m:m + r] = RtT[:, :r].index_select(0, js)
             if yrows:
-                pack[q, m + r:m + r + yrows] = y[:, jl]
+                pack[qs, m + r:m + r + yrows] = y.index_select(1, js).t()
         comm.all_reduce(pack)
         packT = pack.t()                                  # (m + r + yrows) x w, column-major view
         Acols = packT[:m, :]
@@ -373,18 +375,18 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
         if n_r:
             At = to_colmajor(a[Ik_t, :].t())            # n_r x width
             Ut = colmajor_empty(n_r, width, dev)
-            be.gemm(to_colmajor(Rt[:r, :].t()), to_colmajor(L[Ik_t, :r].t()), At, -1.0, Ut)
-            Rk = colmajor_empty(n_r, width, dev)
+            be.gemm(RtT[:, :r], to_colmajor(L[Ik_t, :r].t()), At, -1.0, Ut)
+            Rk = RtT[:, r:r + width]                     # R~_k^T solved in place of its columns
             be.rows_solve(Ut, D, Rk)
-            Rt[r:r + width, :].copy_(Rk.t())
             # ---- downdate Y^T -= R~_k^T Y(:,J_k)^T (sketch.cpp:26-41) ----
             Yt = to_colmajor(y.t())                      # n_r x cp
             Ynew = colmajor_empty(n_r, y.shape[0], dev)
             be.gemm(Rk, to_colmajor(Ycols[:, :width].t()), Yt, -1.0, Ynew)
             y = to_colmajor(Ynew.t())
-        for q, jl in own:
-            if q < width:
-                col_live[jl] = 0
+        if column_exchange != "sketch":
+            for q, jl in own:
+                if q < width:
+                    col_live[jl] = 0
         if column_exchange == "sketch":
             yfull = _gather_columns(comm, y, widths)
             ysq_all = float(torch.sum(yfull[:c, :] * yfull[:c, :]).item())
