@@ -146,8 +146,9 @@ def kernel_rooflines(engine, stages, cfg, m, n, rank_final, n_iters, hbm):
 
 
 def cpu_reference_sample(a_host, cfg, n_iters_total, budget_s=20.0):
-    """Time the CPU oracle (restatement of the reference, single thread like the reference)
-    on the same matrix: the sketch plus the leading iterations until `budget_s` elapses
+    """Time the CPU oracle (restatement of the reference; its independent-column loops — sketch,
+    GEMMs, the COD's reflector applications and solves — split over all host threads, bitwise the
+    single-thread result) on the same matrix: the sketch plus the leading iterations until `budget_s` elapses
     (or convergence). The unmeasured tail is charged at the cost of the last measured
     iteration — an underestimate (per-iteration cost grows as O(r^3) in the reference's
     COD), so the reported CPU throughput is an upper bound."""
@@ -177,8 +178,10 @@ def cpu_reference_sample(a_host, cfg, n_iters_total, budget_s=20.0):
         t_est = t_meas + max(0, n_iters_total - measured) * last
         note = (f"sketch + first {measured} of {n_iters_total} iterations measured ({t_meas:.2f} s); "
                 f"remaining iterations charged at the last measured iteration's {last:.3f} s (lower bound on time)")
-    return {"value": m * n / t_est, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle restatement of the reference (-O3, 1 thread) on config 2's matrix: {note}",
+    threads = int(os.environ.get("ORACLE_THREADS", "0") or 0) or (os.cpu_count() or 1)
+    return {"value": m * n / t_est, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle restatement of the reference (-O3, {threads} host threads over independent columns) "
+                      f"on the bench config's matrix: {note}",
             "t_est_s": t_est, "t_measured_s": t_meas, "iterations_measured": measured}
 
 

@@ -23,8 +23,101 @@
 #include <string>
 #include <unordered_set>
 #include <vector>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <functional>
+#include <mutex>
+#include <thread>
 
 namespace oracle {
+
+// ---------------------------------------------------------------------------------
+// Host threading for the CPU timing arm (no OpenMP runtime in this image): a persistent pool
+// that splits an index range [b, e) into static contiguous chunks. Only loops over independent
+// columns use it, each column's operations unchanged, so results are bitwise the 1-thread
+// ones. ORACLE_THREADS (default: all hardware threads) sets the pool size; 1 = sequential.
+// ---------------------------------------------------------------------------------
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool p;
+    return p;
+  }
+  int size() const { return nthreads_; }
+  void run(std::int64_t b, std::int64_t e, const std::function<void(std::int64_t)>& fn) {
+    std::unique_lock<std::mutex> lk(mu_);
+    fn_ = &fn;
+    b_ = b;
+    e_ = e;
+    pending_ = nthreads_ - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    chunk(0, b, e, fn);  // the caller takes chunk 0
+    lk.lock();
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  Pool() {
+    const char* env = std::getenv("ORACLE_THREADS");
+    int n = env ? std::atoi(env) : static_cast<int>(std::thread::hardware_concurrency());
+    nthreads_ = n < 1 ? 1 : n;
+    for (int t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void chunk(int t, std::int64_t b, std::int64_t e, const std::function<void(std::int64_t)>& fn) const {
+    const std::int64_t n = e - b, per = (n + nthreads_ - 1) / nthreads_;
+    const std::int64_t lo = b + t * per, hi = std::min(e, lo + per);
+    for (std::int64_t i = lo; i < hi; ++i) fn(i);
+  }
+  void loop(int t) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      const auto* fn = fn_;
+      const std::int64_t b = b_, e = e_;
+      lk.unlock();
+      chunk(t, b, e, *fn);
+      lk.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  int nthreads_ = 1;
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(std::int64_t)>* fn_ = nullptr;
+  std::int64_t b_ = 0, e_ = 0;
+  int pending_ = 0;
+  std::uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+template <class F>
+void parallel_for(std::int64_t b, std::int64_t e, bool worth_it, F&& f) {
+  if (e <= b) return;
+  Pool* pool = worth_it && (e - b) > 1 ? &Pool::get() : nullptr;
+  if (!pool || pool->size() == 1) {
+    for (std::int64_t i = b; i < e; ++i) f(i);
+    return;
+  }
+  const std::function<void(std::int64_t)> fn = [&](std::int64_t i) { f(i); };
+  pool->run(b, e, fn);
+}
 
 using Index = std::int64_t;
 using IndexList = std::vector<Index>;
@@ -205,7 +298,8 @@ struct Cod {
       qr(k, k) = beta;
       hcoeffs[static_cast<size_t>(k)] = tau;
       maxpivot = std::max(maxpivot, std::abs(beta));
-      for (Index j = k + 1; j < cols; ++j) {
+      // columns are independent: threads change nothing but the wall time (same operations, same order)
+      parallel_for(k + 1, cols, (cols - k) * (rows - k) > 32768, [&](Index j) {
         // apply reflector (stored with implicit leading 1) to column j
         double* y = qr.col(j) + k;
         const double* v = qr.col(k) + k;
@@ -215,8 +309,8 @@ struct Cod {
           y[0] -= tau * tmp;
           for (Index q = 1; q < rows - k; ++q) y[q] -= tau * v[q] * tmp;
         }
-      }
-      for (Index j = k + 1; j < cols; ++j) {
+      });
+      parallel_for(k + 1, cols, (cols - k) * (rows - k) > 32768, [&](Index j) {
         double& nu = norm_upd[static_cast<size_t>(j)];
         if (nu != 0.0) {
           double temp = std::abs(qr(k, j)) / nu;
@@ -231,7 +325,7 @@ struct Cod {
             nu *= std::sqrt(temp);
           }
         }
-      }
+      });
     }
     const double pre = std::abs(maxpivot) * threshold;
     rank = 0;
@@ -250,7 +344,8 @@ struct Cod {
         make_householder(lq.col(k) + k, cols - k, tau, beta);
         lq(k, k) = beta;
         lq_tau[static_cast<size_t>(k)] = tau;
-        for (Index j = k + 1; j < rank; ++j) apply_left(lq.col(k) + k, cols - k, tau, lq.col(j) + k);
+        parallel_for(k + 1, rank, (rank - k) * (cols - k) > 32768,
+                     [&](Index j) { apply_left(lq.col(k) + k, cols - k, tau, lq.col(j) + k); });
       }
     }
   }
@@ -260,8 +355,8 @@ struct Cod {
     if (rhs.rows != rows) throw std::invalid_argument("apply_pinv_left: expected " + std::to_string(rows) +
                                                       " rows, got " + std::to_string(rhs.rows));
     Mat out(cols, rhs.cols);
-    std::vector<double> c(static_cast<size_t>(rows)), z(static_cast<size_t>(cols));
-    for (Index col = 0; col < rhs.cols; ++col) {
+    parallel_for(0, rhs.cols, rhs.cols * rows * cols > 65536, [&](Index col) {
+      std::vector<double> c(static_cast<size_t>(rows)), z(static_cast<size_t>(cols));
       std::copy(rhs.col(col), rhs.col(col) + rows, c.begin());
       const Index size = std::min(rows, cols);
       for (Index k = 0; k < size; ++k)  // c = Q^T b
@@ -286,7 +381,7 @@ struct Cod {
         for (Index j = 0; j < cols; ++j) z[static_cast<size_t>(j)] = w[static_cast<size_t>(j)];
       }
       for (Index k = 0; k < cols; ++k) out(perm[static_cast<size_t>(k)], col) = z[static_cast<size_t>(k)];
-    }
+    });
     return out;
   }
 };
@@ -345,7 +440,7 @@ Mat gather_rows(const View& a, const IndexList& rows) {  // matrix.cpp:196-206
 View view(const Mat& m) { return View{m.v.data(), m.rows, m.cols, m.rows}; }
 // C += alpha * A * B (plain loops, column-major; order a-priori fixed)
 void gemm_acc(const Mat& a, const Mat& b, Mat& c, double alpha) {
-  for (Index j = 0; j < b.cols; ++j)
+  parallel_for(0, b.cols, b.cols * a.cols * a.rows > 65536, [&](Index j) {
     for (Index k = 0; k < a.cols; ++k) {
       const double bk = alpha * b(k, j);
       if (bk == 0.0) continue;
@@ -353,6 +448,7 @@ void gemm_acc(const Mat& a, const Mat& b, Mat& c, double alpha) {
       double* cj = c.col(j);
       for (Index i = 0; i < a.rows; ++i) cj[i] += ak[i] * bk;
     }
+  });
 }
 
 // proj/include/itercur/pinv.hpp:57-66
@@ -420,16 +516,17 @@ SketchState make_sketch(std::uint64_t seed, Index b, const View& a, int kind, in
   double asq = 0.0;
   if (kind == ORACLE_SKETCH_GAUSSIAN) {
     const Mat g = gaussian_matrix(c, m, seed, ORACLE_STREAM_SKETCH);  // sketch.cpp:19
-    for (Index j = 0; j < n; ++j) {                                      // sketch.cpp:20 (G*A)
+    for (Index j = 0; j < n; ++j)  // ||A||^2: one running sum in column order (as before threading)
+      for (Index k = 0; k < m; ++k) asq += a.p[j * a.ld + k] * a.p[j * a.ld + k];
+    parallel_for(0, n, n * m * c > 65536, [&](Index j) {  // sketch.cpp:20 (G*A)
       double* y = st.sketched_input.col(j);
       const double* aj = a.p + j * a.ld;
       for (Index k = 0; k < m; ++k) {
         const double akj = aj[k];
-        asq += akj * akj;
         const double* gk = g.col(k);
         for (Index i = 0; i < c; ++i) y[i] += gk[i] * akj;
       }
-    }
+    });
   } else if (kind == ORACLE_SKETCH_SPARSE_SIGN) {
     const int zeta_eff = static_cast<int>(std::min<Index>(zeta, c));
     if (zeta_eff < 1) throw std::invalid_argument("sparse_nnz must be at least 1");
@@ -438,19 +535,20 @@ SketchState make_sketch(std::uint64_t seed, Index b, const View& a, int kind, in
     for (Index i = 0; i < m; ++i)
       sparse_sign_column(seed, i, c, zeta_eff, rows.data() + i * zeta_eff, signs.data() + i * zeta_eff);
     const double scale = 1.0 / std::sqrt(static_cast<double>(zeta_eff));
-    for (Index j = 0; j < n; ++j) {
+    for (Index j = 0; j < n; ++j)  // ||A||^2: one running sum in column order (as before threading)
+      for (Index i = 0; i < m; ++i) asq += a.p[j * a.ld + i] * a.p[j * a.ld + i];
+    parallel_for(0, n, n * m > 65536, [&](Index j) {
       double* y = st.sketched_input.col(j);
       const double* aj = a.p + j * a.ld;
       for (Index i = 0; i < m; ++i) {
         const double v = aj[i];
-        asq += v * v;
         for (int t = 0; t < zeta_eff; ++t) {
           const size_t q = static_cast<size_t>(i * zeta_eff + t);
           if (signs[q] > 0) y[rows[q]] += v; else y[rows[q]] -= v;
         }
       }
       for (Index i = 0; i < c; ++i) y[i] *= scale;
-    }
+    });
   } else {
     throw std::invalid_argument("unknown sketch kind");
   }

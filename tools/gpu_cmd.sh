@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_sharded.py -x -q > gpurun_out/pytest_sharded.log 2>&1
-timeout 900 python bench.py --sharded --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_sharded_sketch.json 2>gpurun_out/bench_sharded.err
+nproc > gpurun_out/nproc.txt
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
