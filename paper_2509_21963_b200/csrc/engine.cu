@@ -871,14 +871,19 @@ void run_iterative_cur(itercur_run* run) {
         static const bool force_cross_lu = env_flag("ITERCUR_FORCE_CROSS_LU");  // A/B check
         if (row_lupp_path >= 0 || force_cross_lu)  // the cluster / panel LUPP emitted D_k's factors itself
           CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
-        if (!row_fused)
+        static const bool pair_off = env_flag("ITERCUR_NO_PAIR_GATHER");  // A/B
+        const bool y_here = fused_ub && !y_side && !col_fused;  // Y(:, J_k) gathered right before the U block
+        if (!row_fused && y_here && !pair_off)  // L(I_k, :)^T and Y(:, J_k) in one launch
+          CK(launch_gather_pair(run->L.p, run->ldL, 1, ldbg, arr.row_idx, ws.Bg.p, ldbg, true, ws.Y.p, 1, cp, cp,
+                                arr.col_idx, ws.Yg.p, cp, false, &slot->width, B, st, d_ctl));
+        else if (!row_fused)
           CK(launch_gather(run->L.p, run->ldL, 1, ldbg, arr.row_idx, &slot->width, B, ws.Bg.p, ldbg, st, d_ctl, true));
         if (fused_ub) {
           // Y(:, J_k) before the downdate, then one kernel: U_k^T, the solves against D_k,
           // R~ rows, Y^T -= R~_k^T Y(:, J_k)^T, ||Y||^2 partials and Wc
           if (y_side)
             CK(cudaStreamWaitEvent(st, side_stream().join, 0));
-          else if (!col_fused)
+          else if (y_here && (row_fused || pair_off))
             CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
           TsGemmParams p = ublock_params(ldbg, slot, arr);
           p.k_plan = k_plan;
@@ -899,7 +904,7 @@ void run_iterative_cur(itercur_run* run) {
           }
           CK(run_ts_gemm_ublock(p, st));
           batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0) - (col_fused ? 2 : 0) - (begin_fused ? 1 : 0) -
-                            (row_fused ? 1 : 0);
+                            (row_fused ? 1 : 0) - ((!row_fused && y_here && !pair_off) ? 1 : 0);
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));  // downdate fused into the core step
           if (!fused_commit) {

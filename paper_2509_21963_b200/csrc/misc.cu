@@ -93,6 +93,45 @@ cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_str
                    d_w, w_max, out, ldo, ctl, k_from_r ? 1 : 0);
 }
 
+// Two gathers of the same (dynamic) width in one launch: the U block's operands L(I_k, :)^T and
+// Y(:, J_k) (one launch per iteration fewer inside the batch graphs)
+struct GatherDesc {
+  const double* src;
+  int64_t row_stride, col_stride, Kmax;
+  const int64_t* idx;
+  double* out;
+  int64_t ldo;
+  int k_from_r;
+};
+__global__ void gather_pair_kernel(GatherDesc g0, GatherDesc g1, const int* __restrict__ d_w, int w_max,
+                                   const IterCtl* __restrict__ ctl) {
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl && ctl->done) return;
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  const int64_t K0 = (ctl && g0.k_from_r) ? min(g0.Kmax, ctl->r) : g0.Kmax;
+  const int64_t K1 = (ctl && g1.k_from_r) ? min(g1.Kmax, ctl->r) : g1.Kmax;
+  const int64_t t0 = K0 * w_max, total = t0 + K1 * w_max;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const bool second = e >= t0;
+    const GatherDesc& g = second ? g1 : g0;
+    const int64_t K = second ? K1 : K0, f = second ? e - t0 : e;
+    const int64_t q = f / K, k = f - q * K;
+    g.out[k + q * g.ldo] = q < w ? g.src[k * g.row_stride + g.idx[q] * g.col_stride] : 0.0;
+  }
+}
+cudaError_t launch_gather_pair(const double* src0, int64_t rs0, int64_t cs0, int64_t K0, const int64_t* idx0,
+                               double* out0, int64_t ldo0, bool k_from_r0, const double* src1, int64_t rs1,
+                               int64_t cs1, int64_t K1, const int64_t* idx1, double* out1, int64_t ldo1,
+                               bool k_from_r1, const int* d_w, int w_max, cudaStream_t st, const IterCtl* ctl) {
+  const int64_t total = (K0 + K1) * w_max;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  const GatherDesc g0{src0, rs0, cs0, K0, idx0, out0, ldo0, k_from_r0 ? 1 : 0};
+  const GatherDesc g1{src1, rs1, cs1, K1, idx1, out1, ldo1, k_from_r1 ? 1 : 0};
+  return launch_ex(gather_pair_kernel, dim3(blocks), dim3(256), 0, st, dim3(0, 0, 0), g0, g1, d_w, w_max, ctl);
+}
+
 __global__ void gather2_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ idx, int64_t K,
                                int w, double* __restrict__ out, int64_t ldo) {
   const int64_t total = K * w;

@@ -132,6 +132,10 @@ cudaError_t launch_transpose(const double* A, int64_t m, int64_t n, int64_t lda,
                              cudaStream_t st);
 // out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < min(*d_w, w_max), zero for
 // q >= w. With ctl: skipped when ctl->done, and K = ctl->r when k_from_r.
+cudaError_t launch_gather_pair(const double* src0, int64_t rs0, int64_t cs0, int64_t K0, const int64_t* idx0,
+                               double* out0, int64_t ldo0, bool k_from_r0, const double* src1, int64_t rs1,
+                               int64_t cs1, int64_t K1, const int64_t* idx1, double* out1, int64_t ldo1,
+                               bool k_from_r1, const int* d_w, int w_max, cudaStream_t st, const IterCtl* ctl);
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
                           const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
                           const IterCtl* ctl = nullptr, bool k_from_r = false);

@@ -1,3 +1,4 @@
-nproc > gpurun_out/nproc.txt
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+for i in 1 2; do
+python tools/time_runs.py --config 2 --runs 8 > gpurun_out/tr_pair_$i.txt 2>&1
+ITERCUR_NO_PAIR_GATHER=1 python tools/time_runs.py --config 2 --runs 8 > gpurun_out/tr_nopair_$i.txt 2>&1
+done
