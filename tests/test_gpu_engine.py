@@ -23,7 +23,8 @@ def low_rank_plus_noise(oracle, m, n, r, rel_noise, seed):
 
 
 @pytest.mark.parametrize("case", ["expdecay600", "lowrank_noise", "rbf1500", "sparse_sign", "sparse_sign_b40",
-                                  "odd_shape", "b64", "b1"])
+                                  "sparse_sign_b40_tcgen05", "sparse_sign_b40_mma_s8", "sparse_sign_b40_dmma",
+                                  "sparse_sign_b50_tall", "odd_shape", "b64", "b1"])
 def test_engine_matches_oracle(engine, oracle, case):
     rng = np.random.default_rng(11)
     kw = dict(epsilon=1e-6, b=10, seed=0)
@@ -42,12 +43,18 @@ def test_engine_matches_oracle(engine, oracle, case):
         v, _ = np.linalg.qr(rng.standard_normal((400, 400)))
         a = (u * (np.arange(1, 401) ** -2.0)) @ v.T
         kw.update(epsilon=1e-4, b=20, seed=2, sketch="sparse_sign")
-    elif case == "sparse_sign_b40":  # c_pad = 48, through the opt-in sparse-operator sketch kernel
+    elif case.startswith("sparse_sign_b40"):  # c_pad = 48 through each sparse-sign sketch kernel
         import os
 
-        os.environ["ITERCUR_SPARSE_SKETCH"] = "1"
+        mode = {"sparse_sign_b40": "1", "sparse_sign_b40_tcgen05": "", "sparse_sign_b40_mma_s8": "2",
+                "sparse_sign_b40_dmma": "0"}[case]  # "" = the default (tcgen05 above c_pad 32)
+        if mode:
+            os.environ["ITERCUR_SPARSE_SKETCH"] = mode
         a = low_rank_plus_noise(oracle, 900, 700, 120, 1e-9, 13)
         kw.update(epsilon=1e-7, b=40, seed=5, sketch="sparse_sign")
+    elif case == "sparse_sign_b50_tall":  # config 4's block size (c = 55), tcgen05 sketch, split K
+        a = low_rank_plus_noise(oracle, 6000, 900, 140, 1e-10, 17)
+        kw.update(epsilon=1e-8, b=50, seed=7, sketch="sparse_sign")
     elif case == "b64":  # wide blocks: block-level LU and 64-wide solves (configs 4/5 use b = 50 / 64)
         a = low_rank_plus_noise(oracle, 700, 520, 150, 1e-10, 21)
         kw.update(epsilon=1e-8, b=64, seed=6)

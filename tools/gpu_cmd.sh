@@ -1,4 +1,1 @@
-for i in 1 2; do
-python tools/time_runs.py --config 2 --runs 8 > gpurun_out/tr_pair_$i.txt 2>&1
-ITERCUR_NO_PAIR_GATHER=1 python tools/time_runs.py --config 2 --runs 8 > gpurun_out/tr_nopair_$i.txt 2>&1
-done
+timeout 900 python -m pytest tests/test_gpu_engine.py -x -q -k "matches_oracle" > gpurun_out/pytest_engine.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_engine.log
