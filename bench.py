@@ -94,6 +94,54 @@ class ClockSampler:
 NCU_FULL = "profiles/ncu_full_r01_cfg2_v5.txt"  # the committed `ncu --set full` summary of this config
 
 
+def e2e_fits(bytes_needed, device_copy=True):
+    """Whether the e2e leg can pin `bytes_needed` of host memory (<= 40% of MemAvailable) and, for
+    the host entry's own device copy, allocate it beside the resident matrix. Configs 4/5 (80 GB)
+    do not: their e2e leg is skipped with the reason rather than risking the box."""
+    import torch
+
+    avail = 0
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                avail = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    if avail and bytes_needed > 0.4 * avail:
+        return False, f"pinned host copy of {bytes_needed / 1e9:.0f} GB > 40% of available host memory"
+    if device_copy and torch.cuda.is_available():
+        free, _ = torch.cuda.mem_get_info()
+        if bytes_needed * 1.15 > free:
+            return False, f"a second device copy of A ({bytes_needed / 1e9:.0f} GB) does not fit in free HBM"
+    return True, ""
+
+
+def run_e2e(engine, a, m, n, run_cfg, args, world):
+    """e2e leg: the host entry (MatrixHandle.dense over pinned memory), H2D inside the timed call."""
+    import torch
+
+    a_host_t = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+    a_host_t.copy_(a.t())
+    a_host = a_host_t.numpy().T  # (m, n) Fortran-ordered view of pinned memory
+    hh = engine.MatrixHandle.dense(a_host)
+    assert hh._host.ctypes.data == a_host.ctypes.data  # no copy: the H2D copy reads pinned memory
+    engine.iterative_cur(hh, **run_cfg)  # warm
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(1, args.steps)):
+        fe = te = None
+        t0 = time.perf_counter()
+        fe, te = engine.iterative_cur(hh, **run_cfg)
+        _ = (fe.row_indices, fe.col_indices, te.rhos)  # already on the host
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    d2h = 8 * 2 * fe.rank + 8 * len(te.rhos)
+    e2e = {"value": world * m * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
+           "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s}
+    del fe, te, hh
+    return e2e
+
+
 def sketch_kernel_name(sketch, c):
     """The sketch-apply kernel the engine runs for this sketch kind (csrc/engine.cu sparse_sketch_mode)."""
     if sketch != "sparse_sign":
@@ -254,15 +302,22 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     # e2e: each rank's shard from pinned host memory, H2D inside the timed region
-    host = torch.empty(shard.shape[1], shard.shape[0], dtype=torch.float64, pin_memory=True)
-    host.copy_(shard.t())
-    t0 = time.perf_counter()
-    for _ in range(max(1, args.steps)):
-        dshard = host.to("cuda", non_blocking=True).t()
-        r2 = iterative_cur_sharded(dshard, lo, n, **run)
-        _ = (r2.row_indices, r2.col_indices)
-    torch.cuda.synchronize()
-    e2e_ms = 1e3 * (time.perf_counter() - t0) / max(1, args.steps)
+    fits, why = e2e_fits(8 * shard.shape[0] * shard.shape[1])
+    fits_t = torch.tensor([1.0 if fits else 0.0], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(fits_t, op=torch.distributed.ReduceOp.MIN)
+    e2e_ms = float("nan")
+    if fits_t.item() > 0:
+        host = torch.empty(shard.shape[1], shard.shape[0], dtype=torch.float64, pin_memory=True)
+        host.copy_(shard.t())
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            dshard = host.to("cuda", non_blocking=True).t()
+            r2 = iterative_cur_sharded(dshard, lo, n, **run)
+            _ = (r2.row_indices, r2.col_indices)
+        torch.cuda.synchronize()
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / max(1, args.steps)
+        del host
     if world > 1:
         tt = torch.tensor([ms, e2e_ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -273,8 +328,11 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
                 "config": {**cfg_line, "parallelism": f"column-sharded x{world}",
                            "column_exchange": args.exchange},
-                "e2e": {"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
-                        "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms},
+                "e2e": ({"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
+                         "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms}
+                        if e2e_ms == e2e_ms else
+                        {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                         "skipped": why or "a rank's shard does not fit the e2e leg"}),
                 "clocks": clk.summary(),
                 "run": {"status": res.status, "rank": res.rank, "iterations": len(res.rhos),
                         "exchanges_per_run": res.exchanges}}
@@ -379,25 +437,11 @@ def main():
     value = world * m * n / (ms * 1e-3)
 
     # ---- e2e through the public API with a pinned host matrix ----
-    a_host_t = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
-    a_host_t.copy_(a.t())
-    a_host = a_host_t.numpy().T  # (m, n) Fortran-ordered view of pinned memory
-    hh = engine.MatrixHandle.dense(a_host)
-    assert hh._host.ctypes.data == a_host.ctypes.data  # no copy: the H2D copy reads pinned memory
-    engine.iterative_cur(hh, **run_cfg)  # warm
-    torch.cuda.synchronize()
-    e2e_t = []
-    for _ in range(max(1, args.steps)):
-        fe = te = None
-        t0 = time.perf_counter()
-        fe, te = engine.iterative_cur(hh, **run_cfg)
-        _ = (fe.row_indices, fe.col_indices, te.rhos)  # already on the host
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_s = sum(e2e_t) / len(e2e_t)
-    d2h = 8 * 2 * fe.rank + 8 * len(te.rhos)
-    e2e = {"value": world * m * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
-           "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s}
-    del fe, te, hh
+    ok, why = e2e_fits(8 * m * n)
+    if not ok:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0, "skipped": why}
+    else:
+        e2e = run_e2e(engine, a, m, n, run_cfg, args, world)
 
     # ---- roofline: the sketch-apply kernel alone (CUDA events on its stream) ----
     hbm, hbm_src = peaks()
@@ -428,8 +472,12 @@ def main():
             "run": {"status": status, "rank": rank_final, "iterations": n_iters, "phases_s": phases}}
 
     if rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_sample(np.asfortranarray(a.cpu().numpy()), {**cfg}, n_iters,
-                                                    budget_s=args.ref_budget)
+        if 8 * m * n <= 8e9:
+            line["cpu_baseline"] = cpu_reference_sample(np.asfortranarray(a.cpu().numpy()), {**cfg}, n_iters,
+                                                        budget_s=args.ref_budget)
+        else:  # the oracle's sketch alone exceeds the sample budget at this size
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                    "sample": "skipped: A exceeds 8 GB (configs 4/5); see configs 1-3"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_engine.py -x -q -k "matches_oracle" > gpurun_out/pytest_engine.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_engine.log
+ITERCUR_HOST_TRACE=1 python tools/time_runs.py --config 2 --runs 30 > gpurun_out/tr_trace.txt 2> gpurun_out/tr_trace.err
