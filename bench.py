@@ -91,7 +91,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-NCU_FULL = "profiles/ncu_full_r01_cfg2_v5.txt"  # the committed `ncu --set full` summary of this config
+NCU_FULL = "profiles/ncu_full_r01_cfg2_v6.txt"  # the committed `ncu --set full` summary of this config
 
 
 def e2e_fits(bytes_needed, device_copy=True):
