@@ -347,13 +347,7 @@ static SketchKernelFn kernel_for_nt(int nt, bool tma, int* smem, int* bm) {
     case 2: return pick_kernel<2>(tma, smem, bm);
     case 3: return pick_kernel<3>(tma, smem, bm);
     case 4: return pick_kernel<4>(tma, smem, bm);
-    case 5: {
-      // two m-tiles per warp (256 columns per CTA, 16-row stages): 5.96 vs 6.09 ms at config 3's
-      // 50000 x 50000, c = 35 (B fragments reused across both m-tiles); ITERCUR_SKETCH_MT2=0 for MT = 1
-      static const int v = getenv("ITERCUR_SKETCH_MT2") ? atoi(getenv("ITERCUR_SKETCH_MT2")) : 1;
-      if (v == 1) return pick_kernel<5, 2, 16>(tma, smem, bm);
-      return pick_kernel<5>(tma, smem, bm);
-    }
+    case 5: return pick_kernel<5>(tma, smem, bm);
     case 6: return pick_kernel<6>(tma, smem, bm);
     case 7: return pick_kernel<7>(tma, smem, bm);
     case 8: return pick_kernel<8>(tma, smem, bm);
