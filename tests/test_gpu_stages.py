@@ -128,6 +128,18 @@ def test_sparse_sign_integer_path_exact_on_integers(engine, oracle, monkeypatch,
     assert np.array_equal(y.cpu().numpy(), y_or)
 
 
+@pytest.mark.parametrize("mode", ["2", "3"])
+def test_sparse_sign_integer_paths_deterministic(engine, oracle, monkeypatch, mode):
+    """Repeated launches (persistent CTAs, K splits, exponent folds) give bitwise the same Y: no
+    race between the producer, the converters, the MMA issuer and the folds."""
+    monkeypatch.setenv("ITERCUR_SPARSE_SKETCH", mode)
+    S = _stages()
+    a = S.colmajor(oracle.random_gaussian(24000, 1500, 3) * (2.0 ** np.linspace(-8, 8, 24000))[:, None])
+    ys = [S.sketch(a, 50, 9, kind="sparse_sign")[0].cpu().numpy() for _ in range(6)]
+    for y in ys[1:]:
+        assert np.array_equal(y, ys[0])
+
+
 def test_sparse_sign_dense_and_sparse_paths_agree(engine, oracle, monkeypatch):
     S = _stages()
     a = S.colmajor(oracle.random_gaussian(600, 500, 5))
