@@ -1493,6 +1493,7 @@ static UmPlan plan_umma(int64_t m, int64_t n, int64_t c_pad) {
       s = t;
     }
   }
+  if (const char* e = getenv("ITERCUR_UMMA_SPLITS")) s = std::max<int64_t>(1, atoll(e));  // A/B
   s = std::max<int64_t>(s, ceil_div(p.ksteps, int64_t(1) << 17));
   p.kps = ceil_div(p.ksteps, s);
   p.splits = ceil_div(p.ksteps, p.kps);
