@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define ITERCUR_B200_ABI_VERSION 3
+#define ITERCUR_B200_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define ITERCUR_API __attribute__((visibility("default")))
@@ -73,6 +73,16 @@ enum itercur_run_status { ITERCUR_CONVERGED = 0, ITERCUR_MAX_RANK = 1, ITERCUR_R
 enum itercur_pivot_kind { ITERCUR_PIVOT_LUPP = 0, ITERCUR_PIVOT_QRCP = 1, ITERCUR_PIVOT_OSINSKY = 2 };
 enum itercur_sketch_kind { ITERCUR_SKETCH_GAUSSIAN = 0, ITERCUR_SKETCH_SPARSE_SIGN = 1 };
 
+struct itercur_run;
+struct itercur_iteration_record;
+/* IterationObserver (proj/include/itercur/driver.hpp:70-72, called at driver.cpp:154): invoked after
+   each completed iteration with the run as it stands (rank, indices, factors through the
+   itercur_run_* accessors) and that iteration's record. A nonzero return aborts the run with
+   ITERCUR_E_RUNTIME ("iteration observer failed"). With an observer the engine runs one iteration
+   per device batch (slow path; the reference uses it in tests). */
+typedef int (*itercur_observer_fn)(void* user, const struct itercur_run* run,
+                                   const struct itercur_iteration_record* record);
+
 /* StoppingConfig + the two SelectionMethods + seed + the new sketch options. */
 typedef struct itercur_config {
   double epsilon;      /* 1e-6  */
@@ -84,13 +94,21 @@ typedef struct itercur_config {
   int64_t max_iters;   /* 0 -> ceil(min(m, n) / b) + 1 */
   int32_t col_method;  /* ITERCUR_PIVOT_LUPP */
   int32_t row_method;  /* ITERCUR_PIVOT_LUPP */
-  double pivot_floor;  /* 1e-13 */
+  double pivot_floor;  /* 1e-13: col_method.pivot_floor (select.hpp:12-15) */
   uint64_t seed;       /* 0 */
   int32_t sketch_kind; /* ITERCUR_SKETCH_GAUSSIAN (the reference's only kind) */
   int32_t sparse_nnz;  /* 8 */
   int32_t profile;     /* 1: record per-phase CUDA-event times into the trace */
   int32_t sketch_stream; /* 0 -> RngStream::Sketch (1); 2 = SluppSketch (the s-LUPP baseline) */
   int64_t sketch_rows;   /* 0 -> floor(1.1 b) (sketch.hpp:10); > 0 overrides (s-LUPP: ceil(1.1 r)) */
+  /* ABI 4 */
+  double row_pivot_floor;        /* 1e-13: row_method.pivot_floor; <= 0 -> pivot_floor */
+  itercur_observer_fn observer;  /* NULL: none */
+  void* observer_user;           /* passed back to observer */
+  int32_t keep_device_copy;      /* host entry: 1 keeps the device copy of A alive with the run (the
+                                    accessors and the run-matrix error / sketched residual then use it);
+                                    0 (default) frees it when the call returns, keeping only compact
+                                    gathers of C = A(:,J) and R = A(I,:) */
 } itercur_config;
 
 /* One IterationRecord (proj/include/itercur/driver.hpp:32-44) plus pivot-margin data. */
@@ -155,9 +173,29 @@ ITERCUR_API int itercur_run_r_matrix(const itercur_run* run, double* out);
 ITERCUR_API int itercur_run_core_matrix(const itercur_run* run, double* out);
 /* ||A - CUR||_F / ||A||_F evaluated on the device over column panels. */
 ITERCUR_API int itercur_true_relative_error_device(const itercur_run* run, double* out);
+/* true_relative_error(A, factors) (proj/src/driver.cpp:169-190) for a GIVEN matrix A (m x n, the
+   run's shape; ld lda) and the run's factors: ||A - C core R||_F / ||A||_F. a_on_device = 1: dA is a
+   device pointer; 0: a host buffer streamed to the device in column panels. */
+ITERCUR_API int itercur_true_relative_error_matrix(const itercur_run* run, const double* A, int64_t m, int64_t n,
+                                                   int64_t lda, int32_t a_on_device, double* out);
+/* FactoredPinv::solve / solve_transposed (proj/include/itercur/pinv.hpp:27-33) of the run's core:
+   out = X^{-1} rhs (transposed = 0) or X^{-T} rhs (1), X = A(I, J) (r x r), rhs r x k (ld ldr),
+   out r x k (ld ldo); host buffers, computed on the device from the block-LU factors. */
+ITERCUR_API int itercur_run_core_apply(const itercur_run* run, int32_t transposed, const double* rhs, int64_t k,
+                                       int64_t ldr, double* out, int64_t ldo);
 /* make_sketch(seed, b, A) then downdate_col_residual(estimator, factors) for the run's factors
  * (proj/src/sketch.cpp:10-41; used by run_threshold, proj/src/bench.cpp:171-174, to score the
  * s-LUPP baseline with the adaptive run's estimator): out = ||GA - GA(:,J) X^{-1} R||_F / ||GA||_F. */
+/* The same for a given device matrix dA (the run's shape, ld lda) — for host-entry runs that no
+   longer hold A. */
+ITERCUR_API int itercur_sketched_residual_matrix(const itercur_run* run, const double* dA, int64_t lda, int64_t b,
+                                                 uint64_t seed, int32_t kind, int32_t sparse_nnz, double* out);
+/* 1 when the run still references a device copy of its input (device entry, or host entry with
+   keep_device_copy), else 0. */
+ITERCUR_API int32_t itercur_run_holds_matrix(const itercur_run* run);
+/* Copy `bytes` from device memory to host memory on the current device (plumbing for bindings
+   that do not link the CUDA runtime themselves, e.g. the C++ facade's MatrixHandle::device). */
+ITERCUR_API int itercur_copy_to_host(void* dst, const void* d_src, uint64_t bytes);
 /* ||A||_F of a device matrix (proj/src/matrix.cpp:297-302 fro_norm), fixed-order reduction. */
 ITERCUR_API int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda, void* stream, double* out);
 ITERCUR_API int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind,

@@ -189,8 +189,9 @@ double uniform_at(std::uint64_t seed, std::uint32_t stream, Index i, Index j) {
 // rng.cpp:61-67
 Mat gaussian_matrix(Index rows, Index cols, std::uint64_t seed, std::uint32_t stream) {
   Mat out(rows, cols);
-  for (Index j = 0; j < cols; ++j)
+  parallel_for(0, cols, rows * cols > 65536, [&](Index j) {  // entries are independent of fill order
     for (Index i = 0; i < rows; ++i) out(i, j) = normal_at(seed, stream, i, j);
+  });
   return out;
 }
 
@@ -433,8 +434,9 @@ Mat gather_rows(const View& a, const IndexList& rows) {  // matrix.cpp:196-206
   for (Index i : rows)
     if (i < 0 || i >= a.rows) bad_index("gather_rows", i, a.rows);
   Mat out(static_cast<Index>(rows.size()), a.cols);
-  for (Index j = 0; j < a.cols; ++j)
+  parallel_for(0, a.cols, a.cols * static_cast<Index>(rows.size()) > 65536, [&](Index j) {
     for (size_t k = 0; k < rows.size(); ++k) out(static_cast<Index>(k), j) = a(rows[k], j);
+  });
   return out;
 }
 View view(const Mat& m) { return View{m.v.data(), m.rows, m.cols, m.rows}; }
@@ -494,6 +496,29 @@ Mat apply_pinv_right(const FactoredPinv& p, const Mat& m) { return transpose(p.c
 // ---------------------------------------------------------------------------------
 inline Index sketch_rows_for_block(Index b) { return (11 * b) / 10; }  // sketch.hpp:10
 
+// ||A||_F^2 as per-column partial sums added in column order (threads split the columns, so the
+// value does not depend on the thread count); optionally the MatrixHandle finite check
+// (matrix.cpp:73-77).
+double column_sumsq(const View& a, bool check_finite) {
+  std::vector<double> part(static_cast<size_t>(std::max<Index>(a.cols, 0)), 0.0);
+  std::atomic<bool> bad{false};
+  parallel_for(0, a.cols, a.cols * a.rows > 65536, [&](Index j) {
+    const double* aj = a.p + j * a.ld;
+    double s = 0.0;
+    bool fin = true;
+    for (Index i = 0; i < a.rows; ++i) {
+      fin &= std::isfinite(aj[i]);
+      s += aj[i] * aj[i];
+    }
+    if (check_finite && !fin) bad.store(true);
+    part[static_cast<size_t>(j)] = s;
+  });
+  if (bad.load()) throw std::invalid_argument("matrix contains non-finite entries");
+  double asq = 0.0;
+  for (double v : part) asq += v;
+  return asq;
+}
+
 struct SketchState {  // sketch.hpp:19-27
   Mat sketched_input;  // S*A (c x n)
   Mat col_residual;    // Y
@@ -516,8 +541,7 @@ SketchState make_sketch(std::uint64_t seed, Index b, const View& a, int kind, in
   double asq = 0.0;
   if (kind == ORACLE_SKETCH_GAUSSIAN) {
     const Mat g = gaussian_matrix(c, m, seed, ORACLE_STREAM_SKETCH);  // sketch.cpp:19
-    for (Index j = 0; j < n; ++j)  // ||A||^2: one running sum in column order (as before threading)
-      for (Index k = 0; k < m; ++k) asq += a.p[j * a.ld + k] * a.p[j * a.ld + k];
+    asq = column_sumsq(a, false);
     parallel_for(0, n, n * m * c > 65536, [&](Index j) {  // sketch.cpp:20 (G*A)
       double* y = st.sketched_input.col(j);
       const double* aj = a.p + j * a.ld;
@@ -535,8 +559,7 @@ SketchState make_sketch(std::uint64_t seed, Index b, const View& a, int kind, in
     for (Index i = 0; i < m; ++i)
       sparse_sign_column(seed, i, c, zeta_eff, rows.data() + i * zeta_eff, signs.data() + i * zeta_eff);
     const double scale = 1.0 / std::sqrt(static_cast<double>(zeta_eff));
-    for (Index j = 0; j < n; ++j)  // ||A||^2: one running sum in column order (as before threading)
-      for (Index i = 0; i < m; ++i) asq += a.p[j * a.ld + i] * a.p[j * a.ld + i];
+    asq = column_sumsq(a, false);
     parallel_for(0, n, n * m > 65536, [&](Index j) {
       double* y = st.sketched_input.col(j);
       const double* aj = a.p + j * a.ld;
@@ -778,14 +801,8 @@ void log_steps(oracle_result* res, int kind, Index k, const SelectionResult& sel
 void iterative_cur(const View& a, const oracle_config& cfg, oracle_result* res) {
   // MatrixHandle construction rejects non-finite entries (matrix.cpp:73-77); then the
   // driver's validation order (driver.cpp:51-54).
-  double asq = 0.0;
-  for (Index j = 0; j < a.cols; ++j) {
-    const double* aj = a.p + j * a.ld;
-    for (Index i = 0; i < a.rows; ++i) {
-      if (!std::isfinite(aj[i])) throw std::invalid_argument("matrix contains non-finite entries");
-      asq += aj[i] * aj[i];
-    }
-  }
+  // (per-column partial sums, added in column order: the same value for any thread count)
+  const double asq = column_sumsq(a, /*check_finite=*/true);
   if (a.rows == 0 || a.cols == 0) throw std::invalid_argument("matrix must be nonempty");
   if (std::sqrt(asq) == 0.0) throw std::invalid_argument("matrix must be nonzero");
   if (cfg.epsilon < 0.0) throw std::invalid_argument("epsilon must be nonnegative");
@@ -842,6 +859,7 @@ void iterative_cur(const View& a, const oracle_config& cfg, oracle_result* res) 
     cur = std::move(next);
     rho = downdate_col_residual(st, cur);
     if (k < res->cap_iters) {
+      if (res->cod_rank) res->cod_rank[k] = cur.core.cod.rank;
       res->rhos[k] = rho;
       res->widths[k] = static_cast<Index>(width);
       if (res->iter_seconds) res->iter_seconds[k] = seconds_since(it_start);
@@ -928,8 +946,15 @@ double oracle_uniform_at(uint64_t seed, uint32_t stream, int64_t i, int64_t j) {
   return oracle::uniform_at(seed, stream, i, j);
 }
 void oracle_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream, double* out) {
-  for (int64_t j = 0; j < cols; ++j)
+  oracle::parallel_for(0, cols, rows * cols > 65536, [&](int64_t j) {
     for (int64_t i = 0; i < rows; ++i) out[i + j * rows] = oracle::normal_at(seed, stream, i, j);
+  });
+}
+void oracle_gaussian_fill(int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint32_t stream, double scale,
+                          double* out) {
+  oracle::parallel_for(0, cols, rows * cols > 65536, [&](int64_t j) {
+    for (int64_t i = 0; i < rows; ++i) out[i + j * ld] = scale * oracle::normal_at(seed, stream, i, j);
+  });
 }
 int oracle_sparse_sign_pattern(int64_t c, int64_t m, uint64_t seed, int32_t zeta, int32_t* rows_out,
                                int8_t* signs_out) {
@@ -1008,6 +1033,28 @@ int oracle_core_matrix(const double* A, int64_t m, int64_t n, int64_t lda, const
     for (int64_t i = 0; i < r; ++i) eye(i, i) = 1.0;
     const oracle::Mat p = cur.core.cod.solve(eye);  // FactoredPinv::materialize, pinv.cpp:40-43
     std::memcpy(core_out, p.v.data(), sizeof(double) * p.v.size());
+  });
+}
+
+int oracle_core_solve(const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I, const int64_t* J,
+                      int64_t r, const double* rhs, int64_t k, int64_t ldrhs, double* out) {
+  return guarded([&] {
+    const oracle::View a{A, m, n, lda};
+    const auto Il = to_list(I, r), Jl = to_list(J, r);
+    oracle::check_distinct(Il, "row");
+    oracle::check_distinct(Jl, "column");
+    oracle::Mat cross(r, r);  // gather_block, matrix.cpp:224-227
+    for (int64_t q = 0; q < r; ++q)
+      for (int64_t p = 0; p < r; ++p) {
+        if (Il[p] < 0 || Il[p] >= m) oracle::bad_index("gather_rows", Il[p], m);
+        if (Jl[q] < 0 || Jl[q] >= n) oracle::bad_index("gather_cols", Jl[q], n);
+        cross(p, q) = a(Il[p], Jl[q]);
+      }
+    const oracle::FactoredPinv core = oracle::build_pinv(cross);
+    oracle::Mat b(r, k);
+    for (int64_t j = 0; j < k; ++j) std::memcpy(b.col(j), rhs + j * ldrhs, sizeof(double) * r);
+    const oracle::Mat x = oracle::apply_pinv_left(core, b);
+    std::memcpy(out, x.v.data(), sizeof(double) * x.v.size());
   });
 }
 

@@ -85,6 +85,9 @@ typedef struct {
   double ga_norm;
   int64_t c;
   char note[128];
+  /* per iteration: numerical rank of the COD of the cross block A(I,J) (threshold
+     1e-12 * r, proj/src/pinv.cpp:54-60); < rank means the reference's core truncated (may be NULL) */
+  int64_t* cod_rank;
 } oracle_result;
 
 const char* oracle_last_error(void);
@@ -94,6 +97,9 @@ void oracle_philox4x32(const uint32_t* ctr, const uint32_t* key, uint32_t* out);
 double oracle_normal_at(uint64_t seed, uint32_t stream, int64_t i, int64_t j);
 double oracle_uniform_at(uint64_t seed, uint32_t stream, int64_t i, int64_t j);
 void oracle_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream, double* out);
+/* out(i, j) = scale * normal_at(seed, stream, i, j) + out(i, j) * keep  (col-major, ld = rows; threaded) */
+void oracle_gaussian_fill(int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint32_t stream, double scale,
+                          double* out);
 
 /* sparse-sign stream (new): rows_out[i*zeta+t] = h_t(i), signs_out[i*zeta+t] = +-1 */
 int oracle_sparse_sign_pattern(int64_t c, int64_t m, uint64_t seed, int32_t zeta, int32_t* rows_out,
@@ -120,6 +126,11 @@ int oracle_true_relative_error(const double* A, int64_t m, int64_t n, int64_t ld
 /* core_out = A(I,J)^+ (r x r column-major), via the COD restatement (proj/src/pinv.cpp:40-65) */
 int oracle_core_matrix(const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I,
                        const int64_t* J, int64_t r, double* core_out);
+
+/* out = A(I,J)^+ * rhs (r x k, ld r) by the COD's minimum-norm solve (FactoredPinv::solve,
+   proj/src/pinv.cpp:24-31) — what true_relative_error applies to R's panels (driver.cpp:183-185) */
+int oracle_core_solve(const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I, const int64_t* J,
+                      int64_t r, const double* rhs, int64_t k, int64_t ldrhs, double* out);
 
 /* one-shot s-LUPP CUR baseline (proj/src/baselines.cpp:39-62): I, J (length *rank <= r) */
 int oracle_slupp_cur(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r, uint64_t seed, int64_t* I,

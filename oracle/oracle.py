@@ -47,6 +47,7 @@ class _Result(C.Structure):
         ("rank", C.c_int64), ("n_iters", C.c_int64), ("n_steps", C.c_int64), ("status", C.c_int32),
         ("final_rho", C.c_double), ("threshold", C.c_double), ("sketch_s", C.c_double), ("total_s", C.c_double),
         ("ga_norm", C.c_double), ("c", C.c_int64), ("note", C.c_char * 128),
+        ("cod_rank", C.POINTER(C.c_int64)),
     ]
 
 
@@ -75,6 +76,7 @@ def lib() -> C.CDLL:
         L.oracle_uniform_at.restype = C.c_double
         L.oracle_uniform_at.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64]
         L.oracle_gaussian_matrix.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint32, dp]
+        L.oracle_gaussian_fill.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32, C.c_double, dp]
         L.oracle_philox4x32.argtypes = [C.POINTER(C.c_uint32)] * 3
         L.oracle_sparse_sign_pattern.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
                                                  C.POINTER(C.c_int32), C.POINTER(C.c_int8)]
@@ -90,6 +92,8 @@ def lib() -> C.CDLL:
                                            C.POINTER(_Result)]
         L.oracle_true_relative_error.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, i64p, i64p, C.c_int64, dp]
         L.oracle_core_matrix.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, i64p, i64p, C.c_int64, dp]
+        L.oracle_core_solve.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, i64p, i64p, C.c_int64, dp, C.c_int64,
+                                        C.c_int64, dp]
         L.oracle_slupp_cur.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, i64p, i64p,
                                        C.POINTER(C.c_int64)]
         L.oracle_fixture_random_dense.argtypes = [C.c_int64, C.c_int64, C.c_uint32, C.c_double, C.c_double, dp]
@@ -160,6 +164,13 @@ def gaussian_matrix(rows, cols, seed, stream=STREAM_SKETCH) -> np.ndarray:
     out = np.empty((rows, cols), dtype=np.float64, order="F")
     lib().oracle_gaussian_matrix(rows, cols, seed, stream, _dp(out))
     return out
+
+
+def gaussian_fill(out: np.ndarray, seed, stream, scale=1.0) -> None:
+    """out(i, j) = scale * normal_at(seed, stream, i, j) in place (Fortran-ordered float64; threaded)."""
+    assert out.dtype == np.float64 and out.flags.f_contiguous and out.ndim == 2
+    rows, cols = out.shape
+    lib().oracle_gaussian_fill(rows, cols, max(rows, 1), seed, stream, scale, _dp(out))
 
 
 def sparse_sign_pattern(c, m, seed, zeta=8):
@@ -252,6 +263,7 @@ class OracleRun:
     c: int
     steps: list  # (kind, iteration, index, best, second)
     iter_seconds: list = field(default_factory=list)
+    cod_ranks: list = field(default_factory=list)  # per iteration: numerical rank of the core's COD
 
     @property
     def rank(self) -> int:
@@ -283,6 +295,8 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     res.cap_rank, res.row_indices, res.col_indices = cap_rank, _i64p(I), _i64p(J)
     res.cap_iters, res.rhos, res.widths = cap_iters, _dp(rhos), _i64p(widths)
     res.iter_seconds = _dp(iter_s)
+    cod = np.zeros(cap_iters, dtype=np.int64)
+    res.cod_rank = _i64p(cod)
     res.cap_steps = cap_steps
     res.step_kind = sk.ctypes.data_as(C.POINTER(C.c_int32))
     res.step_iter, res.step_index, res.step_best, res.step_second = _i64p(si), _i64p(sx), _dp(sb), _dp(ss)
@@ -292,7 +306,8 @@ def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=Fals
     steps = [(int(sk[q]), int(si[q]), int(sx[q]), float(sb[q]), float(ss[q])) for q in range(nst)]
     return OracleRun([int(v) for v in I[:r]], [int(v) for v in J[:r]], STATUS_NAMES[res.status], res.final_rho,
                      res.threshold, list(rhos[:k]), [int(v) for v in widths[:k]], res.note.decode(),
-                     res.sketch_s, res.total_s, res.ga_norm, res.c, steps, list(iter_s[:k]))
+                     res.sketch_s, res.total_s, res.ga_norm, res.c, steps, list(iter_s[:k]),
+                     [int(v) for v in cod[:k]])
 
 
 def slupp_cur(a, rank, seed=0):
@@ -325,4 +340,18 @@ def core_matrix(a, row_indices, col_indices) -> np.ndarray:
     r = len(I)
     out = np.zeros((r, r), dtype=np.float64, order="F")
     _check(lib().oracle_core_matrix(_dp(a), m, n, max(m, 1), _i64p(I), _i64p(J), r, _dp(out)))
+    return out
+
+
+def core_solve(a, row_indices, col_indices, rhs) -> np.ndarray:
+    """A(I,J)^+ @ rhs by the oracle's COD minimum-norm solve (proj/src/pinv.cpp:24-31)."""
+    a = _colmajor(a)
+    m, n = a.shape
+    I = np.asarray(row_indices, dtype=np.int64)
+    J = np.asarray(col_indices, dtype=np.int64)
+    rhs = _colmajor(rhs)
+    r, k = rhs.shape
+    assert r == len(I) == len(J)
+    out = np.zeros((r, k), dtype=np.float64, order="F")
+    _check(lib().oracle_core_solve(_dp(a), m, n, max(m, 1), _i64p(I), _i64p(J), r, _dp(rhs), k, max(r, 1), _dp(out)))
     return out

@@ -105,7 +105,7 @@ class MatrixHandle:
         a = np.asfortranarray(np.asarray(array, dtype=np.float64))
         if a.ndim != 2:
             raise ValueError("dense matrix must be two-dimensional")
-        if not np.all(np.isfinite(a)):
+        if not _all_finite(a):
             raise ValueError("matrix contains non-finite entries")
         return MatrixHandle(host=a)
 
@@ -169,6 +169,18 @@ class MatrixHandle:
         return f"<MatrixHandle {self.rows}x{self.cols} dense{' device' if self.is_device else ''}>"
 
 
+def _all_finite(a: np.ndarray) -> bool:
+    """MatrixHandle's finite check (proj/src/matrix.cpp:73-77) over column panels with torch's
+    multi-threaded CPU kernels (no matrix-sized temporary; ~GB/s per core)."""
+    if a.size == 0:
+        return True
+    import torch
+
+    t = torch.from_numpy(a.T if a.flags.f_contiguous else np.ascontiguousarray(a).T)  # (n, m) row-major view
+    step = max(1, (1 << 27) // max(a.shape[0], 1))
+    return all(bool(torch.isfinite(t[j:j + step]).all()) for j in range(0, t.shape[0], step))
+
+
 def _as_handle(a) -> MatrixHandle:
     if isinstance(a, MatrixHandle):
         return a._densified_on_device() if a.is_sparse else a
@@ -179,6 +191,10 @@ def _as_handle(a) -> MatrixHandle:
             return MatrixHandle.device(a)
     except ImportError:  # pragma: no cover
         pass
+    if hasattr(a, "to_numpy") and hasattr(a, "is_sparse") and not isinstance(a, np.ndarray):
+        # a handle of the reference's own binding (module.cpp:36-57: rows / cols / is_sparse /
+        # to_numpy): its dense copy is the matrix (CSR handles densify, as to_dense() does)
+        return MatrixHandle.dense(a.to_numpy())
     return MatrixHandle.dense(a)
 
 
@@ -269,7 +285,7 @@ class RunTrace:
 
 
 def _config(epsilon, b, delta, alpha, risk_adjust, max_rank, max_iters, col_method, row_method, pivot_floor, seed,
-            sketch, sparse_nnz, profile) -> _capi.Config:
+            sketch, sparse_nnz, profile, row_pivot_floor=None) -> _capi.Config:
     cfg = _capi.Config()
     _lib().itercur_config_default(C.byref(cfg))
     for name, m in (("col_method", col_method), ("row_method", row_method)):
@@ -281,7 +297,9 @@ def _config(epsilon, b, delta, alpha, risk_adjust, max_rank, max_iters, col_meth
     cfg.risk_adjust = 1 if risk_adjust else 0
     cfg.max_rank, cfg.max_iters = int(max_rank), int(max_iters)
     cfg.col_method, cfg.row_method = _METHODS[col_method], _METHODS[row_method]
+    # module.cpp:95-96 builds both SelectionMethods with the one pivot_floor; the C-ABI keeps one per method
     cfg.pivot_floor, cfg.seed = float(pivot_floor), int(seed)
+    cfg.row_pivot_floor = float(pivot_floor if row_pivot_floor is None else row_pivot_floor)
     cfg.sketch_kind, cfg.sparse_nnz = _SKETCHES[sketch], int(sparse_nnz)
     cfg.profile = 1 if profile else 0
     return cfg
@@ -319,16 +337,92 @@ def _collect(run_ptr, keepalive):
     return factors, trace
 
 
+class _ObservedFactors:
+    """The factors as they stand after one iteration, handed to an ``observer`` (IterationObserver,
+    proj/include/itercur/driver.hpp:70-72). Valid only during the callback: the run continues
+    afterwards, so c_matrix / r_matrix / core_matrix raise once it returns."""
+
+    def __init__(self, run_ptr):
+        self._ptr = run_ptr
+        self.live = True
+        L = _lib()
+        r = L.itercur_run_rank(run_ptr)
+        I = np.zeros(max(r, 1), dtype=np.int64)
+        J = np.zeros(max(r, 1), dtype=np.int64)
+        _check(L.itercur_run_indices(run_ptr, I.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     J.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.row_indices = [int(v) for v in I[:r]]
+        self.col_indices = [int(v) for v in J[:r]]
+
+    @property
+    def rank(self) -> int:
+        return len(self.col_indices)
+
+    def _mat(self, fn, shape):
+        if not self.live:
+            raise RuntimeError("observed factors are only valid during the observer callback")
+        out = np.zeros(shape, dtype=np.float64, order="F")
+        if self.rank:
+            _check(fn(self._ptr, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def c_matrix(self):
+        return self._mat(_lib().itercur_run_c_matrix, (_lib().itercur_run_rows(self._ptr), self.rank))
+
+    def r_matrix(self):
+        return self._mat(_lib().itercur_run_r_matrix, (self.rank, _lib().itercur_run_cols(self._ptr)))
+
+    def core_matrix(self):
+        return self._mat(_lib().itercur_run_core_matrix, (self.rank, self.rank))
+
+
+def _observer_trampoline(observer, errors):
+    def cb(_user, run_ptr, rec_ptr):
+        snap = None
+        try:
+            x = C.cast(rec_ptr, C.POINTER(_capi.IterationRecord)).contents
+            rec = IterationRecord(int(x.k), x.rho, int(x.cols_added), int(x.rows_added), bool(x.col_truncated),
+                                  bool(x.row_truncated), x.select_cols_s, x.row_residual_s, x.select_rows_s,
+                                  x.core_s, x.downdate_s, x.min_col_margin, x.min_row_margin)
+            snap = _ObservedFactors(run_ptr)
+            observer(snap, rec)
+            return 0
+        except BaseException as e:  # re-raised by iterative_cur after the engine unwinds
+            errors.append(e)
+            return 1
+        finally:
+            if snap is not None:
+                snap.live = False
+    return _capi.OBSERVER_FN(cb)
+
+
 def iterative_cur(a, epsilon=1e-6, b=50, delta=0.0, alpha=0.05, risk_adjust=False, max_rank=0, max_iters=0,
                   col_method="lupp", row_method="lupp", pivot_floor=1e-13, seed=0, sketch="gaussian",
-                  sparse_nnz=8, profile=False):
+                  sparse_nnz=8, profile=False, observer=None, row_pivot_floor=None):
     """Run the rank-adaptive decomposition; returns (factors, trace).
 
     proj/bindings/python/module.cpp:82-103 -> itercur::iterative_cur, proj/src/driver.cpp:48-167.
+    Extensions: ``sketch`` / ``sparse_nnz`` (sparse-sign sketch), ``observer(factors, record)``
+    called after every iteration (the C++ API's IterationObserver, driver.hpp:70-72; the Python
+    binding does not expose it), ``row_pivot_floor`` (the row SelectionMethod's floor; default:
+    ``pivot_floor`` for both, as module.cpp:95-96).
     """
     h = _as_handle(a)
     cfg = _config(epsilon, b, delta, alpha, risk_adjust, max_rank, max_iters, col_method, row_method, pivot_floor,
-                  seed, sketch, sparse_nnz, profile)
+                  seed, sketch, sparse_nnz, profile, row_pivot_floor)
+    errors = []
+    if observer is not None:
+        cb = _observer_trampoline(observer, errors)
+        cfg.observer = C.cast(cb, C.c_void_p)
+    try:
+        return _run(h, cfg)
+    except RuntimeError:
+        if errors:
+            raise errors[0]
+        raise
+
+
+def _run(h, cfg):
     L = _lib()
     out = C.c_void_p()
     if h.is_device:
@@ -361,35 +455,29 @@ def slupp_cur(a, rank, seed=0) -> CurFactors:
     cfg = _config(0.0, r, 0.0, 0.05, False, r, 1, "lupp", "lupp", 1e-13, seed, "gaussian", 8, False)
     cfg.sketch_stream = 2
     cfg.sketch_rows = (11 * r + 9) // 10
-    L = _lib()
-    out = C.c_void_p()
-    if h.is_device:
-        import torch
-
-        t = h._tensor
-        with torch.cuda.device(t.device):
-            stream = torch.cuda.current_stream(t.device).cuda_stream
-            _check(L.itercur_iterative_cur_device(C.c_void_p(t.data_ptr()), h.rows, h.cols, h.lda, C.byref(cfg),
-                                                  C.c_void_p(stream), C.byref(out)))
-        factors, trace = _collect(out.value, h)
-    else:
-        host = h._host
-        _check(L.itercur_iterative_cur_host(host.ctypes.data_as(C.c_void_p), h.rows, h.cols, max(h.rows, 1),
-                                            C.byref(cfg), C.byref(out)))
-        factors, trace = _collect(out.value, None)
+    factors, _ = _run(h, cfg)
     if factors.rank == 0:
         raise RuntimeError("singular cross block")
     return factors
 
 
 def true_relative_error(a, factors: CurFactors) -> float:
-    """||A - CUR||_F / ||A||_F (proj/src/driver.cpp:169-190), evaluated on the device from the
-    run's factors (A is the matrix the factors were computed from)."""
+    """||A - C core R||_F / ||A||_F (proj/src/driver.cpp:169-190) for the GIVEN matrix `a` and the
+    run's factors, on the device over column panels (a host `a` is streamed through the device)."""
+    h = _as_handle(a)
     if factors.rank == 0 or factors._run is None:
-        h = _as_handle(a)
         return 0.0 if h.fro_norm() == 0.0 else 1.0
     out = C.c_double()
-    _check(_lib().itercur_true_relative_error_device(factors._run.ptr, C.byref(out)))
+    if h.is_device:
+        import torch
+
+        t = h._tensor
+        with torch.cuda.device(t.device):
+            _check(_lib().itercur_true_relative_error_matrix(factors._run.ptr, C.c_void_p(t.data_ptr()), h.rows,
+                                                             h.cols, h.lda, 1, C.byref(out)))
+    else:
+        _check(_lib().itercur_true_relative_error_matrix(factors._run.ptr, h._host.ctypes.data_as(C.c_void_p),
+                                                         h.rows, h.cols, max(h.rows, 1), 0, C.byref(out)))
     return out.value
 
 
@@ -410,8 +498,20 @@ def sketched_relative_error(a, factors: CurFactors, b: int, seed: int = 0, sketc
     if sketch not in _SKETCHES:
         raise ValueError(f"unknown sketch '{sketch}'")
     out = C.c_double()
-    _check(_lib().itercur_sketched_residual_device(factors._run.ptr, int(b), int(seed), _SKETCHES[sketch],
-                                                   int(sparse_nnz), C.byref(out)))
+    L = _lib()
+    if L.itercur_run_holds_matrix(factors._run.ptr):
+        _check(L.itercur_sketched_residual_device(factors._run.ptr, int(b), int(seed), _SKETCHES[sketch],
+                                                  int(sparse_nnz), C.byref(out)))
+        return out.value
+    # host-entry run (its device copy of A was released): the given matrix, on the device
+    import torch
+
+    h = _as_handle(a)
+    t = h._tensor if h.is_device else torch.from_numpy(np.ascontiguousarray(h._host.T)).cuda().t()
+    lda = int(t.stride(1)) if t.shape[1] > 1 else max(int(t.shape[0]), 1)
+    with torch.cuda.device(t.device):
+        _check(L.itercur_sketched_residual_matrix(factors._run.ptr, C.c_void_p(t.data_ptr()), lda, int(b), int(seed),
+                                                  _SKETCHES[sketch], int(sparse_nnz), C.byref(out)))
     return out.value
 
 

@@ -31,6 +31,8 @@ EXPORTED = [
     "itercur_time_sketch_kernel", "itercur_time_lupp", "itercur_time_gemm",
     "itercur_lupp_dist_step", "itercur_gemm_device", "itercur_block_lu_device", "itercur_rows_lu_solve_device",
     "itercur_select_qrcp_device", "itercur_csr_to_dense_device",
+    "itercur_true_relative_error_matrix", "itercur_run_core_apply", "itercur_sketched_residual_matrix",
+    "itercur_run_holds_matrix", "itercur_copy_to_host",
 ]
 
 
@@ -41,7 +43,13 @@ class Config(C.Structure):
         ("col_method", C.c_int32), ("row_method", C.c_int32), ("pivot_floor", C.c_double),
         ("seed", C.c_uint64), ("sketch_kind", C.c_int32), ("sparse_nnz", C.c_int32),
         ("profile", C.c_int32), ("sketch_stream", C.c_int32), ("sketch_rows", C.c_int64),
+        ("row_pivot_floor", C.c_double), ("observer", C.c_void_p), ("observer_user", C.c_void_p),
+        ("keep_device_copy", C.c_int32),
     ]
+
+
+# int (*)(void* user, const itercur_run* run, const itercur_iteration_record* record)
+OBSERVER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 
 
 class IterationRecord(C.Structure):
@@ -95,6 +103,12 @@ def lib() -> C.CDLL:
         "itercur_run_r_matrix": (C.c_int, [runp, dp]),
         "itercur_run_core_matrix": (C.c_int, [runp, dp]),
         "itercur_true_relative_error_device": (C.c_int, [runp, dp]),
+        "itercur_true_relative_error_matrix": (C.c_int, [runp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, dp]),
+        "itercur_run_core_apply": (C.c_int, [runp, C.c_int32, vp, C.c_int64, C.c_int64, vp, C.c_int64]),
+        "itercur_sketched_residual_matrix": (C.c_int, [runp, vp, C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
+                                                       C.c_int32, dp]),
+        "itercur_run_holds_matrix": (C.c_int32, [runp]),
+        "itercur_copy_to_host": (C.c_int, [vp, vp, C.c_uint64]),
         "itercur_fro_norm_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, dp]),
         "itercur_sketched_residual_device": (C.c_int, [runp, C.c_int64, C.c_uint64, C.c_int32, C.c_int32, dp]),
         "itercur_run_free": (None, [runp]),

@@ -47,6 +47,24 @@ def _compile(src):
     return obj
 
 
+FACADE_SRC = os.path.join(HERE, "facade", "itercur_facade.cpp")
+FACADE_LIB = os.path.join(HERE, "libitercur_facade.so")
+CXX = os.environ.get("CXX", "g++")
+
+
+def build_facade() -> str:
+    """The C++ facade (include/itercur/driver_b200.hpp -> itercur::iterative_cur & co.) over the
+    C-ABI: g++, linked against libitercur_b200.so with an $ORIGIN rpath."""
+    deps = [FACADE_SRC, LIB, os.path.join(INCLUDE, "itercur_b200.h"), os.path.join(INCLUDE, "itercur", "driver_b200.hpp")]
+    if _stale(FACADE_LIB, deps):
+        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-shared", "-fvisibility=hidden", "-Wall", "-Wextra",
+               "-I" + INCLUDE, FACADE_SRC, "-L" + HERE, "-litercur_b200", "-Wl,-rpath,$ORIGIN", "-o", FACADE_LIB]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"facade build failed:\n{r.stdout}\n{r.stderr}")
+    return FACADE_LIB
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
@@ -57,6 +75,7 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_facade()
     if verbose:
         print(LIB)
     return LIB

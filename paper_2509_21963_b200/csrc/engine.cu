@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -81,10 +82,20 @@ thread_local cudaStream_t g_alloc_stream = nullptr;
 
 // The engine's own non-blocking work stream (one per host thread, never destroyed): the
 // iteration batches are captured into CUDA graphs, which the legacy default stream cannot do.
+// Streams are cached per host thread AND per device ordinal: a thread that runs on cuda:0 and
+// later on cuda:1 must not launch into (or allocate on) a stream of the first device.
+constexpr int kMaxDevices = 64;
+int current_device() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) fail(ITERCUR_E_CUDA, "device ordinal out of range");
+  return dev;
+}
 cudaStream_t work_stream() {
-  thread_local cudaStream_t s = nullptr;
-  if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  return s;
+  thread_local cudaStream_t s[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!s[dev]) CK(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
+  return s[dev];
 }
 
 // A second work stream for graph branches off the iteration's critical path, with its two events.
@@ -93,26 +104,27 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream() {
-  thread_local SideStream ss;
-  if (!ss.s) {
-    CK(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  thread_local SideStream ss[kMaxDevices];
+  SideStream& x = ss[current_device()];
+  if (!x.s) {
+    CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
   }
-  return ss;
+  return x;
 }
 
 void configure_mempool_once() {
-  static bool done = false;
-  if (done) return;
+  static std::atomic<bool> done[kMaxDevices] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return;
+  if (done[dev].load()) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done = true;
+  done[dev].store(true);
 }
 
 template <class T>
@@ -174,7 +186,8 @@ struct itercur_run {
   cudaStream_t wstream = nullptr;  // the engine's work stream for iterative_cur (capturable)
   int64_t m = 0, n = 0, lda = 0;
   const double* A = nullptr;
-  DevBuf<double> A_owned;  // host entry: device copy of A
+  DevBuf<double> A_owned;  // host entry: device copy of A (freed when the call returns unless kept)
+  DevBuf<double> Cg, RgT;  // host entry without the copy: C = A(:,J) (m x r), R^T = A(I,:)^T (n x r)
   itercur_config cfg{};
   int64_t c = 0, cp = 0;
   int64_t r = 0;
@@ -191,6 +204,7 @@ struct itercur_run {
   DevBuf<double> L;     // m x capL, column-major, ld ldL
   DevBuf<double> Rt;    // capL rows of n, row-major (Rt[q * ldR + j])
   DevBuf<double> Dinv;  // per block: LU of D_k (w x w, ld bmax) at offset start * bmax
+  DevBuf<int> Piv;      // QRCP rows only: D_k's partial-pivoting permutation at offset start
   DevBuf<int64_t> dI, dJ;
   int64_t ldL = 0, ldR = 0, capL = 0, bmax = 0;
   int64_t launches = 0;  // kernels of this library launched by the run (sketch + loop)
@@ -213,6 +227,10 @@ itercur_config default_config() {
   c.col_method = ITERCUR_PIVOT_LUPP;
   c.row_method = ITERCUR_PIVOT_LUPP;
   c.pivot_floor = 1e-13;
+  c.row_pivot_floor = 1e-13;
+  c.observer = nullptr;
+  c.observer_user = nullptr;
+  c.keep_device_copy = 0;
   c.seed = 0;
   c.sketch_kind = ITERCUR_SKETCH_GAUSSIAN;
   c.sparse_nnz = 8;
@@ -284,12 +302,23 @@ static int sparse_sketch_mode(int kind, int64_t c, int64_t cp, int zeta_eff, con
 static int zeta_effective(int kind, int sparse_nnz, int64_t c) {
   return kind == kSketchSparseSign ? static_cast<int>(std::min<int64_t>(std::max(sparse_nnz, 1), c)) : 0;
 }
+// The sparse-sign nonzeros per column: the oracle rejects zeta < 1 (itercur_oracle.cpp make_sketch);
+// the device kernels draw at most kMaxSparseNnz = 16 slots per column into fixed-size per-thread
+// arrays (sketch.cu sparse_sign_slots), so min(zeta, c) above 16 is rejected rather than overrun.
+constexpr int kMaxSparseNnz = 16;
+static void check_sparse_nnz(int kind, int sparse_nnz, int64_t c) {
+  if (kind != kSketchSparseSign) return;
+  if (sparse_nnz < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "sparse_nnz must be at least 1");
+  if (std::min<int64_t>(sparse_nnz, c) > kMaxSparseNnz)
+    fail(ITERCUR_E_INVALID_ARGUMENT, "sparse_nnz above 16 is not supported by the B200 engine");
+}
 // Y (cp x n, ld cp) = scale * S * A, ||A||^2 -> stats.d_asq, ||Y||^2 -> stats.d_ysq. Returns the
 // number of kernel launches.
 static int apply_sketch(const double* A, int64_t m, int64_t n, int64_t lda, int kind, int sparse_nnz, uint64_t seed,
                         uint32_t stream_tag, int64_t c, int64_t cp, double* Y, const SketchStats& stats,
                         SketchBuffers& buf, cudaStream_t st, SketchLaunchInfo* info = nullptr,
                         bool operator_ready = false) {
+  check_sparse_nnz(kind, sparse_nnz, c);
   const int ze = zeta_effective(kind, sparse_nnz, c);
   const double scale = kind == kSketchSparseSign ? 1.0 / std::sqrt(static_cast<double>(ze)) : 1.0;
   const int mode = sparse_sketch_mode(kind, c, cp, ze, A, lda);
@@ -409,7 +438,6 @@ void run_iterative_cur(itercur_run* run) {
     if (cfg.b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
     fail(ITERCUR_E_INVALID_ARGUMENT, "block exceeds row count");
   }
-  if (cfg.b > 180) fail(ITERCUR_E_INVALID_ARGUMENT, "block size above 180 is not supported by the B200 engine yet");
 
   const int64_t b = cfg.b;
   const int64_t min_dim = std::min(m, n);
@@ -476,8 +504,12 @@ void run_iterative_cur(itercur_run* run) {
     return;
   }
   // the reference validates the selection methods on the first select_* call
-  if (!(cfg.pivot_floor > 0.0 && cfg.pivot_floor < 1.0))
-    fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+  // per-method floors (SelectionMethod::pivot_floor, select.hpp:12-15); the column method is
+  // validated first, as select_columns runs before select_rows (select.cpp:24-28)
+  const double col_floor = cfg.pivot_floor;
+  const double row_floor = cfg.row_pivot_floor > 0.0 ? cfg.row_pivot_floor : cfg.pivot_floor;
+  if (!(col_floor > 0.0 && col_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+  if (!(row_floor > 0.0 && row_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
   check_method(cfg.col_method);
   check_method(cfg.row_method);
 
@@ -499,7 +531,9 @@ void run_iterative_cur(itercur_run* run) {
   // iterations are enqueued in batches of kBatch without a host round trip; the loop control
   // (budgets, stop tests, rank) lives on the device (IterCtl), and every kernel of an
   // iteration after the stop returns immediately.
-  const int kBatch = 8;
+  // With an IterationObserver every batch is one iteration, so the observer sees each
+  // iteration's factors (driver.cpp:154) before the next one starts.
+  const int kBatch = cfg.observer ? 1 : 8;
   const size_t slot_bytes = round_up(iter_state_bytes(B), 64);
   ws.state.alloc(slot_bytes * kBatch + sizeof(IterCtl));
   char* slots = ws.state.p;
@@ -522,6 +556,9 @@ void run_iterative_cur(itercur_run* run) {
     *hc = h;
     CK(cudaMemcpyAsync(d_ctl, hc, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
   }
+  // QRCP rows are not in pivot order: D_k is factored with partial pivoting (cross_lu) and
+  // its permutation kept per block for the solves and the core export
+  if (row_qrcp) run->Piv.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dI.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dJ.alloc(std::max<int64_t>(max_rank + b, 1));
   run->capL = 0;
@@ -645,7 +682,7 @@ void run_iterative_cur(itercur_run* run) {
     p.dbg_k = ub_trace_k;
     return p;
   };
-  const bool fused_ub = !env_flag("ITERCUR_NO_FUSED_UBLOCK") && [&] {
+  const bool fused_ub = !env_flag("ITERCUR_NO_FUSED_UBLOCK") && !row_qrcp && [&] {
     IterState* slot0 = reinterpret_cast<IterState*>(slots);
     TsGemmParams p = ublock_params(run->capL, slot0, iter_arrays(slot0, B));
     p.norm_part = reinterpret_cast<double*>(16);  // placeholder: allocated below
@@ -685,7 +722,7 @@ void run_iterative_cur(itercur_run* run) {
     ~GraphCache() { clear(); }
   } graphs;
   int64_t graph_cap = -1;
-  int64_t k_host = 0, r_host = 0;
+  int64_t k_host = 0, r_host = 0, observed = 0;
   int64_t ev_i = 2;
   std::vector<size_t> iter_events;
   bool done = false;
@@ -767,7 +804,7 @@ void run_iterative_cur(itercur_run* run) {
           la.mask = ws.col_mask.p;
           la.epoch = epoch;
           la.d_norm_sq = &d_ctl->ysq;
-          la.pivot_floor = cfg.pivot_floor;
+          la.pivot_floor = col_floor;
           la.d_idx = arr.col_idx;
           la.d_best = arr.col_best;
           la.d_second = arr.col_second;
@@ -794,7 +831,7 @@ void run_iterative_cur(itercur_run* run) {
           if (col_qrcp) {  // QRCP over the c-row columns of (a copy of) Y, select.cpp:79-117,121-139
             CK(cudaMemcpyAsync(ws.Wq.p, ws.Y.p, sizeof(double) * cp * n, cudaMemcpyDeviceToDevice, st));
             CK(run_qrcp(ws.Wq.p, n, static_cast<int>(c), nullptr, 1, cp, &d_ctl->block, B, ws.col_mask.p, epoch,
-                        &d_ctl->ysq, cfg.pivot_floor, arr.col_idx, arr.col_best, arr.col_second, &slot->ncols,
+                        &d_ctl->ysq, col_floor, arr.col_idx, arr.col_best, arr.col_second, &slot->ncols,
                         nullptr, nullptr, ws.qrcp_scratch.p, d_ctl, st));
           } else {
             CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, nullptr));
@@ -840,7 +877,7 @@ void run_iterative_cur(itercur_run* run) {
           la.mask = ws.row_mask.p;
           la.epoch = epoch;
           la.d_norm_sq = nullptr;  // ||S_row||_F over its |cols| columns, computed in-kernel
-          la.pivot_floor = cfg.pivot_floor;
+          la.pivot_floor = row_floor;
           la.d_idx = arr.row_idx;
           la.d_best = arr.row_best;
           la.d_second = arr.row_second;
@@ -858,7 +895,7 @@ void run_iterative_cur(itercur_run* run) {
           if (row_qrcp) {  // QRCP over the rows of S_row (select.cpp:141-165); D_k by cross_lu below
             row_lupp_path = 0;
             CK(run_qrcp(ws.Wr.p, m, B, &slot->ncols, ldm, 1, &slot->ncols, B, ws.row_mask.p, epoch, nullptr,
-                        cfg.pivot_floor, arr.row_idx, arr.row_best, arr.row_second, &slot->nrows, &slot->width,
+                        row_floor, arr.row_idx, arr.row_best, arr.row_second, &slot->nrows, &slot->width,
                         &slot->ncols, ws.qrcp_scratch.p, d_ctl, st));
           } else {
             CK(run_lupp_with_scratch(la, ws.lupp_scratch.p, st, &row_lupp_path));
@@ -870,7 +907,8 @@ void run_iterative_cur(itercur_run* run) {
         //     Rt_k = D_k^{-1} U_k by row-wise LU solves (rows r..r+w of Rt)
         static const bool force_cross_lu = env_flag("ITERCUR_FORCE_CROSS_LU");  // A/B check
         if (row_lupp_path >= 0 || force_cross_lu)  // the cluster / panel LUPP emitted D_k's factors itself
-          CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl));
+          CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl,
+                             run->Piv.p));
         static const bool pair_off = env_flag("ITERCUR_NO_PAIR_GATHER");  // A/B
         const bool y_here = fused_ub && !y_side && !col_fused;  // Y(:, J_k) gathered right before the U block
         if (!row_fused && y_here && !pair_off)  // L(I_k, :)^T and Y(:, J_k) in one launch
@@ -945,7 +983,7 @@ void run_iterative_cur(itercur_run* run) {
           CK(run_ts_gemm(p, st));
         }
         CK(launch_rows_lu_solve(ws.Ut.p, ldn, n, run->Dinv.p, run->bmax, &slot->width, B, run->Rt.p, run->ldR, st,
-                                d_ctl, run->ldR));
+                                d_ctl, run->ldR, run->Piv.p));
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
 
         // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
@@ -1078,6 +1116,16 @@ void run_iterative_cur(itercur_run* run) {
       ++k_host;
     }
     if (hc->r != r_host || hc->k != k_host) fail(ITERCUR_E_LOGIC, "device / host iteration bookkeeping diverged");
+    if (cfg.observer && k_host > observed) {
+      // driver.cpp:154: the observer sees the factors after the iteration (one per batch here)
+      run->r = r_host;
+      observed = k_host;
+      cudaStream_t saved = g_alloc_stream;
+      const int rc = cfg.observer(cfg.observer_user, run, &run->iters.back());
+      g_alloc_stream = saved;
+      CK(cudaSetDevice(run->device));
+      if (rc != 0) fail(ITERCUR_E_RUNTIME, "iteration observer failed");
+    }
     if (host_trace)
       fprintf(stderr, "[itercur batch] r=%lld capL=%lld grow=%.0fus capture=%.0fus launch=%.0fus sync=%.0fus total=%.0fus\n",
               static_cast<long long>(r_host), static_cast<long long>(run->capL), t_grow, t_capture, t_launch, t_sync,
@@ -1133,6 +1181,22 @@ void run_iterative_cur(itercur_run* run) {
 }
 
 // ------------------------------------------------------------------ exports
+// Host entry: keep only C = A(:,J) and R^T = A(I,:)^T (r (m + n) doubles) and free the m x n
+// device copy of A, so a live result does not pin the input's HBM (80 GB at configs 4/5).
+void release_input_copy(itercur_run* run) {
+  cudaStream_t st = run->wstream;
+  g_alloc_stream = st;
+  if (run->r > 0) {
+    run->Cg.alloc(static_cast<size_t>(run->m) * run->r);
+    run->RgT.alloc(static_cast<size_t>(run->n) * run->r);
+    CK(launch_gather(run->A, 1, run->lda, run->m, run->dJ.p, nullptr, static_cast<int>(run->r), run->Cg.p, run->m, st));
+    CK(launch_gather(run->A, run->lda, 1, run->n, run->dI.p, nullptr, static_cast<int>(run->r), run->RgT.p, run->n, st));
+  }
+  run->A_owned.reset();
+  run->A = nullptr;
+  CK(cudaStreamSynchronize(st));
+}
+
 void gather_host(const itercur_run* run, const double* src, int64_t row_stride, int64_t col_stride, int64_t K,
                  const int64_t* d_idx, int64_t w, double* out) {
   if (K == 0 || w == 0) return;
@@ -1146,12 +1210,12 @@ void gather_host(const itercur_run* run, const double* src, int64_t row_stride, 
 // X^{-1} with X = A(I,J) = Lc * Uc, Lc = L(I,:) block-lower (diagonal blocks D_k),
 // Uc = Rt(:,J) unit block-upper.  Zt = (Lc^{-1})^T by block forward substitution, then
 // Xit = (Uc^{-1} Z)^T by block back substitution; core = Xit^T.
-void core_matrix_impl(const itercur_run* run, double* out) {
+// Xit = X^{-T} (r x r, column-major, ld r) on the device, X = A(I, J).
+void core_xit_device(const itercur_run* run, DevBuf<double>& Xit) {
   const int64_t r = run->r;
-  if (r == 0) return;
   cudaStream_t st = run->stream;
   const int B = static_cast<int>(run->bmax);
-  DevBuf<double> Zt, Xit, T, Bg;
+  DevBuf<double> Zt, T, Bg;
   Zt.alloc(static_cast<size_t>(r) * r);
   Xit.alloc(static_cast<size_t>(r) * r);
   T.alloc(static_cast<size_t>(r) * B);
@@ -1185,7 +1249,7 @@ void core_matrix_impl(const itercur_run* run, double* out) {
     p.ldc0 = r;
     CK(run_ts_gemm(p, st));
     CK(launch_rows_lu_solve(T.p, r, r, run->Dinv.p + run->bmax * s, run->bmax, nullptr, static_cast<int>(w),
-                            Zt.p + r * s, r, st));
+                            Zt.p + r * s, r, st, nullptr, 0, run->Piv.p ? run->Piv.p + s : nullptr));
   }
   for (size_t kb = nb; kb-- > 0;) {
     const int64_t s = run->block_start[kb], w = run->block_width[kb];
@@ -1213,6 +1277,14 @@ void core_matrix_impl(const itercur_run* run, double* out) {
     p.ldc0 = r;
     CK(run_ts_gemm(p, st));
   }
+}
+
+void core_matrix_impl(const itercur_run* run, double* out) {
+  const int64_t r = run->r;
+  if (r == 0) return;
+  cudaStream_t st = run->stream;
+  DevBuf<double> Xit;
+  core_xit_device(run, Xit);
   std::vector<double> h(static_cast<size_t>(r) * r);
   CK(cudaMemcpyAsync(h.data(), Xit.p, sizeof(double) * r * r, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1220,37 +1292,125 @@ void core_matrix_impl(const itercur_run* run, double* out) {
     for (int64_t i = 0; i < r; ++i) out[i + j * r] = h[j + i * r];  // core = Xit^T
 }
 
-double true_error_impl(const itercur_run* run) {
+// out = X^{-1} rhs (transposed = 0) or X^{-T} rhs (1): FactoredPinv::solve / solve_transposed
+// (pinv.cpp:24-39) of the engine's exact core, on the device GEMM with the materialised inverse.
+void core_apply_impl(const itercur_run* run, bool transposed, const double* rhs, int64_t k, int64_t ldr, double* out,
+                     int64_t ldo) {
+  const int64_t r = run->r;
+  if (r == 0 || k == 0) return;
   cudaStream_t st = run->stream;
-  const double asq = device_sumsq(run->A, run->m, run->n, run->lda, st);
-  const double a_norm = std::sqrt(asq);
-  if (a_norm == 0.0) return 0.0;
-  if (run->r == 0) return 1.0;
+  DevBuf<double> Xit, op, B, C;
+  core_xit_device(run, Xit);
+  const int64_t ldop = even(r);
+  op.alloc(static_cast<size_t>(ldop) * r);
+  if (transposed) {  // X^{-T} = Xit
+    CK(cudaMemcpy2DAsync(op.p, sizeof(double) * ldop, Xit.p, sizeof(double) * r, sizeof(double) * r, r,
+                         cudaMemcpyDeviceToDevice, st));
+  } else {  // X^{-1} = Xit^T
+    CK(launch_transpose(Xit.p, r, r, r, op.p, ldop, st));
+  }
+  B.alloc(static_cast<size_t>(r) * k);
+  C.alloc(static_cast<size_t>(r) * k);
+  CK(cudaMemcpy2DAsync(B.p, sizeof(double) * r, rhs, sizeof(double) * ldr, sizeof(double) * r, k,
+                       cudaMemcpyHostToDevice, st));
+  constexpr int64_t kChunk = 1 << 20;  // columns per GEMM launch (grid.y bound)
+  for (int64_t q0 = 0; q0 < k; q0 += kChunk) {
+    TsGemmParams p;
+    p.M = r;
+    p.K = r;
+    p.N = static_cast<int>(std::min(kChunk, k - q0));
+    p.A = op.p;
+    p.lda = ldop;
+    p.B = B.p + q0 * r;
+    p.bsk = 1;
+    p.bsn = r;
+    p.base_mode = kBaseNone;
+    p.alpha = 1.0;
+    p.out_mode = kOutColMajor;
+    p.C0 = C.p + q0 * r;
+    p.ldc0 = r;
+    CK(run_ts_gemm(p, st));
+  }
+  CK(cudaMemcpy2DAsync(out, sizeof(double) * ldo, C.p, sizeof(double) * r, sizeof(double) * r, k,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// ||A - L R~||_F^2 over columns [j0, j0 + w) of a device matrix Ap (column j0 at Ap, ld lda),
+// summed into *d_out (fixed-order reduction).
+void residual_sumsq_panel(const itercur_run* run, const double* Ap, int64_t lda, int64_t j0, int64_t w,
+                          DevBuf<double>& part, double* d_out, cudaStream_t st) {
   TsGemmParams p;
   p.M = run->m;
   p.K = run->r;
-  p.N = static_cast<int>(std::min<int64_t>(run->n, 1 << 30));
+  p.N = static_cast<int>(w);
   p.A = run->L.p;
   p.lda = run->ldL;
-  p.B = run->Rt.p;
+  p.B = run->Rt.p + j0;  // B(k, q) = R~(k, j0 + q)
   p.bsk = run->ldR;
   p.bsn = 1;
   p.base_mode = kBaseContigCols;
-  p.src = run->A;
-  p.lds = run->lda;
+  p.src = Ap;
+  p.lds = lda;
   p.col0 = 0;
   p.alpha = -1.0;
   p.out_mode = kOutNone;
   const int64_t parts = ts_gemm_grid_size(p.M, p.N);
-  DevBuf<double> part, outd;
-  part.alloc(parts);
-  outd.alloc(1);
+  if (part.count < static_cast<size_t>(parts)) part.alloc(parts);
   p.norm_part = part.p;
   CK(run_ts_gemm(p, st));
-  CK(launch_sum_partials(part.p, parts, outd.p, st));
-  double sq = 0.0;
-  CK(cudaMemcpyAsync(&sq, outd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(launch_sum_partials(part.p, parts, d_out, st));
+}
+
+// true_relative_error(A, factors), proj/src/driver.cpp:169-190: ||A - C core R|| / ||A|| with
+// C core R = L R~ (the incremental form). A is the run's own matrix or any m x n matrix given on
+// the device or on the host (streamed through the device in column panels).
+double true_error_impl(const itercur_run* run, const double* A, int64_t lda, bool on_device) {
+  cudaStream_t st = run->stream;
+  const int64_t m = run->m, n = run->n;
+  if (on_device) {
+    const double asq = device_sumsq(A, m, n, lda, st);
+    const double a_norm = std::sqrt(asq);
+    if (a_norm == 0.0) return 0.0;
+    if (run->r == 0) return 1.0;
+    DevBuf<double> part, outd;
+    outd.alloc(1);
+    constexpr int64_t kPanel = 1 << 30;
+    double sq = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += kPanel) {
+      residual_sumsq_panel(run, A + j0 * lda, lda, j0, std::min(kPanel, n - j0), part, outd.p, st);
+      double h = 0.0;
+      CK(cudaMemcpyAsync(&h, outd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      sq += h;
+    }
+    return std::sqrt(sq) / a_norm;
+  }
+  // host matrix: column panels of <= 512 MB through a device buffer; per-panel sums in panel order
+  const int64_t w_max = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / std::max<int64_t>(m, 1)));
+  const int64_t npanels = (n + w_max - 1) / w_max;
+  DevBuf<double> panel, part, outd, apart;
+  panel.alloc(static_cast<size_t>(m) * w_max);
+  outd.alloc(2 * npanels);
+  apart.alloc(148 * 8);
+  for (int64_t pi = 0; pi < npanels; ++pi) {
+    const int64_t j0 = pi * w_max, w = std::min(w_max, n - j0);
+    CK(cudaMemcpy2DAsync(panel.p, sizeof(double) * m, A + j0 * lda, sizeof(double) * lda, sizeof(double) * m, w,
+                         cudaMemcpyHostToDevice, st));
+    CK(launch_sumsq(panel.p, m, w, m, apart.p, 148 * 8, outd.p + 2 * pi, st));
+    if (run->r > 0) residual_sumsq_panel(run, panel.p, m, j0, w, part, outd.p + 2 * pi + 1, st);
+  }
+  std::vector<double> h(static_cast<size_t>(2 * npanels));
+  CK(cudaMemcpyAsync(h.data(), outd.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  double asq = 0.0, sq = 0.0;
+  for (int64_t pi = 0; pi < npanels; ++pi) {
+    asq += h[2 * pi];
+    sq += h[2 * pi + 1];
+  }
+  const double a_norm = std::sqrt(asq);
+  if (a_norm == 0.0) return 0.0;
+  if (run->r == 0) return 1.0;
   return std::sqrt(sq) / a_norm;
 }
 
@@ -1258,7 +1418,8 @@ double true_error_impl(const itercur_run* run) {
 // for a finished run's factors: rho = ||G A - G (C core R)|| / ||G A||. With the incremental
 // form C core R = L R~, so G C core R = (G L) R~: the sketch operator is applied to L (m x r) by
 // the same kernel, then Y^T -= R~^T (G L)^T on the engine's GEMM with ||Y||^2 fused.
-double sketched_residual_impl(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind, int32_t sparse_nnz) {
+double sketched_residual_impl(const itercur_run* run, const double* A, int64_t lda, int64_t b, uint64_t seed,
+                              int32_t kind, int32_t sparse_nnz) {
   cudaStream_t st = run->stream;
   const int64_t m = run->m, n = run->n;
   if (b < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "block size must be at least 1");
@@ -1270,7 +1431,7 @@ double sketched_residual_impl(const itercur_run* run, int64_t b, uint64_t seed, 
   Y.alloc(static_cast<size_t>(cp) * n);
   scal.alloc(4);
   const int64_t r = run->r;
-  apply_sketch(run->A, m, n, run->lda, k, sparse_nnz, seed, kStreamSketch, c, cp, Y.p, SketchStats{scal.p, scal.p + 1},
+  apply_sketch(A, m, n, lda, k, sparse_nnz, seed, kStreamSketch, c, cp, Y.p, SketchStats{scal.p, scal.p + 1},
                sb, st);
   double h[2];
   CK(cudaMemcpyAsync(h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -1381,6 +1542,7 @@ int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t ld
     }
     run->cfg = cfg ? *cfg : default_config();
     run_iterative_cur(run.get());
+    if (!run->cfg.keep_device_copy && run->A_owned.p) release_input_copy(run.get());
     *out = run.release();
   });
 }
@@ -1428,7 +1590,12 @@ int itercur_run_c_matrix(const itercur_run* run, double* out) {
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     // C(i, q) = A(i, J[q]): out(k=i, q) = A[i * 1 + J[q] * lda]
-    gather_host(run, run->A, 1, run->lda, run->m, run->dJ.p, run->r, out);
+    if (run->A) {
+      gather_host(run, run->A, 1, run->lda, run->m, run->dJ.p, run->r, out);
+    } else if (run->r > 0) {
+      CK(cudaMemcpyAsync(out, run->Cg.p, sizeof(double) * run->m * run->r, cudaMemcpyDeviceToHost, run->stream));
+      CK(cudaStreamSynchronize(run->stream));
+    }
   });
 }
 int itercur_run_r_matrix(const itercur_run* run, double* out) {
@@ -1438,7 +1605,12 @@ int itercur_run_r_matrix(const itercur_run* run, double* out) {
     g_alloc_stream = run->stream;
     // R^T(j, q) = A(I[q], j): gathered as (n x r), then transposed on the host
     std::vector<double> t(static_cast<size_t>(run->n) * run->r);
-    gather_host(run, run->A, run->lda, 1, run->n, run->dI.p, run->r, t.data());
+    if (run->A) {
+      gather_host(run, run->A, run->lda, 1, run->n, run->dI.p, run->r, t.data());
+    } else if (run->r > 0) {
+      CK(cudaMemcpyAsync(t.data(), run->RgT.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost, run->stream));
+      CK(cudaStreamSynchronize(run->stream));
+    }
     for (int64_t q = 0; q < run->r; ++q)
       for (int64_t j = 0; j < run->n; ++j) out[q + j * run->r] = t[j + q * run->n];
   });
@@ -1456,7 +1628,35 @@ int itercur_true_relative_error_device(const itercur_run* run, double* out) {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
-    *out = true_error_impl(run);
+    if (!run->A)
+      fail(ITERCUR_E_LOGIC, "the run released its device copy of A (host entry): pass the matrix to "
+                            "itercur_true_relative_error_matrix");
+    *out = true_error_impl(run, run->A, run->lda, true);
+  });
+}
+int itercur_true_relative_error_matrix(const itercur_run* run, const double* A, int64_t m, int64_t n, int64_t lda,
+                                       int32_t a_on_device, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    if (m != run->m || n != run->n)
+      fail(ITERCUR_E_INVALID_ARGUMENT, "true_relative_error: matrix is " + std::to_string(m) + "x" +
+                                           std::to_string(n) + ", factors are for " + std::to_string(run->m) + "x" +
+                                           std::to_string(run->n));
+    if (lda < std::max<int64_t>(m, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "true_relative_error: lda < rows");
+    CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
+    *out = true_error_impl(run, A, lda, a_on_device != 0);
+  });
+}
+int itercur_run_core_apply(const itercur_run* run, int32_t transposed, const double* rhs, int64_t k, int64_t ldr,
+                           double* out, int64_t ldo) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    if (k < 0 || ldr < std::max<int64_t>(run->r, 1) || ldo < std::max<int64_t>(run->r, 1))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "core_apply: invalid shape");
+    CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
+    core_apply_impl(run, transposed != 0, rhs, k, ldr, out, ldo);
   });
 }
 int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind,
@@ -1465,7 +1665,27 @@ int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
-    *out = sketched_residual_impl(run, b, seed, kind, sparse_nnz);
+    if (!run->A)
+      fail(ITERCUR_E_LOGIC, "the run released its device copy of A (host entry): pass the matrix to "
+                            "itercur_sketched_residual_matrix");
+    *out = sketched_residual_impl(run, run->A, run->lda, b, seed, kind, sparse_nnz);
+  });
+}
+int itercur_sketched_residual_matrix(const itercur_run* run, const double* dA, int64_t lda, int64_t b, uint64_t seed,
+                                     int32_t kind, int32_t sparse_nnz, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    if (!dA || lda < std::max<int64_t>(run->m, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "sketched residual: invalid matrix");
+    CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
+    *out = sketched_residual_impl(run, dA, lda, b, seed, kind, sparse_nnz);
+  });
+}
+int32_t itercur_run_holds_matrix(const itercur_run* run) { return run && run->A ? 1 : 0; }
+int itercur_copy_to_host(void* dst, const void* d_src, uint64_t bytes) {
+  return guarded([&] {
+    require_device();
+    if (bytes) CK(cudaMemcpy(dst, d_src, bytes, cudaMemcpyDeviceToHost));
   });
 }
 int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda, void* stream, double* out) {
@@ -1887,9 +2107,9 @@ int itercur_rows_lu_solve_device(const double* dX, int64_t ldx, int64_t M, const
                                  double* dOut, int64_t ldo, void* stream) {
   return guarded([&] {
     require_device();
-    if (M < 0 || w < 0 || w > 180 || ldx < std::max<int64_t>(M, 1) || ldo < std::max<int64_t>(M, 1) ||
+    if (M < 0 || w < 0 || w > 4096 || ldx < std::max<int64_t>(M, 1) || ldo < std::max<int64_t>(M, 1) ||
         ldd < std::max<int64_t>(w, 1))
-      fail(ITERCUR_E_INVALID_ARGUMENT, "rows_lu_solve: invalid shape (block width above 180 unsupported)");
+      fail(ITERCUR_E_INVALID_ARGUMENT, "rows_lu_solve: invalid shape");
     CK(launch_rows_lu_solve(dX, ldx, M, dLU, ldd, nullptr, static_cast<int>(w), dOut, ldo,
                             static_cast<cudaStream_t>(stream), nullptr, 0));
   });

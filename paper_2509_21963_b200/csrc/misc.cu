@@ -170,23 +170,67 @@ cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, ui
 // factors (unit-lower multipliers below the diagonal, U on and above) stay in `lu`; the
 // block is never inverted explicitly (an explicit inverse loses accuracy in proportion to
 // cond(D_k), which reaches 1e9+ once pivots hit the noise floor).
+//
+// With `perm` (row selections that are not LUPP-ordered, e.g. QRCP rows): partial pivoting,
+// P D = Lhat Uhat with perm[q] = the row of D placed at position q (largest |entry| in the
+// column, lowest index on ties) — the reference's COD (pinv.cpp:54-58) accepts any
+// nonsingular cross block, and QRCP's order can put an exact zero on D's diagonal.
 __global__ void cross_lu_kernel(const double* __restrict__ Lk, int64_t ldl, const int64_t* __restrict__ rows,
                                 const int* __restrict__ d_w, int w_max, double* __restrict__ lu, int64_t ldd,
-                                const IterCtl* __restrict__ ctl) {
+                                const IterCtl* __restrict__ ctl, int* __restrict__ perm) {
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
   griddep_wait();
   griddep_launch_dependents();
   if (ctl) {
     if (ctl->done) return;
     Lk += ctl->r * ldl;
     lu += ctl->r * ldd;
+    if (perm) perm += ctl->r;
   }
   const int w = min(*d_w, w_max);
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
     const int p = e % w, q = e / w;
     lu[p + q * ldd] = Lk[rows[p] + q * ldl];
   }
+  if (perm)
+    for (int q = threadIdx.x; q < w; q += blockDim.x) perm[q] = q;
   __syncthreads();
   for (int s = 0; s < w; ++s) {
+    if (perm) {  // argmax |lu(p, s)|, p >= s (lowest index on ties), then swap rows s and p
+      double bv = -1.0;
+      int bi = w;
+      for (int p = s + threadIdx.x; p < w; p += blockDim.x) {
+        const double v = fabs(lu[p + s * ldd]);
+        if (v > bv) { bv = v; bi = p; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if ((threadIdx.x & 31) == 0) { red_v[threadIdx.x >> 5] = bv; red_i[threadIdx.x >> 5] = bi; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int q = 1; q < static_cast<int>(blockDim.x >> 5); ++q)
+          if (red_v[q] > red_v[0] || (red_v[q] == red_v[0] && red_i[q] < red_i[0])) { red_v[0] = red_v[q]; red_i[0] = red_i[q]; }
+      }
+      __syncthreads();
+      const int p = red_i[0];
+      if (p != s && p < w) {
+        for (int t = threadIdx.x; t < w; t += blockDim.x) {
+          const double x = lu[s + t * ldd];
+          lu[s + t * ldd] = lu[p + t * ldd];
+          lu[p + t * ldd] = x;
+        }
+        if (threadIdx.x == 0) {
+          const int x = perm[s];
+          perm[s] = perm[p];
+          perm[p] = x;
+        }
+      }
+      __syncthreads();
+    }
     const double piv = lu[s + s * ldd];
     const int rem = w - s - 1;
     for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
@@ -241,9 +285,11 @@ __global__ void cross_lu_warp_kernel(const double* __restrict__ Lk, int64_t ldl,
 }
 
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
-                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl) {
-  if (w_max <= 32) return launch_ex(cross_lu_warp_kernel, dim3(1), dim3(32), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, lu, ldd, ctl);
-  return launch_ex(cross_lu_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl);
+                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl, int* perm) {
+  if (w_max <= 32 && !perm)
+    return launch_ex(cross_lu_warp_kernel, dim3(1), dim3(32), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, lu, ldd, ctl);
+  return launch_ex(cross_lu_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), Lk, ldl, d_rows, d_w, w_max, lu, ldd, ctl,
+                   perm);
 }
 
 // Row-wise solves D x = u with D = Lhat * Uhat (cross_lu_kernel layout) for every row u of
@@ -254,22 +300,26 @@ template <int WMAX>
 __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
                                      const double* __restrict__ lu, int64_t ldd, const int* __restrict__ d_w,
                                      int w_max, double* __restrict__ out, int64_t ldo,
-                                     const IterCtl* __restrict__ ctl, int64_t out_off_per_r) {
+                                     const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                     const int* __restrict__ perm) {
   extern __shared__ double slu[];
+  __shared__ int sperm[WMAX];
   griddep_wait();
   griddep_launch_dependents();
   if (ctl) {
     if (ctl->done) return;
     lu += ctl->r * ldd;
     out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
   }
   const int w = d_w ? min(*d_w, w_max) : w_max;
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+  for (int q = threadIdx.x; q < WMAX; q += blockDim.x) sperm[q] = (perm && q < w) ? perm[q] : q;
   __syncthreads();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
     double x[WMAX];  // fully unrolled: stays in registers
 #pragma unroll
-    for (int q = 0; q < WMAX; ++q) x[q] = q < w ? X[j + q * ldx] : 0.0;
+    for (int q = 0; q < WMAX; ++q) x[q] = q < w ? X[j + sperm[q] * ldx] : 0.0;  // P u (perm: pivoted LU)
 #pragma unroll
     for (int q = 1; q < WMAX; ++q) {  // Lhat y = u
       if (q < w) {
@@ -295,33 +345,41 @@ __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, 
   }
 }
 
-// generic width (w > 64): same solves with x in local memory
+// generic width (w > 64): same solves with x in a column-strided global workspace; the factors
+// in shared memory while w*w doubles fit one CTA (w <= 168), else read from global memory
+// (L1/L2-resident: every thread walks them in the same order)
+template <bool SMEM>
 __global__ void rows_lu_solve_wide_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
                                           const double* __restrict__ lu, int64_t ldd, const int* __restrict__ d_w,
                                           int w_max, double* __restrict__ out, int64_t ldo,
                                           const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
-                                          double* __restrict__ scratch) {
+                                          double* __restrict__ scratch, const int* __restrict__ perm) {
   extern __shared__ double slu[];
   if (ctl) {
     if (ctl->done) return;
     lu += ctl->r * ldd;
     out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
   }
   const int w = d_w ? min(*d_w, w_max) : w_max;
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
-  __syncthreads();
+  if (SMEM) {
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+    __syncthreads();
+  }
+  const int64_t ld = SMEM ? w : ldd;
+  const double* f = SMEM ? slu : lu;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
     double* x = scratch + j;  // column-strided per-row workspace (ld M)
-    for (int q = 0; q < w; ++q) x[q * M] = X[j + q * ldx];
+    for (int q = 0; q < w; ++q) x[q * M] = X[j + (perm ? perm[q] : q) * ldx];
     for (int q = 1; q < w; ++q) {
       double v = x[q * M];
-      for (int p = 0; p < q; ++p) v = fma(-slu[q + p * w], x[p * M], v);
+      for (int p = 0; p < q; ++p) v = fma(-f[q + p * ld], x[p * M], v);
       x[q * M] = v;
     }
     for (int q = w - 1; q >= 0; --q) {
       double v = x[q * M];
-      for (int p = q + 1; p < w; ++p) v = fma(-slu[q + p * w], x[p * M], v);
-      x[q * M] = v / slu[q + q * w];
+      for (int p = q + 1; p < w; ++p) v = fma(-f[q + p * ld], x[p * M], v);
+      x[q * M] = v / f[q + q * ld];
     }
     for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q * M];
   }
@@ -329,33 +387,41 @@ __global__ void rows_lu_solve_wide_kernel(const double* __restrict__ X, int64_t 
 
 cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
                                  const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
-                                 const IterCtl* ctl, int64_t out_off_per_r) {
+                                 const IterCtl* ctl, int64_t out_off_per_r, const int* perm) {
   if (M <= 0 || w_max <= 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(M, 128), 148 * 16));
   const size_t smem = sizeof(double) * static_cast<size_t>(w_max) * w_max;
   if (w_max <= 16) {
     return launch_ex(rows_lu_solve_kernel<16>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
-                     w_max, out, ldo, ctl, out_off_per_r);
+                     w_max, out, ldo, ctl, out_off_per_r, perm);
   } else if (w_max <= 32) {
     return launch_ex(rows_lu_solve_kernel<32>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
-                     w_max, out, ldo, ctl, out_off_per_r);
+                     w_max, out, ldo, ctl, out_off_per_r, perm);
   } else if (w_max <= 64) {
     return launch_ex(rows_lu_solve_kernel<64>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
-                     w_max, out, ldo, ctl, out_off_per_r);
-  } else if (w_max <= 180) {
-    // X itself serves as the per-row workspace when solving in place is not requested:
-    // use the output buffer (each row's entries are private to its thread)
-    cudaFuncSetAttribute(rows_lu_solve_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    double* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * M * w_max, st);
-    if (e != cudaSuccess) return e;
-    rows_lu_solve_wide_kernel<<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl,
-                                                         out_off_per_r, scratch);
-    cudaFreeAsync(scratch, st);
-  } else {
-    return cudaErrorInvalidValue;  // blocks wider than 180 exceed one CTA's shared memory for D
+                     w_max, out, ldo, ctl, out_off_per_r, perm);
   }
-  return cudaGetLastError();
+  // per-row workspace: M x w doubles (stream-ordered, freed after the launch)
+  double* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * M * w_max, st);
+  if (e != cudaSuccess) return e;
+  constexpr size_t kSmemMax = 227 * 1024;
+  if (smem <= kSmemMax) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(rows_lu_solve_wide_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kSmemMax));
+      attr = true;
+    }
+    rows_lu_solve_wide_kernel<true><<<blocks, 128, smem, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl,
+                                                               out_off_per_r, scratch, perm);
+  } else {  // blocks wider than ~168: the factors stay in global memory
+    rows_lu_solve_wide_kernel<false><<<blocks, 128, 0, st>>>(X, ldx, M, lu, ldd, d_w, w_max, out, ldo, ctl,
+                                                             out_off_per_r, scratch, perm);
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
+  return e;
 }
 
 // CSR (row_ptr, col_idx, values; proj/src/matrix.cpp:79-104 layout) -> dense column-major

@@ -145,15 +145,20 @@ cudaError_t launch_gather2(const double* src, int64_t ld, const int64_t* d_idx, 
 // G(i, j) = normal_at(seed, stream_tag, i, j), rows x cols column-major (rng.cpp:61-67)
 cudaError_t launch_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint32_t stream_tag, double* out,
                                    cudaStream_t st);
-// LU (no pivoting; rows already in LUPP order) of D = Lk(rows, 0:w) into lu (ld ldd).
-// With ctl: Lk += ctl->r * ldl, lu += ctl->r * ldd, skipped when done.
+// LU of D = Lk(rows, 0:w) into lu (ld ldd): without pivoting (rows already in LUPP order), or,
+// with `perm`, partial pivoting P D = Lhat Uhat (perm[q] = row of D at position q).
+// With ctl: Lk += ctl->r * ldl, lu += ctl->r * ldd, perm += ctl->r, skipped when done.
 cudaError_t launch_cross_lu(const double* Lk, int64_t ldl, const int64_t* d_rows, const int* d_w, int w_max,
-                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl = nullptr);
-// out(j, :) = X(j, :) * D^{-T} (each row solves D x = u) via the LU factors (in place allowed).
-// With ctl: lu += ctl->r * ldd, out += ctl->r * out_off_per_r, skipped when done.
+                            double* lu, int64_t ldd, cudaStream_t st, const IterCtl* ctl = nullptr,
+                            int* perm = nullptr);
+// out(j, :) = X(j, :) * D^{-T} (each row solves D x = u) via the LU factors (in place allowed);
+// with `perm` the factors are of P D and u is loaded permuted. Any width (w > 168: factors read
+// from global memory). With ctl: lu += ctl->r * ldd, perm += ctl->r, out += ctl->r * out_off_per_r,
+// skipped when done.
 cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const double* lu, int64_t ldd,
                                  const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
-                                 const IterCtl* ctl = nullptr, int64_t out_off_per_r = 0);
+                                 const IterCtl* ctl = nullptr, int64_t out_off_per_r = 0,
+                                 const int* perm = nullptr);
 cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st,
                                 const IterCtl* ctl = nullptr);
 cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partials, int max_parts,

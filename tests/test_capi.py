@@ -25,7 +25,7 @@ def test_library_builds_loads_and_exports_all_symbols():
     for name in _declared():
         assert hasattr(lib, name), name
     assert sorted(_capi.EXPORTED) == _declared()
-    assert lib.itercur_abi_version() == 3
+    assert lib.itercur_abi_version() == 4
 
 
 def test_cpu_only_call_fails_loudly_without_device():
