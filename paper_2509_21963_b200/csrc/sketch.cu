@@ -334,6 +334,10 @@ using SketchKernelFn = void (*)(CUtensorMap, CUtensorMap, const double*, int64_t
 
 template <int NT, int MT = 1, int KS = 32>
 static SketchKernelFn pick_kernel(bool tma, int* smem_bytes, int* bm) {
+  // Only the validated tile shape is instantiated: the round-1 two-m-tile / 16-row-stage variant
+  // (MT = 2, KS = 16) produced runaway ranks at config 3 and was never root-caused, so it is not
+  // buildable (bitwise determinism at config 3's shape: tests/test_gpu_stages.py).
+  static_assert(MT == 1 && KS == 32, "sketch_dmma_kernel: only MT = 1, KS = 32 is validated");
   using Cfg = SketchCfg<NT, MT, KS>;
   *smem_bytes = Cfg::SMEM_BYTES;
   *bm = Cfg::BM;

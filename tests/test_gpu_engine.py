@@ -333,8 +333,13 @@ def test_sparse_nnz_validation(engine, oracle):
 def test_block_above_180_matches_oracle(engine, oracle, b, sketch):
     """b > 180 (the paper's runs use b = 250; the reference accepts any b <= m,
     driver.cpp:54): wide-block LUPP, cross LU and row solves with the factors in global memory."""
-    a = low_rank_plus_noise(oracle, 1400, 1100, 420, 1e-12, 91)
-    kw = dict(epsilon=1e-10, b=b, seed=4, sketch=sketch)
+    # sigma_i = 10^(-i/60): tol 1e-5 stops near rank 300, pivots far above the rounding floor (a
+    # low-rank-plus-1e-12-noise input would pick its last pivots from cancellation noise, H7)
+    rng = np.random.default_rng(b)
+    u, _ = np.linalg.qr(rng.standard_normal((1400, 1100)))
+    v, _ = np.linalg.qr(rng.standard_normal((1100, 1100)))
+    a = (u * 10.0 ** (-np.arange(1100) / 60.0)) @ v.T
+    kw = dict(epsilon=1e-5, b=b, seed=4, sketch=sketch)
     f, t = engine.iterative_cur(a, **kw)
     o = oracle.iterative_cur(a, **kw)
     v = compare_runs(o, f, t)

@@ -238,3 +238,26 @@ def test_qrcp_reference_cases(oracle):  # proj/tests/test_select.cpp:32-50
     r = oracle.random_dense(6, 9, 17)
     t = torch.from_numpy(np.asfortranarray(r)).cuda().t().contiguous().t()
     assert stages.select_columns(t, 5, method="qrcp").indices == oracle.select_columns(r, 5, method="qrcp").indices
+
+
+def test_gaussian_sketch_bitwise_deterministic_at_config3_shape(engine, oracle):
+    """sketch_dmma_kernel at config 3's shape (50000 x 50000 RBF, b = 32 -> c_pad 40): 20 launches
+    give bitwise the same Y, ||Y|| and ||A|| (fixed-order split-K reduction; the round-1 two-m-tile
+    variant whose ranks ran away at this shape is rejected at compile time)."""
+    import torch
+
+    from paper_2509_21963_b200 import testmat
+
+    S = _stages()
+    a = testmat.generate(3)
+    torch.cuda.synchronize()
+    y0, ga0, an0 = S.sketch(a, 32, 0)
+    for _ in range(19):
+        y, ga, an = S.sketch(a, 32, 0)
+        assert torch.equal(y, y0) and ga == ga0 and an == an0
+    # and the values are the oracle's G A on a column panel (same Philox stream, FP64 sums)
+    panel = a[:, :64].cpu().numpy()
+    y_or, _, _ = oracle.sketch(np.asfortranarray(panel), 32, 0)
+    assert np.allclose(y0[:, :64].cpu().numpy(), y_or, rtol=1e-12, atol=1e-12 * np.abs(y_or).max())
+    del a
+    torch.cuda.empty_cache()
