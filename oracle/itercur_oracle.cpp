@@ -38,13 +38,17 @@ namespace oracle {
 // columns use it, each column's operations unchanged, so results are bitwise the 1-thread
 // ones. ORACLE_THREADS (default: all hardware threads) sets the pool size; 1 = sequential.
 // ---------------------------------------------------------------------------------
+// Threads actually used per parallel loop (<= the pool size): oracle_set_threads() lowers it, so
+// one process can time the same oracle on 1 core and on all cores.
+std::atomic<int> g_thread_limit{1 << 30};
+
 class Pool {
  public:
   static Pool& get() {
     static Pool p;
     return p;
   }
-  int size() const { return nthreads_; }
+  int size() const { return std::min(nthreads_, g_thread_limit.load()); }
   void run(std::int64_t b, std::int64_t e, const std::function<void(std::int64_t)>& fn) {
     std::unique_lock<std::mutex> lk(mu_);
     fn_ = &fn;
@@ -77,7 +81,9 @@ class Pool {
     for (auto& w : workers_) w.join();
   }
   void chunk(int t, std::int64_t b, std::int64_t e, const std::function<void(std::int64_t)>& fn) const {
-    const std::int64_t n = e - b, per = (n + nthreads_ - 1) / nthreads_;
+    const int active = size();
+    if (t >= active) return;
+    const std::int64_t n = e - b, per = (n + active - 1) / active;
     const std::int64_t lo = b + t * per, hi = std::min(e, lo + per);
     for (std::int64_t i = lo; i < hi; ++i) fn(i);
   }
@@ -560,17 +566,34 @@ SketchState make_sketch(std::uint64_t seed, Index b, const View& a, int kind, in
       sparse_sign_column(seed, i, c, zeta_eff, rows.data() + i * zeta_eff, signs.data() + i * zeta_eff);
     const double scale = 1.0 / std::sqrt(static_cast<double>(zeta_eff));
     asq = column_sumsq(a, false);
+    // Y(h, j) = scale * sum over rows i in ascending order of sign * A(i, j) for the rows i that
+    // hit h. Walked per sketch row h over its (ascending) row list, the additions into each Y(h, j)
+    // happen in exactly the order of the row-major scatter "for i: y[h_t(i)] +-= A(i, j)", so the
+    // result is bitwise that loop's — without its store-to-load dependency chains through y.
+    std::vector<std::vector<std::int32_t>> hits(static_cast<size_t>(c));  // i, or ~i for a negative sign
+    for (Index i = 0; i < m; ++i)
+      for (int t = 0; t < zeta_eff; ++t) {
+        const size_t q = static_cast<size_t>(i * zeta_eff + t);
+        hits[static_cast<size_t>(rows[q])].push_back(signs[q] > 0 ? static_cast<std::int32_t>(i)
+                                                                  : ~static_cast<std::int32_t>(i));
+      }
     parallel_for(0, n, n * m > 65536, [&](Index j) {
       double* y = st.sketched_input.col(j);
       const double* aj = a.p + j * a.ld;
-      for (Index i = 0; i < m; ++i) {
-        const double v = aj[i];
-        for (int t = 0; t < zeta_eff; ++t) {
-          const size_t q = static_cast<size_t>(i * zeta_eff + t);
-          if (signs[q] > 0) y[rows[q]] += v; else y[rows[q]] -= v;
+      for (Index h = 0; h < c; ++h) {
+        double s = 0.0;
+        for (const std::int32_t e : hits[static_cast<size_t>(h)]) {
+          // branch-free s -/+= A(i, j): x - y is x + (-y) exactly in IEEE arithmetic
+          const std::int32_t i = e ^ (e >> 31);
+          std::uint64_t bits;
+          std::memcpy(&bits, aj + i, sizeof bits);
+          bits ^= static_cast<std::uint64_t>(static_cast<std::uint32_t>(e) >> 31) << 63;
+          double v;
+          std::memcpy(&v, &bits, sizeof v);
+          s += v;
         }
+        y[h] = s * scale;
       }
-      for (Index i = 0; i < c; ++i) y[i] *= scale;
     });
   } else {
     throw std::invalid_argument("unknown sketch kind");
@@ -934,6 +957,10 @@ oracle::IndexList to_list(const int64_t* p, int64_t n) { return oracle::IndexLis
 extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
+int oracle_set_threads(int n) {
+  oracle::g_thread_limit.store(n < 1 ? (1 << 30) : n);
+  return oracle::Pool::get().size();
+}
 
 void oracle_philox4x32(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
   const auto r = oracle::philox({ctr[0], ctr[1], ctr[2], ctr[3]}, {key[0], key[1]});

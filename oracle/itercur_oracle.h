@@ -91,6 +91,9 @@ typedef struct {
 } oracle_result;
 
 const char* oracle_last_error(void);
+/* Host threads used by the oracle's independent-column loops (results are bitwise independent of
+   it); n < 1 restores all pool threads (ORACLE_THREADS or the hardware count). Returns the count. */
+int oracle_set_threads(int n);
 
 /* rng (proj/src/rng.cpp:30-67) */
 void oracle_philox4x32(const uint32_t* ctr, const uint32_t* key, uint32_t* out);

@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         L.oracle_uniform_at.restype = C.c_double
         L.oracle_uniform_at.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64]
         L.oracle_gaussian_matrix.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint32, dp]
+        L.oracle_set_threads.argtypes = [C.c_int]
+        L.oracle_set_threads.restype = C.c_int
         L.oracle_gaussian_fill.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32, C.c_double, dp]
         L.oracle_philox4x32.argtypes = [C.POINTER(C.c_uint32)] * 3
         L.oracle_sparse_sign_pattern.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int32,
@@ -164,6 +166,11 @@ def gaussian_matrix(rows, cols, seed, stream=STREAM_SKETCH) -> np.ndarray:
     out = np.empty((rows, cols), dtype=np.float64, order="F")
     lib().oracle_gaussian_matrix(rows, cols, seed, stream, _dp(out))
     return out
+
+
+def set_threads(n: int) -> int:
+    """Threads for the oracle's column-parallel loops (0 = all); returns the count in use."""
+    return int(lib().oracle_set_threads(int(n)))
 
 
 def gaussian_fill(out: np.ndarray, seed, stream, scale=1.0) -> None:
