@@ -345,6 +345,77 @@ __global__ void rows_lu_solve_kernel(const double* __restrict__ X, int64_t ldx, 
   }
 }
 
+// Column-oriented form of the same solves for 16 < w <= WMAX, a row shared by a lane pair (lane
+// bit 0 = which half of the row): the outer loop over pivots p is a runtime loop and only the
+// update over the thread's WMAX/2 entries is unrolled, so every register index is static (the
+// row-oriented kernel above keeps its fully unrolled triangle in local memory beyond 16 columns:
+// 255 registers + a 560-byte stack frame at WMAX = 64). x[p] is read with a static select and
+// handed to the partner with one shuffle. The forward substitution updates each x[q] in
+// ascending p, exactly as the row form; the back substitution updates x[q] in descending p (a
+// different, equally backward-stable rounding order).
+template <int WMAX>
+__global__ void __launch_bounds__(128) rows_lu_solve_col_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                                                const double* __restrict__ lu, int64_t ldd,
+                                                                const int* __restrict__ d_w, int w_max,
+                                                                double* __restrict__ out, int64_t ldo,
+                                                                const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                                                const int* __restrict__ perm) {
+  constexpr int H = WMAX / 2;
+  extern __shared__ double slu[];
+  __shared__ int sperm[WMAX];
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
+  }
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+  for (int q = threadIdx.x; q < WMAX; q += blockDim.x) sperm[q] = (perm && q < w) ? perm[q] : q;
+  __syncthreads();
+  const int half = threadIdx.x & 1;
+  const int q0 = half * H;  // this thread's entries: q0 .. q0 + H - 1
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 1);
+  const int64_t rows_pad = ceil_div(M, stride) * stride;  // pairs stay converged: both lanes loop alike
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 1) + (threadIdx.x >> 1); j < rows_pad; j += stride) {
+    const bool live = j < M;
+    double x[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) x[q] = (live && q0 + q < w) ? X[j + sperm[q0 + q] * ldx] : 0.0;  // P u
+    for (int p = 0; p + 1 < w; ++p) {  // Lhat y = u (unit lower)
+      double mine = 0.0;
+#pragma unroll
+      for (int q = 0; q < H; ++q) mine = q0 + q == p ? x[q] : mine;
+      const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+      const double xp = (p >= q0 && p < q0 + H) ? mine : other;
+      const double* col = slu + p * w;
+#pragma unroll
+      for (int q = 0; q < H; ++q)
+        if (q0 + q > p && q0 + q < w) x[q] = fma(-col[q0 + q], xp, x[q]);
+    }
+    for (int p = w - 1; p >= 0; --p) {  // Uhat x = y
+      double mine = 0.0;
+#pragma unroll
+      for (int q = 0; q < H; ++q) mine = q0 + q == p ? x[q] : mine;
+      const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+      const double xp = ((p >= q0 && p < q0 + H) ? mine : other) / slu[p + p * w];
+#pragma unroll
+      for (int q = 0; q < H; ++q) x[q] = q0 + q == p ? xp : x[q];
+      const double* col = slu + p * w;
+#pragma unroll
+      for (int q = 0; q < H; ++q)
+        if (q0 + q < p) x[q] = fma(-col[q0 + q], xp, x[q]);
+    }
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < H; ++q)
+        if (q0 + q < w) out[j + (q0 + q) * ldo] = x[q];
+    }
+  }
+}
+
 // generic width (w > 64): same solves with x in a column-strided global workspace; the factors
 // in shared memory while w*w doubles fit one CTA (w <= 168), else read from global memory
 // (L1/L2-resident: every thread walks them in the same order)
@@ -394,12 +465,19 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
   if (w_max <= 16) {
     return launch_ex(rows_lu_solve_kernel<16>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
-  } else if (w_max <= 32) {
+  } else if (w_max <= 32 && env_flag("ITERCUR_ROWS_SOLVE_ROWFORM")) {  // A/B: the row-oriented form
     return launch_ex(rows_lu_solve_kernel<32>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
-  } else if (w_max <= 64) {
+  } else if (w_max <= 64 && env_flag("ITERCUR_ROWS_SOLVE_ROWFORM")) {
     return launch_ex(rows_lu_solve_kernel<64>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
+  } else if (w_max <= 64) {  // lane pairs: 64 rows per 128-thread CTA
+    const int blocks2 = static_cast<int>(std::min<int64_t>(ceil_div(M, 64), 148 * 16));
+    if (w_max <= 32)
+      return launch_ex(rows_lu_solve_col_kernel<32>, dim3(blocks2), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu,
+                       ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+    return launch_ex(rows_lu_solve_col_kernel<64>, dim3(blocks2), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd,
+                     d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
   }
   // per-row workspace: M x w doubles (stream-ordered, freed after the launch)
   double* scratch = nullptr;
