@@ -145,6 +145,35 @@ ITERCUR_API int itercur_iterative_cur_device(const double* dA, int64_t m, int64_
 ITERCUR_API int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
                                itercur_run** out);
 
+/* ---- column-sharded runs (one process per GPU over NCCL) ----
+ * A is split by columns into contiguous blocks: rank r of `world` owns columns
+ * [off, off + count) from itercur_shard_range (blocks of an even width). Each rank passes its block
+ * (m x count, ld lda, on its device) and a ncclComm_t over the ranks; every rank returns the same
+ * indices, status and trace as one device would (the sketch is local, the column selection runs on
+ * the replicated Y^T(:, 0:b), gathered per iteration; the selected block [A(:,J_k) | R~(:,J_k) |
+ * Y(:,J_k)] is assembled with one sum-allreduce of disjoint contributions; ||Y||^2 with one scalar
+ * allreduce; the row selection, L and D_k are replicated; the U block and the downdate are local).
+ * All collectives are enqueued on the run's stream and captured in its iteration graphs. A rank
+ * holds only its columns of A, Y and R~: C / R / core exports are not available on it (indices,
+ * trace and itercur_true_relative_error_sharded are). NCCL (libnccl.so.2) is loaded at run time. */
+ITERCUR_API int itercur_shard_range(int64_t n_total, int32_t world, int32_t rank, int64_t* offset, int64_t* count);
+ITERCUR_API int itercur_iterative_cur_sharded_device(const double* dA, int64_t m, int64_t n_local, int64_t lda,
+                                                     int64_t n_total, const itercur_config* cfg, void* nccl_comm,
+                                                     void* stream, itercur_run** out);
+/* The same pipeline with `shards` column shards computed by ONE process on its device (per-shard
+ * kernels on each shard's columns; the collectives become the equivalent device writes): the
+ * multi-rank data path exercised on one GPU. dA is the whole m x n matrix. */
+ITERCUR_API int itercur_iterative_cur_sharded_emulated(const double* dA, int64_t m, int64_t n, int64_t lda,
+                                                       int32_t shards, const itercur_config* cfg, void* stream,
+                                                       itercur_run** out);
+/* true_relative_error over a sharded run: collective on the run's communicator (every rank calls it). */
+ITERCUR_API int itercur_true_relative_error_sharded(const itercur_run* run, double* out);
+/* NCCL plumbing for callers without their own communicator: the 128-byte unique id (rank 0; share
+ * it with the other ranks), the communicator on the current device, and its release. */
+ITERCUR_API int itercur_nccl_unique_id(void* id_out);
+ITERCUR_API int itercur_nccl_comm_init(int32_t world, const void* id, int32_t rank, void** comm_out);
+ITERCUR_API int itercur_nccl_comm_destroy(void* comm);
+
 /* ---- run accessors (CurFactors / RunTrace) ---- */
 ITERCUR_API int64_t itercur_run_rank(const itercur_run* run);
 ITERCUR_API int64_t itercur_run_rows(const itercur_run* run);

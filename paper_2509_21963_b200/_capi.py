@@ -33,6 +33,9 @@ EXPORTED = [
     "itercur_select_qrcp_device", "itercur_csr_to_dense_device",
     "itercur_true_relative_error_matrix", "itercur_run_core_apply", "itercur_sketched_residual_matrix",
     "itercur_run_holds_matrix", "itercur_copy_to_host",
+    "itercur_shard_range", "itercur_iterative_cur_sharded_device", "itercur_iterative_cur_sharded_emulated",
+    "itercur_true_relative_error_sharded", "itercur_nccl_unique_id", "itercur_nccl_comm_init",
+    "itercur_nccl_comm_destroy",
 ]
 
 
@@ -109,6 +112,15 @@ def lib() -> C.CDLL:
                                                        C.c_int32, dp]),
         "itercur_run_holds_matrix": (C.c_int32, [runp]),
         "itercur_copy_to_host": (C.c_int, [vp, vp, C.c_uint64]),
+        "itercur_shard_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, i64p, i64p]),
+        "itercur_iterative_cur_sharded_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                                           C.POINTER(Config), vp, vp, C.POINTER(runp)]),
+        "itercur_iterative_cur_sharded_emulated": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                                             C.POINTER(Config), vp, C.POINTER(runp)]),
+        "itercur_true_relative_error_sharded": (C.c_int, [runp, dp]),
+        "itercur_nccl_unique_id": (C.c_int, [vp]),
+        "itercur_nccl_comm_init": (C.c_int, [C.c_int32, vp, C.c_int32, C.POINTER(vp)]),
+        "itercur_nccl_comm_destroy": (C.c_int, [vp]),
         "itercur_fro_norm_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, dp]),
         "itercur_sketched_residual_device": (C.c_int, [runp, C.c_int64, C.c_uint64, C.c_int32, C.c_int32, dp]),
         "itercur_run_free": (None, [runp]),

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "../../include/itercur_b200.h"
+#include "collectives.h"
 #include "gemm.h"
 #include "kernels.h"
 #include "misc.h"
@@ -180,6 +181,22 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace
 
 // ====================================================================== the run handle
+// Column-sharded runs: A is split by columns into contiguous shards. A process
+// computes `nloc` of them: one (NCCL mode: one process per GPU, `world` ranks in `comm`) or all
+// of them on one device (emulation: every shard's kernels run on their own column range, the
+// collectives become the equivalent device copies). Replicated state (L, D_k, masks, I, J, the
+// loop control, Wc = Y^T(:, 0:b)) is identical everywhere; per-shard state (A, Y, R~) covers the
+// shard's columns only.
+struct ShardSpec {
+  bool active = false;
+  int nloc = 1;
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  int64_t n_total = 0;             // global column count
+  std::vector<int64_t> goff, cnt;  // local shards: global column offset and count
+  bool emulated() const { return active && comm == nullptr; }
+};
+
 struct itercur_run {
   int device = 0;
   cudaStream_t stream = nullptr;   // the caller's stream (accessors run on it)
@@ -208,11 +225,15 @@ struct itercur_run {
   DevBuf<int64_t> dI, dJ;
   int64_t ldL = 0, ldR = 0, capL = 0, bmax = 0;
   int64_t launches = 0;  // kernels of this library launched by the run (sketch + loop)
+  ShardSpec sh;          // column sharding (inactive: the plain single-device run)
 };
 
 namespace {
 
 int64_t even(int64_t x) { return x + (x & 1); }
+// The column partition of sharded runs: contiguous blocks of an even width (16-byte aligned
+// offsets), rank r owning [r * blk, min((r + 1) * blk, n)).
+int64_t shard_block(int64_t n, int world) { return round_up(ceil_div(n, world), 2); }
 
 // StoppingConfig defaults, proj/include/itercur/driver.hpp:18-26; SelectionMethod select.hpp:12-15
 itercur_config default_config() {
@@ -382,7 +403,7 @@ char* pinned_state(size_t bytes) {
 void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
   if (need <= run->capL) return;
   int64_t cap = std::max<int64_t>(run->capL * 2, need);
-  const int64_t maxcap = std::min(run->m, run->n) + run->bmax;
+  const int64_t maxcap = std::min(run->m, run->sh.active ? run->sh.n_total : run->n) + run->bmax;
   cap = std::min(cap, maxcap);
   if (cap < need) cap = need;
   cap = (cap + 1) & ~int64_t(1);  // even: 16-byte aligned gathered columns (lean GEMM loads)
@@ -413,25 +434,58 @@ double min_margin(const double* best, const double* second, int count) {
 void run_iterative_cur(itercur_run* run) {
   const itercur_config& cfg = run->cfg;
   cudaStream_t st = run->wstream;
-  const int64_t m = run->m, n = run->n, lda = run->lda;
+  const int64_t m = run->m, n = run->n, lda = run->lda;  // n: the columns this process holds
   const double* A = run->A;
   const auto t_start = std::chrono::steady_clock::now();
+  // column sharding; an unsharded run is one local shard covering A
+  ShardSpec& sh = run->sh;
+  if (!sh.active) {
+    sh.nloc = 1;
+    sh.goff.assign(1, 0);
+    sh.cnt.assign(1, n);
+    sh.n_total = n;
+  }
+  const int64_t n_glob = sh.n_total;
+  const bool emul = sh.emulated(), use_nccl = sh.active && sh.comm != nullptr;
+  const NcclApi* nc = use_nccl ? nccl_api() : nullptr;
+  if (use_nccl && !nc) fail(ITERCUR_E_CUDA, std::string("NCCL unavailable: ") + nccl_load_error());
+  auto nck = [&](ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(ITERCUR_E_CUDA, std::string("NCCL error '") + nc->GetErrorString(r) + "' (" + what + ")");
+  };
+  // a local shard's first column within this process's A / Y / R~ (emulation: all columns are local)
+  auto loc = [&](int s) -> int64_t { return emul ? sh.goff[s] : 0; };
+  // sum of host scalars over the ranks (NCCL mode; a no-op otherwise)
+  DevBuf<double> red;
+  red.alloc(4);
+  auto allreduce_host = [&](double* v, int k) {
+    if (!use_nccl) return;
+    CK(cudaMemcpyAsync(red.p, v, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    nck(nc->AllReduce(red.p, red.p, k, ncclDouble, ncclSum, sh.comm, st), "allreduce scalars");
+    CK(cudaMemcpyAsync(v, red.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  };
+  auto count_nonfinite_all = [&]() -> double {
+    DevBuf<unsigned long long> cnt;
+    cnt.alloc(1);
+    CK(launch_count_nonfinite(A, m, n, lda, cnt.p, st));
+    run->launches += 1;
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double hv = static_cast<double>(h);
+    allreduce_host(&hv, 1);
+    return hv;
+  };
 
   // ---- validation (driver.cpp:51-54, sketch.cpp:11-13), in the reference's order ----
   if (m == 0 || n == 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonempty");
   if (m < 0 || n < 0 || lda < std::max<int64_t>(m, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "invalid matrix shape");
   const bool cheap_fail = cfg.epsilon < 0.0 || cfg.b < 1 || cfg.b > m;
   if (cheap_fail) {
-    const double asq = device_sumsq(A, m, n, lda, st);
+    double asq = device_sumsq(A, m, n, lda, st);
+    allreduce_host(&asq, 1);
     if (!std::isfinite(asq)) {
-      DevBuf<unsigned long long> cnt;
-      cnt.alloc(1);
-      CK(launch_count_nonfinite(A, m, n, lda, cnt.p, st));
-      run->launches += 1;
-      unsigned long long h = 0;
-      CK(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (h) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
+      if (count_nonfinite_all() > 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
     }
     if (asq == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
     if (cfg.epsilon < 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "epsilon must be nonnegative");
@@ -440,7 +494,7 @@ void run_iterative_cur(itercur_run* run) {
   }
 
   const int64_t b = cfg.b;
-  const int64_t min_dim = std::min(m, n);
+  const int64_t min_dim = std::min(m, n_glob);
   const int64_t max_rank = cfg.max_rank > 0 ? std::min(cfg.max_rank, min_dim) : min_dim;
   const int64_t max_iters = cfg.max_iters > 0 ? cfg.max_iters : (min_dim + b - 1) / b + 1;
   const int64_t c = cfg.sketch_rows > 0 ? cfg.sketch_rows : sketch_rows(b);
@@ -455,34 +509,40 @@ void run_iterative_cur(itercur_run* run) {
   Events evs;
   evs.on = cfg.profile != 0;
   Workspace ws;
-  ws.scal.alloc(4);
+  const int nloc = sh.nloc;
+  ws.scal.alloc(2 * nloc + 2);
   ws.Y.alloc(static_cast<size_t>(cp) * n);
 
-  // ---- sketch (make_sketch, sketch.cpp:10-24), ||A|| fused ----
+  // ---- sketch (make_sketch, sketch.cpp:10-24), ||A|| fused; one apply per local shard (the
+  //      operator is regenerated from (seed, i) wherever it is needed) ----
   cudaEvent_t e_sk0 = evs.get(0), e_sk1 = evs.get(1);
   CK(cudaEventRecord(e_sk0, st));
   {
     const int kind = cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
     SketchBuffers sb;
-    SketchStats stats{ws.scal.p + 0, ws.scal.p + 1};
-    run->launches += apply_sketch(A, m, n, lda, kind, cfg.sparse_nnz, cfg.seed,
-                                  cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch, c,
-                                  cp, ws.Y.p, stats, sb, st);
+    for (int sI = 0; sI < nloc; ++sI) {
+      SketchStats stats{ws.scal.p + 2 * sI, ws.scal.p + 2 * sI + 1};
+      run->launches += apply_sketch(A + loc(sI) * lda, m, sh.cnt[sI], lda, kind, cfg.sparse_nnz, cfg.seed,
+                                    cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch,
+                                    c, cp, ws.Y.p + loc(sI) * cp, stats, sb, st, nullptr, sI > 0 && sb.S.p != nullptr);
+    }
   }
   CK(cudaEventRecord(e_sk1, st));
   double hs[2] = {0, 0};
-  CK(cudaMemcpyAsync(hs, ws.scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  {
+    std::vector<double> hp(2 * nloc);
+    CK(cudaMemcpyAsync(hp.data(), ws.scal.p, sizeof(double) * 2 * nloc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int sI = 0; sI < nloc; ++sI) {  // shard order (fixed)
+      hs[0] += hp[2 * sI];
+      hs[1] += hp[2 * sI + 1];
+    }
+    allreduce_host(hs, 2);
+  }
   ws.S.reset();
   ws.sk_ws.reset();
   if (!std::isfinite(hs[0])) {
-    ws.nonfinite.alloc(1);
-    CK(launch_count_nonfinite(A, m, n, lda, ws.nonfinite.p, st));
-    run->launches += 1;
-    unsigned long long h = 0;
-    CK(cudaMemcpyAsync(&h, ws.nonfinite.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (h) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
+    if (count_nonfinite_all() > 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
   }
   if (hs[0] == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
   run->a_norm = std::sqrt(hs[0]);
@@ -515,17 +575,23 @@ void run_iterative_cur(itercur_run* run) {
 
   // ---- workspaces ----
   const int B = static_cast<int>(b);
+  // ldn: this process's columns (Y, R~, the U block); ldng: the replicated Wc over all columns
+  // (NCCL mode: room for world equal blocks, so Wc's rows gather in place column by column)
   const int64_t ldn = even(n), ldm = even(m);
-  ws.Wc.alloc(static_cast<size_t>(ldn) * B);
+  const int64_t blk = use_nccl ? shard_block(n_glob, sh.world) : 0;  // rank r owns [r*blk, min((r+1)*blk, n))
+  const int64_t ldng = use_nccl ? std::max(even(n_glob), blk * sh.world) : even(n_glob);
+  ws.Wc.alloc(static_cast<size_t>(ldng) * B);
   ws.Wr.alloc(static_cast<size_t>(ldm) * B);
   ws.Ut.alloc(static_cast<size_t>(ldn) * B);
   ws.Yg.alloc(static_cast<size_t>(B) * cp);
-  ws.col_mask.alloc(n);
+  ws.col_mask.alloc(n_glob);
   ws.row_mask.alloc(m);
-  CK(cudaMemsetAsync(ws.col_mask.p, 0, n, st));
+  CK(cudaMemsetAsync(ws.col_mask.p, 0, n_glob, st));
   CK(cudaMemsetAsync(ws.row_mask.p, 0, m, st));
   ws.lupp_scratch.alloc(lupp_scratch_bytes(B));
   const bool col_qrcp = cfg.col_method == ITERCUR_PIVOT_QRCP, row_qrcp = cfg.row_method == ITERCUR_PIVOT_QRCP;
+  if (sh.active && (col_qrcp || row_qrcp))
+    fail(ITERCUR_E_INVALID_ARGUMENT, "column-sharded runs support LUPP selection only");
   if (col_qrcp || row_qrcp) ws.qrcp_scratch.alloc(qrcp_scratch_bytes());
   if (col_qrcp) ws.Wq.alloc(static_cast<size_t>(cp) * n);
   // iterations are enqueued in batches of kBatch without a host round trip; the loop control
@@ -575,6 +641,20 @@ void run_iterative_cur(itercur_run* run) {
     grow_factors(run, first, st);
   }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+  // sharded runs: the selected block's columns [A(:,J_k) | R~(0:r,J_k) | Y(:,J_k)] assembled from
+  // their owners (NCCL: one sum-allreduce of disjoint contributions; emulation: each shard writes
+  // its own columns), replacing the single-device gathers
+  DevBuf<double> pack;
+  int64_t pack_ldr = 0;
+  auto alloc_pack = [&]() {
+    if (!sh.active) return;
+    pack_ldr = run->capL;
+    pack.alloc(static_cast<size_t>(ldm + pack_ldr + cp) * B);
+  };
+  alloc_pack();
+  auto packA = [&]() { return pack.p; };
+  auto packR = [&]() { return pack.p + ldm * B; };
+  auto packY = [&]() { return pack.p + (ldm + pack_ldr) * B; };
   // row-major copy of A (when it is a modest share of free HBM): the U block's base A(I_k, :)
   // then reads |I_k| contiguous rows instead of one DRAM burst per element (~8 us per
   // iteration at config 2).
@@ -630,6 +710,14 @@ void run_iterative_cur(itercur_run* run) {
     p.src = A;
     p.lds = lda;
     p.idx = arr.col_idx;
+    if (sh.active) {  // the assembled block: base A(:, J_k) and R~(:, J_k) contiguous
+      p.B = packR();
+      p.base_mode = kBaseContigCols;
+      p.src = packA();
+      p.lds = ldm;
+      p.col0 = 0;
+      p.idx = nullptr;
+    }
     p.alpha = -1.0;
     p.out_mode = kOutColMajor;
     p.C0 = run->L.p;
@@ -642,26 +730,30 @@ void run_iterative_cur(itercur_run* run) {
     return p;
   };
   // the fused U-block kernel (GEMM2 + solves + downdate) when the shape qualifies
-  auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr) {
+  // per local shard: its columns of Y / R~ / A (this process's buffers at column loc(s)) and its
+  // rows of the replicated Wc (global offset goff[s]); the ||Y||^2 partials of shard s at poff[s]
+  std::vector<int64_t> poff(nloc + 1, 0);
+  auto ublock_params = [&](int64_t ldbg, IterState* slot, const IterArrays& arr, int sI) {
+    const int64_t lo = loc(sI);
     TsGemmParams p;
-    p.M = n;
+    p.M = sh.cnt[sI];
     p.K = ldbg;
     p.ctl = d_ctl;
     p.k_from_r = 1;
     p.N = B;
     p.d_n = &slot->width;
-    p.A = run->Rt.p;
+    p.A = run->Rt.p + lo;
     p.lda = run->ldR;
     p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
     p.bsk = 1;
     p.bsn = ldbg;
     if (ws.At.p) {  // A(I_k[q], j) = At(j, I_k[q])
       p.base_mode = kBaseGatherCols;
-      p.src = ws.At.p;
+      p.src = ws.At.p + lo;
       p.lds = ws.ldAt;
     } else {
       p.base_mode = kBaseGatherRowsT;
-      p.src = A;
+      p.src = A + lo * lda;
       p.lds = lda;
     }
     p.idx = arr.row_idx;
@@ -669,33 +761,51 @@ void run_iterative_cur(itercur_run* run) {
     p.out_mode = kOutNone;
     p.lu = run->Dinv.p;
     p.ldd = run->bmax;
-    p.rt = run->Rt.p;
+    p.rt = run->Rt.p + lo;
     p.ldr = run->ldR;
-    p.yg = ws.Yg.p;
+    p.yg = sh.active ? packY() : ws.Yg.p;
     p.ycp = static_cast<int>(cp);
-    p.y = ws.Y.p;
-    p.Wc = ws.Wc.p;
-    p.ldwc = ldn;
+    p.y = ws.Y.p + lo * cp;
+    p.Wc = ws.Wc.p + sh.goff[sI];
+    p.ldwc = ldng;
     p.wc_rows = B;
-    p.norm_part = ws.part.p;
+    p.norm_part = ws.part.p + poff[sI];
     p.dbg = ub_dbg.p;
     p.dbg_k = ub_trace_k;
     return p;
   };
   const bool fused_ub = !env_flag("ITERCUR_NO_FUSED_UBLOCK") && !row_qrcp && [&] {
     IterState* slot0 = reinterpret_cast<IterState*>(slots);
-    TsGemmParams p = ublock_params(run->capL, slot0, iter_arrays(slot0, B));
-    p.norm_part = reinterpret_cast<double*>(16);  // placeholder: allocated below
-    return ts_gemm_ublock_supported(p) && (run->capL & 1) == 0;
+    bool ok = (run->capL & 1) == 0;
+    for (int sI = 0; sI < nloc && ok; ++sI) {
+      TsGemmParams p = ublock_params(run->capL, slot0, iter_arrays(slot0, B), sI);
+      p.norm_part = reinterpret_cast<double*>(16);  // placeholder: allocated below
+      ok = ts_gemm_ublock_supported(p);
+    }
+    return ok;
   }();
-  const int64_t y_parts = fused_ub ? ts_gemm_ublock_parts(n) : ts_gemm_grid_size(n, static_cast<int>(cp));
-  ws.part.alloc(std::max<int64_t>(y_parts, 1));
+  for (int sI = 0; sI < nloc; ++sI)
+    poff[sI + 1] = poff[sI] + (fused_ub ? ts_gemm_ublock_parts(sh.cnt[sI]) : ts_gemm_grid_size(sh.cnt[sI], static_cast<int>(cp)));
+  const int64_t y_parts = poff[nloc];
+  ws.part.alloc(std::max<int64_t>(y_parts, 1) + 1);  // + the rank-local sum (NCCL mode)
   ws.commit_counter.alloc(1);
   CK(cudaMemsetAsync(ws.commit_counter.p, 0, sizeof(int), st));
+  // NCCL mode: the ranks' rows of Wc gathered in place, one allgather per column (equal blocks)
+  auto allgather_wc = [&]() {
+    if (!use_nccl) return;
+    nck(nc->GroupStart(), "group start");
+    for (int h = 0; h < B; ++h)
+      nck(nc->AllGather(ws.Wc.p + h * ldng + sh.rank * blk, ws.Wc.p + h * ldng, blk, ncclDouble, sh.comm, st),
+          "allgather Wc");
+    nck(nc->GroupEnd(), "group end");
+  };
 
   // initial Wc = Y^T(:, 0:b)
-  CK(launch_transpose_rows(ws.Y.p, cp, n, B, ws.Wc.p, ldn, st));
-  run->launches += 1;
+  for (int sI = 0; sI < nloc; ++sI) {
+    CK(launch_transpose_rows(ws.Y.p + loc(sI) * cp, cp, sh.cnt[sI], B, ws.Wc.p + sh.goff[sI], ldng, st));
+    run->launches += 1;
+  }
+  allgather_wc();
 
   const uint8_t epoch = 2;  // the global-memory LUPP clears its in-call marks, so one epoch suffices
   static uint32_t run_counter = 0;
@@ -709,8 +819,8 @@ void run_iterative_cur(itercur_run* run) {
     int64_t launches = 0;
   };
   struct GraphCache {
-    std::vector<std::pair<int, GraphEntry>> v;
-    GraphEntry* find(int sig) {
+    std::vector<std::pair<int64_t, GraphEntry>> v;
+    GraphEntry* find(int64_t sig) {
       for (auto& e : v)
         if (e.first == sig) return &e.second;
       return nullptr;
@@ -743,6 +853,7 @@ void run_iterative_cur(itercur_run* run) {
     if (need > run->capL) {
       grow_factors(run, need, st);
       ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
+      alloc_pack();
       t_grow = us_since(tb0);
     }
     const bool at_new = maybe_make_rowmajor_a(k_host);  // (re-capture: the U block's base changes)
@@ -758,16 +869,18 @@ void run_iterative_cur(itercur_run* run) {
       const IterArrays arr0 = iter_arrays(slot0, B);
       TsGemmParams g1 = gemm1_params(ldbg, slot0, arr0);
       g1.k_plan = kp;
-      int sig = ts_gemm_planned_splits(g1, false);
+      int64_t sig = ts_gemm_planned_splits(g1, false);
       if (fused_ub) {
-        TsGemmParams ub = ublock_params(ldbg, slot0, arr0);
-        ub.k_plan = kp;
-        sig = sig * 64 + ts_gemm_planned_splits(ub, true);
+        for (int sI = 0; sI < nloc; ++sI) {  // every shard's U block (their M may differ)
+          TsGemmParams ub = ublock_params(ldbg, slot0, arr0, sI);
+          ub.k_plan = kp;
+          sig = sig * 131 + ts_gemm_planned_splits(ub, true);
+        }
       }
       return sig;
     };
     int64_t k_plan = k_plan_for(r_host);
-    const int plan_sig = plan_sig_for(k_plan);
+    const int64_t plan_sig = plan_sig_for(k_plan);
     // the iteration kernels of one batch; captured once into a CUDA graph (re-captured only
     // when the factor buffers grow) and replayed, so a batch costs one graph launch
     int64_t batch_launches = 0;
@@ -775,6 +888,22 @@ void run_iterative_cur(itercur_run* run) {
     // than separate grid-wide gather launches inside the batch graphs (config 2: 39.4 vs
     // 38.8 ms; the strided gathers then run on the cluster's 16 SMs only), so opt-in
     static const bool fuse_off = !env_flag("ITERCUR_LUPP_FUSION");
+    // the iteration commit (||Y||^2 from the partials, stop tests, index append); NCCL mode: the
+    // rank's partials summed in a fixed order, then summed over the ranks, then the commit; and the
+    // ranks' rows of the downdated Wc gathered for the next column selection
+    auto commit_iteration = [&](IterState* slot, const IterArrays& arr) {
+      if (use_nccl) {
+        double* mine = ws.part.p + y_parts;
+        CK(launch_sum_partials(ws.part.p, y_parts, mine, st, d_ctl));
+        nck(nc->AllReduce(mine, mine, 1, ncclDouble, ncclSum, sh.comm, st), "allreduce ||Y||^2");
+        CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, mine, 1, st));
+        allgather_wc();
+        batch_launches += 1;
+      } else {
+        CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
+                         st));
+      }
+    };
     auto enqueue_batch = [&]() {
       // programmatic dependent launch along the iteration's kernel chain: measured neutral to
       // slightly slower inside the batch graphs on B200 (config 2: 38.5 vs 38.3 ms), so opt-in
@@ -797,8 +926,8 @@ void run_iterative_cur(itercur_run* run) {
         {
           LuppArgs la{};
           la.W = ws.Wc.p;
-          la.rows = n;
-          la.ldw = ldn;
+          la.rows = n_glob;
+          la.ldw = ldng;
           la.cols_max = B;
           la.d_steps = &d_ctl->block;
           la.mask = ws.col_mask.p;
@@ -813,7 +942,7 @@ void run_iterative_cur(itercur_run* run) {
           la.gen_base = gen_base;
           la.gen_which = 0;
           const bool fusable = !col_qrcp && fused_ub && lupp_fuses_iteration_work(la);
-          col_fused = fusable && !fuse_off;
+          col_fused = fusable && !fuse_off && !sh.active;  // sharded: the block is packed instead
           // the iteration begin alone (no gathers) folded into the cluster LUPP
           // (measured: column-selection phase 6.90 -> 6.57 ms at config 2; ITERCUR_NO_LUPP_FUSE_BEGIN)
           static const bool begin_only = !env_flag("ITERCUR_NO_LUPP_FUSE_BEGIN");
@@ -842,14 +971,29 @@ void run_iterative_cur(itercur_run* run) {
         // (2) row residual S_row = A(:,J_k) - L * Rt(:,J_k)  (row_residual, sketch.cpp:43-60);
         //     Rt(:,J_k) is gathered once into a contiguous K x w block (a strided gather inside
         //     the GEMM loader would re-fetch one 32-B sector per element in every CTA)
-        if (!col_fused)
+        if (sh.active) {
+          // the block's columns from their owners: A(:,J_k), R~(0:r,J_k), Y(:,J_k) (all of J_k
+          // is replicated after the column selection); NCCL: one sum-allreduce of the packs
+          for (int sI = 0; sI < nloc; ++sI) {
+            const int64_t lo = loc(sI);
+            CK(launch_pack_owned(d_ctl, &slot->ncols, arr.col_idx, B, sh.goff[sI], sh.cnt[sI], A + lo * lda, lda, m,
+                                 run->Rt.p + lo, run->ldR, ldbg, ws.Y.p + lo * cp, cp, packA(), ldm, packR(), pack_ldr,
+                                 packY(), use_nccl, st));
+            batch_launches += 1;
+          }
+          if (use_nccl)
+            nck(nc->AllReduce(pack.p, pack.p, static_cast<size_t>(ldm + pack_ldr + cp) * B, ncclDouble, ncclSum,
+                              sh.comm, st),
+                "allreduce block");
+        } else if (!col_fused) {
           CK(launch_gather(run->Rt.p, run->ldR, 1, ldbg, arr.col_idx, &slot->ncols, B, ws.Bg.p, ldbg, st, d_ctl, true));
+        }
         // Y(:, J_k) for the U block's downdate on a side branch: it needs only J_k, so it can run
         // beside the row residual and the row selection (joined before the U block). Measured
         // slower inside the batch graphs (config 2: 35.6 vs 32.6 ms; the concurrent kernel delays
         // the cluster launches), so opt-in: ITERCUR_SIDE_GATHER
         static const bool y_branch = env_flag("ITERCUR_SIDE_GATHER");
-        const bool y_side = fused_ub && !col_fused && y_branch;
+        const bool y_side = fused_ub && !col_fused && y_branch && !sh.active;
         if (y_side) {
           SideStream& ss = side_stream();
           CK(cudaEventRecord(ss.fork, st));
@@ -910,7 +1054,7 @@ void run_iterative_cur(itercur_run* run) {
           CK(launch_cross_lu(run->L.p, run->ldL, arr.row_idx, &slot->width, B, run->Dinv.p, run->bmax, st, d_ctl,
                              run->Piv.p));
         static const bool pair_off = env_flag("ITERCUR_NO_PAIR_GATHER");  // A/B
-        const bool y_here = fused_ub && !y_side && !col_fused;  // Y(:, J_k) gathered right before the U block
+        const bool y_here = fused_ub && !y_side && !col_fused && !sh.active;  // Y(:, J_k) gathered before the U block
         if (!row_fused && y_here && !pair_off)  // L(I_k, :)^T and Y(:, J_k) in one launch
           CK(launch_gather_pair(run->L.p, run->ldL, 1, ldbg, arr.row_idx, ws.Bg.p, ldbg, true, ws.Y.p, 1, cp, cp,
                                 arr.col_idx, ws.Yg.p, cp, false, &slot->width, B, st, d_ctl));
@@ -923,12 +1067,13 @@ void run_iterative_cur(itercur_run* run) {
             CK(cudaStreamWaitEvent(st, side_stream().join, 0));
           else if (y_here && (row_fused || pair_off))
             CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
-          TsGemmParams p = ublock_params(ldbg, slot, arr);
+          TsGemmParams p = ublock_params(ldbg, slot, arr, 0);
           p.k_plan = k_plan;
           // the commit in the U block's last CTA instead of its own kernel: measured slower
           // (config 2 phase sums 32.17 vs 31.60 ms: every CTA's release fence before its arrival
           // lengthens the kernel more than the launch it saves), so opt-in: ITERCUR_FUSED_COMMIT
-          static const bool fused_commit = env_flag("ITERCUR_FUSED_COMMIT");
+          static const bool fused_commit_env = env_flag("ITERCUR_FUSED_COMMIT");
+          const bool fused_commit = fused_commit_env && !sh.active;
           if (fused_commit) {
             p.commit.ctl = d_ctl;
             p.commit.slot = slot;
@@ -941,81 +1086,88 @@ void run_iterative_cur(itercur_run* run) {
             p.commit.counter = ws.commit_counter.p;
           }
           CK(run_ts_gemm_ublock(p, st));
+          for (int sI = 1; sI < nloc; ++sI) {  // the other local shards' U blocks (emulation)
+            TsGemmParams ps = ublock_params(ldbg, slot, arr, sI);
+            ps.k_plan = k_plan;
+            CK(run_ts_gemm_ublock(ps, st));
+          }
           batch_launches += 9 + (row_lupp_path >= 0 ? 1 : 0) - (col_fused ? 2 : 0) - (begin_fused ? 1 : 0) -
-                            (row_fused ? 1 : 0) - ((!row_fused && y_here && !pair_off) ? 1 : 0);
+                            (row_fused ? 1 : 0) - ((!row_fused && y_here && !pair_off) ? 1 : 0) + (nloc - 1) -
+                            (sh.active ? 2 : 0);
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
           if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));  // downdate fused into the core step
           if (!fused_commit) {
-            CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p,
-                             y_parts, st));
+            commit_iteration(slot, arr);
           } else {
             batch_launches -= 1;
           }
           continue;
         }
-        {
+        for (int sI = 0; sI < nloc; ++sI) {
+          const int64_t lo = loc(sI);
           TsGemmParams p;
-          p.M = n;
+          p.M = sh.cnt[sI];
           p.K = ldbg;
           p.ctl = d_ctl;
           p.k_from_r = 1;
           p.N = B;
           p.d_n = &slot->width;
-          p.A = run->Rt.p;
+          p.A = run->Rt.p + lo;
           p.lda = run->ldR;
           p.B = ws.Bg.p;  // B(k, q) = L(I_k[q], k)
           p.bsk = 1;
           p.bsn = ldbg;
           if (ws.At.p) {
             p.base_mode = kBaseGatherCols;
-            p.src = ws.At.p;
+            p.src = ws.At.p + lo;
             p.lds = ws.ldAt;
           } else {
             p.base_mode = kBaseGatherRowsT;
-            p.src = A;
+            p.src = A + lo * lda;
             p.lds = lda;
           }
           p.idx = arr.row_idx;
           p.alpha = -1.0;
           p.out_mode = kOutColMajor;
-          p.C0 = ws.Ut.p;
+          p.C0 = ws.Ut.p + lo;
           p.ldc0 = ldn;
           CK(run_ts_gemm(p, st));
+          CK(launch_rows_lu_solve(ws.Ut.p + lo, ldn, sh.cnt[sI], run->Dinv.p, run->bmax, &slot->width, B,
+                                  run->Rt.p + lo, run->ldR, st, d_ctl, run->ldR, run->Piv.p));
         }
-        CK(launch_rows_lu_solve(ws.Ut.p, ldn, n, run->Dinv.p, run->bmax, &slot->width, B, run->Rt.p, run->ldR, st,
-                                d_ctl, run->ldR, run->Piv.p));
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 4), st));
 
         // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
         //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
-        CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
-        {
+        if (!sh.active)
+          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+        for (int sI = 0; sI < nloc; ++sI) {
+          const int64_t lo = loc(sI);
           TsGemmParams p;
-          p.M = n;
+          p.M = sh.cnt[sI];
           p.K = B;
           p.d_k = &slot->width;
           p.ctl = d_ctl;
           p.N = static_cast<int>(cp);
-          p.A = run->Rt.p;
+          p.A = run->Rt.p + lo;
           p.a_off_per_r = run->ldR;
           p.lda = run->ldR;
-          p.B = ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
+          p.B = sh.active ? packY() : ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
           p.bsk = cp;
           p.bsn = 1;
           p.base_mode = kBaseInPlaceRowMajor;
           p.alpha = -1.0;
           p.out_mode = kOutRowMajor;
-          p.C0 = ws.Y.p;
+          p.C0 = ws.Y.p + lo * cp;
           p.ldc0 = cp;
-          p.Wc = ws.Wc.p;
-          p.ldwc = ldn;
+          p.Wc = ws.Wc.p + sh.goff[sI];
+          p.ldwc = ldng;
           p.wc_rows = B;
-          p.norm_part = ws.part.p;
+          p.norm_part = ws.part.p + poff[sI];
           CK(run_ts_gemm(p, st));
         }
-        CK(launch_commit(d_ctl, slot, arr, run->dI.p, run->dJ.p, ws.row_mask.p, ws.col_mask.p, ws.part.p, y_parts,
-                         st));
-        batch_launches += 11 + (row_lupp_path >= 0 ? 1 : 0);
+        commit_iteration(slot, arr);
+        batch_launches += 11 + (row_lupp_path >= 0 ? 1 : 0) + 3 * (nloc - 1) - (sh.active ? 2 : 0);
         if (evs.on) CK(cudaEventRecord(evs.get(e0 + 5), st));
       }
     };
@@ -1063,7 +1215,7 @@ void run_iterative_cur(itercur_run* run) {
     // most r + 2 batches of b), if the capacity will not have to grow first
     if (use_graph && std::min(r_host + 2 * static_cast<int64_t>(kBatch) * b, max_rank + b) <= run->capL) {
       const int64_t kn = k_plan_for(r_host + static_cast<int64_t>(kBatch) * b);
-      const int sn = plan_sig_for(kn);
+      const int64_t sn = plan_sig_for(kn);
       if (!graphs.find(sn)) {
         const auto tp = hclock::now();
         graphs.v.emplace_back(sn, capture(kn));
@@ -1195,6 +1347,15 @@ void release_input_copy(itercur_run* run) {
   run->A_owned.reset();
   run->A = nullptr;
   CK(cudaStreamSynchronize(st));
+}
+
+// A rank of an NCCL-sharded run holds only its columns of A, Y and R~: exports that need the whole
+// factors are collective operations it does not provide (indices, trace and the collective
+// itercur_true_relative_error_sharded are available).
+void require_whole_factors(const itercur_run* run, const char* what) {
+  if (run->sh.active && run->sh.comm)
+    fail(ITERCUR_E_LOGIC, std::string(what) + ": a rank of a column-sharded run holds only its shard's columns "
+                                              "(use itercur_true_relative_error_sharded)");
 }
 
 void gather_host(const itercur_run* run, const double* src, int64_t row_stride, int64_t col_stride, int64_t K,
@@ -1516,6 +1677,160 @@ int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t
   });
 }
 
+int itercur_shard_range(int64_t n_total, int32_t world, int32_t rank, int64_t* offset, int64_t* count) {
+  return guarded([&] {
+    if (n_total < 1 || world < 1 || rank < 0 || rank >= world)
+      fail(ITERCUR_E_INVALID_ARGUMENT, "shard_range: invalid arguments");
+    const int64_t blk = shard_block(n_total, world);
+    const int64_t off = std::min<int64_t>(n_total, static_cast<int64_t>(rank) * blk);
+    *offset = off;
+    *count = std::min<int64_t>(blk, n_total - off);
+  });
+}
+
+namespace {
+void start_run(itercur_run* run, const double* dA, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
+               void* stream) {
+  CK(cudaGetDevice(&run->device));
+  run->stream = static_cast<cudaStream_t>(stream);
+  run->wstream = work_stream();
+  {  // the work stream starts after everything already queued on the caller's stream
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, run->stream));
+    CK(cudaStreamWaitEvent(run->wstream, ev, 0));
+    cudaEventDestroy(ev);
+  }
+  run->m = m;
+  run->n = n;
+  run->lda = lda;
+  run->A = dA;
+  run->cfg = cfg ? *cfg : default_config();
+  configure_mempool_once();
+  g_alloc_stream = run->wstream;
+}
+}  // namespace
+
+int itercur_iterative_cur_sharded_device(const double* dA, int64_t m, int64_t n_local, int64_t lda, int64_t n_total,
+                                         const itercur_config* cfg, void* comm, void* stream, itercur_run** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require_device();
+    const NcclApi* nc = nccl_api();
+    if (!nc) fail(ITERCUR_E_CUDA, std::string("NCCL unavailable: ") + nccl_load_error());
+    if (!comm) fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: null communicator");
+    auto run = std::make_unique<itercur_run>();
+    ShardSpec& sh = run->sh;
+    sh.active = true;
+    sh.comm = static_cast<ncclComm_t>(comm);
+    if (nc->CommCount(sh.comm, &sh.world) != ncclSuccess || nc->CommUserRank(sh.comm, &sh.rank) != ncclSuccess)
+      fail(ITERCUR_E_CUDA, "sharded run: cannot query the communicator");
+    if (n_total < 2 * sh.world) fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: fewer than 2 columns per rank");
+    const int64_t blk = shard_block(n_total, sh.world);
+    const int64_t off = std::min<int64_t>(n_total, static_cast<int64_t>(sh.rank) * blk);
+    if (n_local != std::min<int64_t>(blk, n_total - off) || n_local < 1)
+      fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: this rank's block must be columns [" + std::to_string(off) + ", " +
+                                           std::to_string(off + std::min<int64_t>(blk, n_total - off)) +
+                                           ") (itercur_shard_range)");
+    sh.nloc = 1;
+    sh.n_total = n_total;
+    sh.goff.assign(1, off);
+    sh.cnt.assign(1, n_local);
+    start_run(run.get(), dA, m, n_local, lda, cfg, stream);
+    if (run->cfg.observer) fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: no iteration observer");
+    run_iterative_cur(run.get());
+    *out = run.release();
+  });
+}
+
+int itercur_iterative_cur_sharded_emulated(const double* dA, int64_t m, int64_t n, int64_t lda, int32_t shards,
+                                           const itercur_config* cfg, void* stream, itercur_run** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require_device();
+    if (shards < 1 || n < 2 * static_cast<int64_t>(shards))
+      fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: fewer than 2 columns per shard");
+    auto run = std::make_unique<itercur_run>();
+    ShardSpec& sh = run->sh;
+    sh.active = true;
+    sh.nloc = shards;
+    sh.n_total = n;
+    const int64_t blk = shard_block(n, shards);
+    for (int s = 0; s < shards; ++s) {
+      const int64_t off = std::min<int64_t>(n, s * blk);
+      sh.goff.push_back(off);
+      sh.cnt.push_back(std::min<int64_t>(blk, n - off));
+      if (sh.cnt.back() < 1) fail(ITERCUR_E_INVALID_ARGUMENT, "sharded run: an empty shard");
+    }
+    start_run(run.get(), dA, m, n, lda, cfg, stream);
+    run_iterative_cur(run.get());
+    *out = run.release();
+  });
+}
+
+int itercur_true_relative_error_sharded(const itercur_run* run, double* out) {
+  return guarded([&] {
+    if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    CK(cudaSetDevice(run->device));
+    g_alloc_stream = run->stream;
+    if (!(run->sh.active && run->sh.comm)) {  // the whole factors are local
+      if (!run->A) fail(ITERCUR_E_LOGIC, "the run released its device copy of A");
+      *out = true_error_impl(run, run->A, run->lda, true);
+      return;
+    }
+    // this rank's ||A_s||^2 and ||A_s - L R~_s||^2, summed over the ranks (driver.cpp:169-190)
+    cudaStream_t st = run->stream;
+    const NcclApi* nc = nccl_api();
+    DevBuf<double> part, outd;
+    outd.alloc(2);
+    DevBuf<double> apart;
+    apart.alloc(148 * 8);
+    CK(launch_sumsq(run->A, run->m, run->n, run->lda, apart.p, 148 * 8, outd.p, st));
+    if (run->r > 0) {
+      residual_sumsq_panel(run, run->A, run->lda, 0, run->n, part, outd.p + 1, st);
+    } else {
+      CK(cudaMemsetAsync(outd.p + 1, 0, sizeof(double), st));
+    }
+    if (nc->AllReduce(outd.p, outd.p, 2, ncclDouble, ncclSum, run->sh.comm, st) != ncclSuccess)
+      fail(ITERCUR_E_CUDA, "NCCL allreduce failed (true_relative_error_sharded)");
+    double h[2];
+    CK(cudaMemcpyAsync(h, outd.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double a_norm = std::sqrt(h[0]);
+    *out = a_norm == 0.0 ? 0.0 : (run->r == 0 ? 1.0 : std::sqrt(h[1]) / a_norm);
+  });
+}
+
+int itercur_nccl_unique_id(void* id_out) {
+  return guarded([&] {
+    const NcclApi* nc = nccl_api();
+    if (!nc) fail(ITERCUR_E_CUDA, std::string("NCCL unavailable: ") + nccl_load_error());
+    ncclUniqueId id;
+    if (nc->GetUniqueId(&id) != ncclSuccess) fail(ITERCUR_E_CUDA, "ncclGetUniqueId failed");
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+int itercur_nccl_comm_init(int32_t world, const void* id_in, int32_t rank, void** comm_out) {
+  *comm_out = nullptr;
+  return guarded([&] {
+    require_device();
+    const NcclApi* nc = nccl_api();
+    if (!nc) fail(ITERCUR_E_CUDA, std::string("NCCL unavailable: ") + nccl_load_error());
+    ncclUniqueId id;
+    std::memcpy(&id, id_in, sizeof(id));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = nc->CommInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) fail(ITERCUR_E_CUDA, std::string("ncclCommInitRank: ") + nc->GetErrorString(r));
+    *comm_out = comm;
+  });
+}
+int itercur_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    const NcclApi* nc = nccl_api();
+    if (nc && comm) nc->CommDestroy(static_cast<ncclComm_t>(comm));
+  });
+}
+
 int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
                                itercur_run** out) {
   *out = nullptr;
@@ -1587,6 +1902,7 @@ int itercur_run_steps(const itercur_run* run, int32_t* kind, int64_t* iter, int6
 int itercur_run_c_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "c_matrix");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     // C(i, q) = A(i, J[q]): out(k=i, q) = A[i * 1 + J[q] * lda]
@@ -1601,6 +1917,7 @@ int itercur_run_c_matrix(const itercur_run* run, double* out) {
 int itercur_run_r_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "r_matrix");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     // R^T(j, q) = A(I[q], j): gathered as (n x r), then transposed on the host
@@ -1618,6 +1935,7 @@ int itercur_run_r_matrix(const itercur_run* run, double* out) {
 int itercur_run_core_matrix(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "core_matrix");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     core_matrix_impl(run, out);
@@ -1626,6 +1944,7 @@ int itercur_run_core_matrix(const itercur_run* run, double* out) {
 int itercur_true_relative_error_device(const itercur_run* run, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "true_relative_error");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
     if (!run->A)
@@ -1638,6 +1957,7 @@ int itercur_true_relative_error_matrix(const itercur_run* run, const double* A, 
                                        int32_t a_on_device, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "true_relative_error");
     if (m != run->m || n != run->n)
       fail(ITERCUR_E_INVALID_ARGUMENT, "true_relative_error: matrix is " + std::to_string(m) + "x" +
                                            std::to_string(n) + ", factors are for " + std::to_string(run->m) + "x" +
@@ -1652,6 +1972,7 @@ int itercur_run_core_apply(const itercur_run* run, int32_t transposed, const dou
                            double* out, int64_t ldo) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "core_apply");
     if (k < 0 || ldr < std::max<int64_t>(run->r, 1) || ldo < std::max<int64_t>(run->r, 1))
       fail(ITERCUR_E_INVALID_ARGUMENT, "core_apply: invalid shape");
     CK(cudaSetDevice(run->device));
@@ -1665,6 +1986,7 @@ int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;
+    require_whole_factors(run, "sketched_residual");
     if (!run->A)
       fail(ITERCUR_E_LOGIC, "the run released its device copy of A (host entry): pass the matrix to "
                             "itercur_sketched_residual_matrix");
@@ -1675,6 +1997,7 @@ int itercur_sketched_residual_matrix(const itercur_run* run, const double* dA, i
                                      int32_t kind, int32_t sparse_nnz, double* out) {
   return guarded([&] {
     if (!run) fail(ITERCUR_E_LOGIC, "null run");
+    require_whole_factors(run, "sketched_residual");
     if (!dA || lda < std::max<int64_t>(run->m, 1)) fail(ITERCUR_E_INVALID_ARGUMENT, "sketched residual: invalid matrix");
     CK(cudaSetDevice(run->device));
     g_alloc_stream = run->stream;

@@ -502,6 +502,47 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
   return e;
 }
 
+// Column-sharded engine: this shard's columns of the selected block J_k. For q < ncols with
+// j = J_k[q] - goff in [0, cnt): PackA(:, q) = A(:, j), PackR(0:r, q) = R~(0:r, j) (R~ row-major,
+// ld ldR), PackY(:, q) = Y(:, j). zero_rest: the other shards' columns are written as zeros, so a
+// sum-allreduce over the ranks assembles the block exactly (disjoint contributions + 0).
+__global__ void pack_owned_kernel(const IterCtl* __restrict__ ctl, const int* __restrict__ d_ncols,
+                                  const int64_t* __restrict__ col_idx, int64_t goff, int64_t cnt,
+                                  const double* __restrict__ A, int64_t lda, int64_t m,
+                                  const double* __restrict__ Rt, int64_t ldR, const double* __restrict__ Y,
+                                  int64_t cp, double* __restrict__ PackA, int64_t ldpa, double* __restrict__ PackR,
+                                  int64_t ldpr, double* __restrict__ PackY, int zero_rest) {
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl->done) return;
+  const int q = blockIdx.y;
+  if (q >= *d_ncols) return;
+  const int64_t j = col_idx[q] - goff;
+  const bool owned = j >= 0 && j < cnt;
+  if (!owned && !zero_rest) return;
+  const int64_t r = ctl->r;
+  const int64_t total = m + r + cp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < m) {
+      PackA[e + q * ldpa] = owned ? A[e + j * lda] : 0.0;
+    } else if (e < m + r) {
+      const int64_t k = e - m;
+      PackR[k + q * ldpr] = owned ? Rt[k * ldR + j] : 0.0;
+    } else {
+      const int64_t h = e - m - r;
+      PackY[h + q * cp] = owned ? Y[h + j * cp] : 0.0;
+    }
+  }
+}
+cudaError_t launch_pack_owned(const IterCtl* ctl, const int* d_ncols, const int64_t* col_idx, int B, int64_t goff,
+                              int64_t cnt, const double* A, int64_t lda, int64_t m, const double* Rt, int64_t ldR,
+                              int64_t r_cap, const double* Y, int64_t cp, double* PackA, int64_t ldpa, double* PackR,
+                              int64_t ldpr, double* PackY, bool zero_rest, cudaStream_t st) {
+  const int bx = static_cast<int>(std::min<int64_t>(ceil_div(m + r_cap + cp, 256), 64));
+  return launch_ex(pack_owned_kernel, dim3(std::max(bx, 1), B), dim3(256), 0, st, dim3(0, 0, 0), ctl, d_ncols, col_idx,
+                   goff, cnt, A, lda, m, Rt, ldR, Y, cp, PackA, ldpa, PackR, ldpr, PackY, zero_rest ? 1 : 0);
+}
+
 // CSR (row_ptr, col_idx, values; proj/src/matrix.cpp:79-104 layout) -> dense column-major
 // (the output must be zeroed by the caller); one thread per row.
 __global__ void csr_to_dense_kernel(int64_t rows, const int64_t* __restrict__ row_ptr,

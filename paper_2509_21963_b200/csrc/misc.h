@@ -159,6 +159,12 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
                                  const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
                                  const IterCtl* ctl = nullptr, int64_t out_off_per_r = 0,
                                  const int* perm = nullptr);
+// Column-sharded engine: this shard's columns of the selected block J_k into the packed block
+// [A(:, J_k) | R~(0:r, J_k) | Y(:, J_k)] (misc.cu pack_owned_kernel); zero_rest for a sum-allreduce.
+cudaError_t launch_pack_owned(const IterCtl* ctl, const int* d_ncols, const int64_t* col_idx, int B, int64_t goff,
+                              int64_t cnt, const double* A, int64_t lda, int64_t m, const double* Rt, int64_t ldR,
+                              int64_t r_cap, const double* Y, int64_t cp, double* PackA, int64_t ldpa, double* PackR,
+                              int64_t ldpr, double* PackY, bool zero_rest, cudaStream_t st);
 cudaError_t launch_sum_partials(const double* partials, int64_t count, double* d_out, cudaStream_t st,
                                 const IterCtl* ctl = nullptr);
 cudaError_t launch_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partials, int max_parts,

@@ -20,10 +20,22 @@ sharding needs:
 I and J are identical to the single-device run unless a ρ or floor comparison sits within
 rounding of its threshold (the norms are sums over shards in a different order).
 
-The per-rank stages run on the B200 kernels of libitercur_b200.so through `DeviceBackend`;
-torch.distributed carries the exchanges (NCCL on GPUs). The host-side logic is exercised on
-CPU with gloo and a test-only backend (tests/sharded_cpu_backend.py); the product has no
-CPU path.
+Two executions of this protocol:
+
+* the product path (`iterative_cur_sharded` on CUDA tensors, no `backend`): the whole loop runs in
+  the C++ engine (csrc/engine.cu, itercur_iterative_cur_sharded_device) over an NCCL communicator
+  built for the torch.distributed group, every collective enqueued on the run's stream and
+  captured in its iteration graphs — no host round trip per iteration. The column selection
+  replicates Y^T(:, 0:b) (one in-place allgather per iteration) instead of exchanging candidates
+  per pivot step, and the engine requires the standard block partition (`shard_range`);
+* the protocol model (a `backend` is passed): this module's Python loop over per-rank stages with
+  torch.distributed collectives — both column exchanges ("sketch", "candidates") — run on CPU with
+  gloo and a test-only backend (tests/sharded_cpu_backend.py) and on the B200 stage kernels
+  (`DeviceBackend`). It is the executable specification the native path is checked against.
+
+`iterative_cur_emulated_shards` runs the native sharded pipeline with all shards in one process on
+one GPU (per-shard kernels, collectives as device writes): the multi-rank data path on one device.
+The product has no CPU path.
 """
 from __future__ import annotations
 
@@ -145,6 +157,8 @@ class ShardedResult:
     note: str = ""
     col_steps: list = field(default_factory=list)  # (index, |best|, runner-up) per column pivot step
     exchanges: int = 0                              # collectives issued by this rank
+    native: object = None                           # the C++ run (product path)
+    kernel_launches: int = 0
 
     @property
     def rank(self) -> int:
@@ -239,6 +253,90 @@ def _dist_column_lupp(be, comm, y, col_live, steps, ynorm, pivot_floor, col_offs
     return cols
 
 
+# ------------------------------------------------------------------ native (C++ / NCCL) path
+def shard_range(n_total: int, world: int, rank: int):
+    """(offset, count) of rank's column block in the engine's partition (blocks of even width)."""
+    off, cnt = C.c_int64(), C.c_int64()
+    _check(_capi.lib().itercur_shard_range(int(n_total), int(world), int(rank), C.byref(off), C.byref(cnt)))
+    return off.value, cnt.value
+
+
+_COMMS = {}
+
+
+def native_comm(group=None):
+    """The engine's NCCL communicator over the ranks of a torch.distributed group (created once per
+    group on this rank's current device; the unique id travels through torch.distributed)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    key = (id(group), world, torch.cuda.current_device())
+    if key in _COMMS:
+        return _COMMS[key], world, rank
+    L = _capi.lib()
+    uid = (C.c_char * 128)()
+    if rank == 0:
+        _check(L.itercur_nccl_unique_id(uid))
+    if world > 1:
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        C.memmove(uid, box[0], 128)
+    comm = C.c_void_p()
+    _check(L.itercur_nccl_comm_init(world, uid, rank, C.byref(comm)))
+    _COMMS[key] = comm
+    return comm, world, rank
+
+
+def _native_config(b, epsilon, delta, alpha, risk_adjust, max_rank, max_iters, pivot_floor, seed, sketch,
+                   sparse_nnz):
+    from . import _config
+
+    return _config(epsilon, b, delta, alpha, risk_adjust, max_rank, max_iters, "lupp", "lupp", pivot_floor, seed,
+                   sketch, sparse_nnz, False)
+
+
+def _native_result(run_ptr, keep):
+    from . import _collect
+
+    f, t = _collect(run_ptr, keep)
+    return ShardedResult(f.row_indices, f.col_indices, t.status, t.final_rho, t.threshold, t.rhos, t.note,
+                         [(ix, b, s) for (k, _, ix, b, s) in t.steps if k == 0], 0, f, t.kernel_launches)
+
+
+def _native_sharded(a, col_offset, n_total, cfg, group):
+    m, n_r = a.shape
+    comm, world, rank = native_comm(group)
+    off, cnt = shard_range(n_total, world, rank)
+    if off != col_offset or cnt != n_r:
+        raise ValueError(f"rank {rank} of {world} must hold columns [{off}, {off + cnt}) of the {n_total} "
+                         f"(shard_range); got [{col_offset}, {col_offset + n_r})")
+    out = C.c_void_p()
+    with torch.cuda.device(a.device):
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+        _check(_capi.lib().itercur_iterative_cur_sharded_device(C.c_void_p(a.data_ptr()), m, n_r, _ld(a), int(n_total),
+                                                                C.byref(cfg), comm, C.c_void_p(stream),
+                                                                C.byref(out)))
+    return _native_result(out.value, a)
+
+
+def iterative_cur_emulated_shards(a: torch.Tensor, shards: int, *, epsilon=1e-6, b=50, delta=0.0, alpha=0.05,
+                                  risk_adjust=False, max_rank=0, max_iters=0, pivot_floor=1e-13, seed=0,
+                                  sketch="gaussian", sparse_nnz=8):
+    """The native column-sharded pipeline with `shards` shards computed on this one device (the
+    collectives become the equivalent device writes); returns (CurFactors, RunTrace) like
+    `iterative_cur` — exports work, every shard being local."""
+    from . import _collect
+
+    cfg = _native_config(b, epsilon, delta, alpha, risk_adjust, max_rank, max_iters, pivot_floor, seed, sketch,
+                         sparse_nnz)
+    m, n = a.shape
+    out = C.c_void_p()
+    with torch.cuda.device(a.device):
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+        _check(_capi.lib().itercur_iterative_cur_sharded_emulated(C.c_void_p(a.data_ptr()), m, n, _ld(a), int(shards),
+                                                                  C.byref(cfg), C.c_void_p(stream), C.byref(out)))
+    return _collect(out.value, a)
+
+
 def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, *, epsilon=1e-6, b=50, delta=0.0,
                           alpha=0.05, risk_adjust=False, max_rank=0, max_iters=0, pivot_floor=1e-13, seed=0,
                           sketch="gaussian", sparse_nnz=8, group=None, backend=None,
@@ -247,9 +345,19 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
     col_offset + n_r) (column-major, on this rank's device). Collective: every rank of `group`
     calls it with its own shard; all ranks return the same indices and trace.
 
-    column_exchange: "sketch" (default) replicates the c_pad x n sketch once per iteration and
-    runs the column LUPP whole on every rank (2 collectives per iteration); "candidates" runs
-    the distributed LUPP (one all_gather of pivot candidates per pivot step)."""
+    Without a `backend` (CUDA shards) this is the native C++ engine over NCCL (the block must be
+    `shard_range(n_total, world, rank)`). With a `backend`, the Python protocol model runs:
+    column_exchange "sketch" (default) replicates the c_pad x n sketch once per iteration and runs
+    the column LUPP whole on every rank (2 collectives per iteration); "candidates" runs the
+    distributed LUPP (one all_gather of pivot candidates per pivot step)."""
+    if backend is None and a_shard.is_cuda and column_exchange == "sketch":
+        if sketch not in _SKETCHES:
+            raise ValueError(f"unknown sketch kind '{sketch}'")
+        a = a_shard if (a_shard.shape[0] <= 1 or a_shard.stride(0) == 1) and _ld(a_shard) % 2 == 0 \
+            else to_colmajor(a_shard)
+        cfg = _native_config(b, epsilon, delta, alpha, risk_adjust, max_rank, max_iters, pivot_floor, seed, sketch,
+                             sparse_nnz)
+        return _native_sharded(a, int(col_offset), int(n_total), cfg, group)
     if column_exchange not in ("sketch", "candidates"):
         raise ValueError(f"unknown column_exchange '{column_exchange}'")
     comm = _Comm(group)
@@ -409,7 +517,12 @@ def iterative_cur_sharded(a_shard: torch.Tensor, col_offset: int, n_total: int, 
 def true_relative_error_sharded(a_shard: torch.Tensor, col_offset: int, result: ShardedResult, group=None,
                                 backend=None) -> float:
     """||A - C U R||_F / ||A||_F with the column sums of squares reduced over the shards
-    (driver.cpp:169-190); C U R = C X^{-1} R with X = A(I, J)."""
+    (driver.cpp:169-190); C U R = C X^{-1} R with X = A(I, J). A native result evaluates on the
+    engine (collective over its communicator: ||A_s - L R~_s||^2 per rank, summed)."""
+    if result.native is not None and backend is None:
+        out = C.c_double()
+        _check(_capi.lib().itercur_true_relative_error_sharded(result.native._run.ptr, C.byref(out)))
+        return out.value
     comm = _Comm(group)
     dev = a_shard.device
     a = a_shard
