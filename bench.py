@@ -21,10 +21,10 @@ larger than L2 (no flush needed).
 cannot be built here, no Eigen) on the same config, with A formed on the host by
 oracle/host_testmat.py (the engine library is never loaded on that arm), and prints the same
 line with "impl": "reference".
-Multi-GPU (torchrun, N > 1): by default every rank runs the workload on its own GPU (replicas,
-weak scaling), value = N * m*n / max-over-ranks time. With --sharded one matrix is
-column-sharded over the ranks (paper_2509_21963_b200/sharded.py; strong scaling),
-value = m*n / max-over-ranks time.
+Multi-GPU (torchrun, N > 1): configs 4/5 (80 GB) run column-sharded by default — one matrix split
+by columns over the ranks, the native engine with NCCL collectives captured in its iteration
+graphs (strong scaling), value = m*n / max-over-ranks time; --replicas (and the
+smaller configs by default) run N independent replicas (weak scaling), value = N * m*n / max time.
 """
 from __future__ import annotations
 
@@ -71,7 +71,7 @@ class ClockSampler:
     NVML (pynvml) every `period` s — cheaper and less intrusive than spawning nvidia-smi (whose per-call
     NVML initialisation perturbed round 1's timings by several percent). Falls back to nvidia-smi."""
 
-    def __init__(self, index: int, period: float = 0.02):
+    def __init__(self, index: int, period: float = 0.25):
         self.index = index
         self.period = period
         self.samples = []  # (sm_mhz, sm_max_mhz, hw_slowdown, hw_thermal, sw_thermal, sw_power_cap)
@@ -266,24 +266,27 @@ def run_reference_arm(args, cfgno, world):
 
 
 def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
-    """--sharded: one matrix column-sharded over the ranks (paper_2509_21963_b200/sharded.py,
-    SURVEY §8(e)); strong scaling: value = m*n / max-over-ranks time of one run."""
+    """Column-sharded run: one matrix split by columns over the ranks, the native
+    engine over NCCL (csrc/engine.cu, itercur_iterative_cur_sharded_device); strong scaling:
+    value = m*n / max-over-ranks device time of one run. e2e: each rank's block copied from pinned
+    host memory inside the timed region."""
     import torch
 
     import paper_2509_21963_b200 as engine  # noqa: F401  (loads the engine)
     from paper_2509_21963_b200 import build, testmat
-    from paper_2509_21963_b200.sharded import iterative_cur_sharded
+    from paper_2509_21963_b200.sharded import iterative_cur_sharded, shard_range
 
     build.build()
+    lo, cnt = shard_range(n, world, rank)
     a = testmat.generate(args.config)
-    lo, hi = round(rank * n / world), round((rank + 1) * n / world)
-    shard = a[:, lo:hi].t().contiguous().t()
+    shard = torch.empty(cnt, m, dtype=torch.float64, device="cuda").t()
+    shard.copy_(a[:, lo:lo + cnt])
     del a
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
-    run = dict(run_cfg, column_exchange=args.exchange)
     res = None
-    for _ in range(args.warmup):
-        res = iterative_cur_sharded(shard, lo, n, **run)
+    for _ in range(max(1, args.warmup)):
+        res = iterative_cur_sharded(shard, lo, n, **run_cfg)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -292,22 +295,43 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            res = iterative_cur_sharded(shard, lo, n, **run)
+            res = None
+            res = iterative_cur_sharded(shard, lo, n, **run_cfg)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    launches = res.kernel_launches
+    # e2e: this rank's block from pinned host memory, H2D inside the timed region
+    host = torch.empty(cnt, m, dtype=torch.float64, pin_memory=True)
+    host.copy_(shard.t())
+    del shard
+    torch.cuda.empty_cache()
     if world > 1:
-        tt = torch.tensor([ms], device="cuda")
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        dshard = host.to("cuda", non_blocking=True).t()
+        r2 = iterative_cur_sharded(dshard, lo, n, **run_cfg)
+        _ = (r2.row_indices, r2.col_indices)
+        del dshard
+    torch.cuda.synchronize()
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / max(1, args.steps)
+    if world > 1:
+        tt = torch.tensor([ms, e2e_ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt[0])
+        ms, e2e_ms = float(tt[0]), float(tt[1])
     if rank == 0:
         line = {"metric": METRIC, "value": m * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
-                "config": {**cfg_line, "parallelism": f"column-sharded x{world}", "column_exchange": args.exchange},
-                "clocks": clk.summary(),
+                "config": {**cfg_line, "parallelism": f"column-sharded x{world}"},
+                "e2e": {"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
+                        "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms,
+                        "source": "each rank's column block from pinned host memory"},
+                "gpu_launches": launches * args.steps, "clocks": clk.summary(),
                 "run": {"status": res.status, "rank": res.rank, "iterations": len(res.rhos),
-                        "exchanges_per_run": res.exchanges}}
+                        "engine": "native column-sharded (NCCL collectives in the iteration graphs)",
+                        "block_columns": [lo, lo + cnt]}}
         print(json.dumps(line))
     if world > 1:
         torch.distributed.barrier()
@@ -326,10 +350,10 @@ def main():
     ap.add_argument("--no-cpu-one-core", action="store_true", help="skip the 1-core oracle run")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=300.0, help="reference arm: time budget for its steps (s)")
-    ap.add_argument("--exchange", default="sketch", choices=["sketch", "candidates"],
-                    help="--sharded column selection: replicate Y per iteration, or exchange pivot candidates per step")
     ap.add_argument("--sharded", action="store_true",
-                    help="N > 1: one matrix column-sharded over the GPUs (strong scaling) instead of N replicas")
+                    help="one matrix column-sharded over the GPUs (strong scaling; the default for N > 1 on "
+                         "configs 4/5)")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: N independent replicas (weak scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -366,7 +390,7 @@ def main():
     run_cfg = dict(epsilon=cfg["epsilon"], b=cfg["b"], seed=0, sketch=cfg["sketch"], max_rank=cfg["max_rank"])
     cfg_line = config_line(args.config, world)
 
-    if args.sharded:
+    if args.sharded or (world > 1 and args.config in (4, 5) and not args.replicas):
         return run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local)
 
     import paper_2509_21963_b200 as engine

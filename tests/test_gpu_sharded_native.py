@@ -65,7 +65,7 @@ def test_emulated_shards_match_engine_and_oracle(engine, oracle, case, shards):
     assert np.array_equal(f.c_matrix(), a[:, f.col_indices])
     core = f.core_matrix()
     X = a[np.ix_(f.row_indices, f.col_indices)]
-    assert np.linalg.norm(core @ X - np.eye(f.rank)) <= 1e-7 * max(1.0, np.linalg.cond(X) * 1e-8)
+    assert np.linalg.norm(core @ X - np.eye(f.rank)) <= 1e-10 * np.linalg.cond(X)
 
 
 def test_emulated_shards_deterministic(engine, oracle):
