@@ -66,56 +66,80 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
-class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region, in-process through
-    NVML (pynvml) every `period` s — cheaper and less intrusive than spawning nvidia-smi (whose per-call
-    NVML initialisation perturbed round 1's timings by several percent). Falls back to nvidia-smi."""
+_SAMPLER_SRC = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+period = float(sys.argv[2])
+bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+        pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+print("ready", flush=True)
+while sys.stdin.readline().strip() == "s":
+    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(sm, mx, *[int(bool(r & b)) for b in bits], flush=True)
+"""
 
-    def __init__(self, index: int, period: float = 0.25):
+
+class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region every `period`
+    s by a separate sampler process (pynvml; nvidia-smi as a fallback). NVML queries from inside the
+    benchmarking process serialised with its CUDA work (measured: config 2 at 65.6 ms per step
+    instead of 32 ms), and spawning nvidia-smi per sample cost ~7% in round 1."""
+
+    def __init__(self, index: int, period: float = 0.2):
         self.index = index
         self.period = period
         self.samples = []  # (sm_mhz, sm_max_mhz, hw_slowdown, hw_thermal, sw_thermal, sw_power_cap)
         self._stop = threading.Event()
         self._t = None
+        self._proc = None
 
-    def _nvml_handle(self):
-        import pynvml
-
-        pynvml.nvmlInit()
-        index = self.index
+    def _physical_index(self):
         vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
-        if vis and vis.split(",")[0].strip().isdigit():
-            index = int(vis.split(",")[self.index].strip())
-        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
+        parts = [x.strip() for x in vis.split(",") if x.strip()]
+        if parts and all(x.isdigit() for x in parts) and self.index < len(parts):
+            return int(parts[self.index])
+        return self.index
+
+    def _start(self):
+        try:
+            self._proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(self._physical_index()),
+                                           str(self.period)], stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                          stderr=subprocess.DEVNULL, text=True)
+            if self._proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("sampler did not start")
+        except Exception:
+            self._proc = None
 
     def _run(self):
-        try:
-            nv, h = self._nvml_handle()
-            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((float(sm), float(mx), *[bool(r & b) for b in bits]))
-                self._stop.wait(self.period)
-            return
-        except Exception:
-            pass
+        if self._proc is not None:
+            try:
+                while True:  # a sample as the timed region starts, then every `period`
+                    self._proc.stdin.write("s\n")
+                    self._proc.stdin.flush()
+                    v = self._proc.stdout.readline().split()
+                    if len(v) == 6:
+                        self.samples.append((float(v[0]), float(v[1]), *[x == "1" for x in v[2:]]))
+                    if self._stop.wait(self.period):
+                        return
+            except Exception:
+                pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
+        while not self._stop.wait(self.period):
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self._physical_index()), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 v = [x.strip() for x in out.stdout.strip().split(",")]
                 if len(v) == 6:
                     self.samples.append((float(v[0]), float(v[1]), *[x == "Active" for x in v[2:]]))
             except Exception:
                 pass
-            self._stop.wait(0.2)
 
     def __enter__(self):
+        self._start()  # the sampler process is up before the timed region begins
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -123,6 +147,13 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._proc is not None:
+            try:
+                self._proc.stdin.write("q\n")
+                self._proc.stdin.flush()
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
 
     def summary(self):
         if not self.samples:
@@ -131,7 +162,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k]})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.samples[0][1], "reasons": reasons,
-                "samples": len(sm), "source": "NVML (pynvml), in-process"}
+                "samples": len(sm), "source": "NVML in a sampler process"}
 
 
 # the committed `ncu --set full` summary of the sketch kernel per config (tools/summarize_ncu.py)
@@ -301,6 +332,8 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     launches = res.kernel_launches
+    status, rank_final, n_iters, n_rhos = res.status, res.rank, len(res.rhos), len(res.rhos)
+    res = None  # (holds the shard)
     # e2e: this rank's block from pinned host memory, H2D inside the timed region
     host = torch.empty(cnt, m, dtype=torch.float64, pin_memory=True)
     host.copy_(shard.t())
@@ -309,12 +342,15 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
+    r2 = None
     for _ in range(max(1, args.steps)):
+        r2 = None  # release the previous step's block before the next copy
         dshard = host.to("cuda", non_blocking=True).t()
         r2 = iterative_cur_sharded(dshard, lo, n, **run_cfg)
         _ = (r2.row_indices, r2.col_indices)
         del dshard
     torch.cuda.synchronize()
+    r2 = None
     e2e_ms = 1e3 * (time.perf_counter() - t0) / max(1, args.steps)
     if world > 1:
         tt = torch.tensor([ms, e2e_ms], device="cuda")
@@ -326,10 +362,10 @@ def run_sharded(args, m, n, cfg, run_cfg, cfg_line, world, rank, local):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated, BASELINE config)",
                 "config": {**cfg_line, "parallelism": f"column-sharded x{world}"},
                 "e2e": {"value": m * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
-                        "d2h_bytes_per_step": 16 * res.rank + 8 * len(res.rhos), "ms_per_step": e2e_ms,
+                        "d2h_bytes_per_step": 16 * rank_final + 8 * n_rhos, "ms_per_step": e2e_ms,
                         "source": "each rank's column block from pinned host memory"},
                 "gpu_launches": launches * args.steps, "clocks": clk.summary(),
-                "run": {"status": res.status, "rank": res.rank, "iterations": len(res.rhos),
+                "run": {"status": status, "rank": rank_final, "iterations": n_iters,
                         "engine": "native column-sharded (NCCL collectives in the iteration graphs)",
                         "block_columns": [lo, lo + cnt]}}
         print(json.dumps(line))

@@ -281,7 +281,20 @@ def native_comm(group=None):
         dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
         C.memmove(uid, box[0], 128)
     comm = C.c_void_p()
-    _check(L.itercur_nccl_comm_init(world, uid, rank, C.byref(comm)))
+    # NCCL prints its version banner on stdout at init: keep stdout clean for callers that emit
+    # machine-read lines there (bench.py), routing the banner to stderr
+    import os
+    import sys
+
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        rc = L.itercur_nccl_comm_init(world, uid, rank, C.byref(comm))
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
+    _check(rc)
     _COMMS[key] = comm
     return comm, world, rank
 
