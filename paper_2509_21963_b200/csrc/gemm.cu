@@ -183,16 +183,21 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
       }
       cp_async_commit();
     }
+    // the Y^T rows to downdate, prefetched while the block is narrow (b <= 32); wider blocks
+    // (NT > 4) load them in the epilogue instead: their accumulators, base values and the
+    // downdate's fragments would not fit the register file together
+    if constexpr (NT <= 4) {
 #pragma unroll
-    for (int ny = 0; ny < NTY; ++ny)
+      for (int ny = 0; ny < NTY; ++ny)
 #pragma unroll
-      for (int dq = 0; dq < 2; ++dq)
+        for (int dq = 0; dq < 2; ++dq)
 #pragma unroll
-        for (int dr = 0; dr < 2; ++dr) {
-          const int h = ny * 8 + 2 * t + dq;
-          const int64_t j = r0 + dr;
-          yv[ny][dr * 2 + dq] = (finisher && h < p.ycp && j < p.M) ? p.y[j * p.ycp + h] : 0.0;
-        }
+          for (int dr = 0; dr < 2; ++dr) {
+            const int h = ny * 8 + 2 * t + dq;
+            const int64_t j = r0 + dr;
+            yv[ny][dr * 2 + dq] = (finisher && h < p.ycp && j < p.M) ? p.y[j * p.ycp + h] : 0.0;
+          }
+    }
   }
   ub_stamp(p, 1);
   if (splits > 1) {
@@ -416,7 +421,8 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
       for (int dr = 0; dr < 2; ++dr) {
         const int64_t j = r0 + dr;
         if (j >= p.M) continue;
-        const double v = yv[ny][dr * 2 + dq] + p.alpha * yacc[ny][dr * 2 + dq];
+        const double y0 = NT <= 4 ? yv[ny][dr * 2 + dq] : p.y[j * p.ycp + h];
+        const double v = y0 + p.alpha * yacc[ny][dr * 2 + dq];
         p.y[j * p.ycp + h] = v;
         sq = fma(v, v, sq);
         if (h < p.wc_rows) p.Wc[j + h * p.ldwc] = v;
@@ -448,7 +454,8 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
   }
 }
 
-static int ts_gemm_nt_host(int n) { return n <= 8 ? 1 : (n <= 16 ? 2 : (n <= 24 ? 3 : (n <= 32 ? 4 : 9))); }
+// fused U block: n-tiles of 8 for blocks up to 64 wide
+static int ts_gemm_nt_host(int n) { return n <= 64 ? static_cast<int>(std::max<int64_t>(1, ceil_div(n, 8))) : 9; }
 
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -764,7 +771,8 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
 }
 
 bool ts_gemm_ublock_supported(const TsGemmParams& p) {
-  return p.N >= 1 && p.N <= 32 && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) &&
+  static const int max_n = env_int("ITERCUR_UB_MAX_N", 64);  // A/B: 32 = round 1's fused range
+  return p.N >= 1 && p.N <= std::min(64, max_n) && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) &&
          (p.base_mode == kBaseGatherRowsT || p.base_mode == kBaseGatherCols) &&
          p.norm_part && p.y && p.rt && p.lu && p.yg && p.ctl;
 }
@@ -775,14 +783,20 @@ template <int NT>
 static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
   static const int forced = env_int("ITERCUR_UB_LEAN", env_int("ITERCUR_GEMM_LEAN", -1));
   static const int ub_splits = env_int("ITERCUR_UB_SPLITS", 0);
-  const int lean = forced > 0 ? forced : (p.M >= 16000 ? 2 : 1);
+  // wide blocks need the deeper 32-row stages: the epilogue's LU block and Y(:,J_k) staging
+  // (NT = 8: 9.3K doubles + the split-K buffer) must fit the ring
+  const int lean = NT > 4 ? 2 : (forced > 0 ? forced : (p.M >= 16000 ? 2 : 1));
   // at most 2 K-splits: only the split-0 CTA runs the (serial) epilogue while its peers wait at
   // the cluster barrier, so deeper splits cost more than they save (config 2, profile-mode
   // phase sums: 7.64 ms at 2 splits vs 7.68 at 3 and 7.99 at 4)
   const int64_t tiles = ceil_div(p.M, 64);
   g_splits_override =
       ub_splits > 0 ? ub_splits : std::min(2, gemm_splits(tiles, p.k_plan > 0 ? p.k_plan : p.K, lean == 2 ? 32 : 16));
-  const cudaError_t e = lean == 2 ? launch_lean<NT, 4, 32, 3, true>(p, st) : launch_lean<NT, 4, 16, 4, true>(p, st);
+  cudaError_t e;
+  if constexpr (NT > 4)
+    e = launch_lean<NT, 4, 32, 3, true>(p, st);
+  else
+    e = lean == 2 ? launch_lean<NT, 4, 32, 3, true>(p, st) : launch_lean<NT, 4, 16, 4, true>(p, st);
   g_splits_override = 0;
   return e;
 }
@@ -794,7 +808,11 @@ cudaError_t run_ts_gemm_ublock(const TsGemmParams& p, cudaStream_t st) {
     case 1: return launch_ublock_nt<1>(p, st);
     case 2: return launch_ublock_nt<2>(p, st);
     case 3: return launch_ublock_nt<3>(p, st);
-    default: return launch_ublock_nt<4>(p, st);
+    case 4: return launch_ublock_nt<4>(p, st);
+    case 5: return launch_ublock_nt<5>(p, st);
+    case 6: return launch_ublock_nt<6>(p, st);
+    case 7: return launch_ublock_nt<7>(p, st);
+    default: return launch_ublock_nt<8>(p, st);
   }
 }
 
