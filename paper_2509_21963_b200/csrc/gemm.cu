@@ -317,6 +317,81 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
       }
     }
   const int qbase = lane & ~3;
+  if constexpr (NT > 4) {
+    // wide blocks (33..64): the same substitutions as below with runtime loops over the pivot p
+    // (the fully unrolled form outgrows the instruction cache at NT = 7: ncu showed "no
+    // instruction" as the top stall and 785 us per call at config 4); x[p] is read from its
+    // n-tile with a static select, so acc never needs a dynamic register index
+    auto pick = [&](int ntp, int dqp, int row) {
+      double v = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        if (nt == ntp) v = dqp ? acc[nt][row * 2 + 1] : acc[nt][row * 2];
+      return v;
+    };
+#pragma unroll 1
+    for (int pp = 0; pp < w; ++pp) {
+      const int ntp = pp >> 3, tp = (pp & 7) >> 1, dqp = pp & 1;
+      const double x0 = __shfl_sync(0xffffffffu, pick(ntp, dqp, 0), qbase | tp);
+      const double x1 = __shfl_sync(0xffffffffu, pick(ntp, dqp, 1), qbase | tp);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq) {
+          const int q = nt * 8 + 2 * t + dq;
+          if (q > pp && q < w) {
+            const double l = s_lu[q + pp * W];
+            acc[nt][dq] = fma(-l, x0, acc[nt][dq]);
+            acc[nt][2 + dq] = fma(-l, x1, acc[nt][2 + dq]);
+          }
+        }
+    }
+    ub_stamp(p, 4);
+#pragma unroll 1
+    for (int pp = w - 1; pp >= 0; --pp) {
+      const int ntp = pp >> 3, tp = (pp & 7) >> 1, dqp = pp & 1;
+      const double upp = s_lu[pp + pp * W];
+      const double a0 = __shfl_sync(0xffffffffu, pick(ntp, dqp, 0), qbase | tp);
+      const double a1 = __shfl_sync(0xffffffffu, pick(ntp, dqp, 1), qbase | tp);
+      const double yrc = s_lu[W * W + pp];
+      double x0 = __dmul_rn(a0, yrc), x1 = __dmul_rn(a1, yrc);
+      x0 = __fma_rn(__fma_rn(-x0, upp, a0), yrc, x0);
+      x1 = __fma_rn(__fma_rn(-x1, upp, a1), yrc, x1);
+      auto out_of_range = [](double v) {
+        const unsigned hi = static_cast<unsigned>(__double_as_longlong(v) >> 32) & 0x7fffffffu;
+        const unsigned e = hi >> 20;
+        return static_cast<unsigned>((e - 56u) > (1990u - 56u)) & static_cast<unsigned>(v != 0.0);
+      };
+      const unsigned bad = out_of_range(a0) | out_of_range(a1) | out_of_range(x0) | out_of_range(x1) |
+                           static_cast<unsigned>(!pivot_in_range(upp));
+      if (__any_sync(0xffffffffu, bad)) {
+        x0 = ieee_div(a0, upp);
+        x1 = ieee_div(a1, upp);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        if (nt == ntp && t == tp) {
+          if (dqp) {
+            acc[nt][1] = x0;
+            acc[nt][3] = x1;
+          } else {
+            acc[nt][0] = x0;
+            acc[nt][2] = x1;
+          }
+        }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq) {
+          const int q = nt * 8 + 2 * t + dq;
+          if (q < pp) {
+            const double u = s_lu[q + pp * W];
+            acc[nt][dq] = fma(-u, x0, acc[nt][dq]);
+            acc[nt][2 + dq] = fma(-u, x1, acc[nt][2 + dq]);
+          }
+        }
+    }
+  } else {
   // forward substitution with the unit-lower factor: x[q] -= L(q, p) x[p], p ascending
 #pragma unroll
   for (int pp = 0; pp < W; ++pp) {
@@ -379,6 +454,7 @@ __device__ __forceinline__ void ublock_epilogue(const TsGemmParams& p, double (&
           acc[nt][2 + dq] = fma(-u, x1, acc[nt][2 + dq]);
         }
       }
+  }
   }
   ub_stamp(p, 5);
   // R~ rows r .. r+w
@@ -771,7 +847,9 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
 }
 
 bool ts_gemm_ublock_supported(const TsGemmParams& p) {
-  static const int max_n = env_int("ITERCUR_UB_MAX_N", 64);  // A/B: 32 = round 1's fused range
+  // blocks up to 64 wide fuse too (NT 5-8), but measured slower than GEMM + row solves + downdate
+  // at config 4 (b = 50: 615 vs ~530 us per iteration; tie at config 5): opt-in, ITERCUR_UB_MAX_N=64
+  const int max_n = env_int("ITERCUR_UB_MAX_N", 32);
   return p.N >= 1 && p.N <= std::min(64, max_n) && p.ycp <= 8 * (ts_gemm_nt_host(p.N) + 1) && lean_ok(p) &&
          (p.base_mode == kBaseGatherRowsT || p.base_mode == kBaseGatherCols) &&
          p.norm_part && p.y && p.rt && p.lu && p.yg && p.ctl;

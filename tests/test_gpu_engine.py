@@ -365,3 +365,21 @@ def test_slupp_large_rank_matches_oracle(engine, oracle, rank):
     err = engine.true_relative_error(a, f)
     err_o = oracle.true_relative_error(a, I, J)
     assert abs(err - err_o) <= 1e-8 + 1e-3 * err_o, (err, err_o)
+
+
+@pytest.mark.parametrize("b,sketch", [(50, "sparse_sign"), (64, "gaussian"), (40, "gaussian")])
+def test_fused_wide_ublock_matches_oracle(engine, oracle, monkeypatch, b, sketch):
+    """The fused U block for blocks 33..64 wide (opt-in ITERCUR_UB_MAX_N=64: U_k, the solves against
+    D_k's LU with runtime pivot loops, R~_k and the downdate in one kernel) against the oracle."""
+    monkeypatch.setenv("ITERCUR_UB_MAX_N", "64")
+    a = low_rank_plus_noise(oracle, 1500, 1100, 220, 1e-10, 41 + b)
+    kw = dict(epsilon=1e-8, b=b, seed=2, sketch=sketch)
+    f, t = engine.iterative_cur(a, **kw)
+    monkeypatch.delenv("ITERCUR_UB_MAX_N")
+    f2, t2 = engine.iterative_cur(a, **kw)  # the unfused path
+    o = oracle.iterative_cur(a, **kw)
+    v = compare_runs(o, f, t)
+    assert v["status_equal"] and v["identical"], v
+    assert f.col_indices == f2.col_indices and np.allclose(t.rhos, t2.rhos, rtol=1e-9, atol=1e-13)
+    err = engine.true_relative_error(a, f)
+    assert abs(err - oracle.true_relative_error(a, o.row_indices, o.col_indices)) <= 1e-8
