@@ -416,6 +416,146 @@ __global__ void __launch_bounds__(128) rows_lu_solve_col_kernel(const double* __
   }
 }
 
+// The row-oriented solves with each thread's row in SHARED memory (xs[q][thread]: consecutive
+// threads, consecutive banks) and runtime loops: the register-array form above ends up in local
+// memory beyond 16 columns and is latency-bound there (250 us at 100000 rows x 50); here the only
+// dependency chain is the FMA accumulation of v (the loads of x[p] and L(q, p) are independent of
+// it). Same operations in the same order as rows_lu_solve_kernel: bitwise its results.
+template <int WMAX>
+__global__ void __launch_bounds__(128) rows_lu_solve_smem_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                                                 const double* __restrict__ lu, int64_t ldd,
+                                                                 const int* __restrict__ d_w, int w_max,
+                                                                 double* __restrict__ out, int64_t ldo,
+                                                                 const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                                                 const int* __restrict__ perm) {
+  extern __shared__ double sm[];
+  double* slu = sm;                 // w x w factors (ld w)
+  double* xs = sm + WMAX * WMAX;    // xs[q * 128 + tid]
+  __shared__ int sperm[WMAX];
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
+  }
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) slu[e] = lu[(e % w) + (e / w) * ldd];
+  for (int q = threadIdx.x; q < WMAX; q += blockDim.x) sperm[q] = (perm && q < w) ? perm[q] : q;
+  __syncthreads();
+  double* x = xs + threadIdx.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+    for (int q = 0; q < w; ++q) x[q * 128] = X[j + sperm[q] * ldx];  // P u
+    for (int q = 1; q < w; ++q) {  // Lhat y = u
+      double v = x[q * 128];
+      const double* lq = slu + q;
+#pragma unroll 4
+      for (int p = 0; p < q; ++p) v = fma(-lq[p * w], x[p * 128], v);
+      x[q * 128] = v;
+    }
+    for (int q = w - 1; q >= 0; --q) {  // Uhat x = y
+      double v = x[q * 128];
+      const double* lq = slu + q;
+#pragma unroll 4
+      for (int p = q + 1; p < w; ++p) v = fma(-lq[p * w], x[p * 128], v);
+      x[q * 128] = v / slu[q + q * w];
+    }
+    for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q * 128];
+  }
+}
+
+// Blocked form (default for 16 < w <= 64): the row in shared memory in chunks of 8 entries, the
+// factors zero-padded to 64 x 64. Each chunk of 8 unknowns is updated by every earlier (forward) /
+// later (back) chunk with an unrolled 8 x 8 block of FMAs on registers — eight shared-memory reads
+// of x per 64 FMAs instead of one per FMA (the per-FMA form above is bound by shared-memory
+// bandwidth: 187 us at 100000 x 50). The forward sweep accumulates each x[q] in ascending p like the
+// row form; the back sweep subtracts the later chunks before the chunk's own triangle.
+__global__ void __launch_bounds__(128) rows_lu_solve_blk_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                                                const double* __restrict__ lu, int64_t ldd,
+                                                                const int* __restrict__ d_w, int w_max,
+                                                                double* __restrict__ out, int64_t ldo,
+                                                                const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                                                const int* __restrict__ perm) {
+  constexpr int WP = 64, T = 128;
+  extern __shared__ double sm[];
+  double* slu = sm;             // 64 x 64, zero-padded, ld 64
+  double* xs = sm + WP * WP;    // xs[q * 128 + tid]
+  __shared__ int sperm[WP];
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
+  }
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < WP * WP; e += T) {
+    const int a = e % WP, b = e / WP;
+    slu[e] = (a < w && b < w) ? lu[a + b * ldd] : (a == b ? 1.0 : 0.0);  // identity padding: exact no-ops
+  }
+  for (int q = threadIdx.x; q < WP; q += T) sperm[q] = (perm && q < w) ? perm[q] : q;
+  __syncthreads();
+  const int nch = (w + 7) / 8;
+  double* x = xs + threadIdx.x;
+  for (int64_t j = blockIdx.x * (int64_t)T + threadIdx.x; j < M; j += (int64_t)gridDim.x * T) {
+    for (int q = 0; q < nch * 8; ++q) x[q * T] = q < w ? X[j + sperm[q] * ldx] : 0.0;  // P u, zero-padded
+    // forward: Lhat y = u (unit lower)
+    for (int P = 0; P < nch; ++P) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = x[(8 * P + i) * T];
+      for (int Q = 0; Q < P; ++Q) {
+        double xq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xq[k] = x[(8 * Q + k) * T];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double* l = slu + 8 * P + (8 * Q + k) * WP;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = fma(-l[i], xq[k], v[i]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double* l = slu + 8 * P + (8 * P + k) * WP;
+#pragma unroll
+        for (int i = k + 1; i < 8; ++i) v[i] = fma(-l[i], v[k], v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[(8 * P + i) * T] = v[i];
+    }
+    // back: Uhat x = y
+    for (int P = nch - 1; P >= 0; --P) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = x[(8 * P + i) * T];
+      for (int Q = P + 1; Q < nch; ++Q) {
+        double xq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xq[k] = x[(8 * Q + k) * T];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double* u = slu + 8 * P + (8 * Q + k) * WP;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = fma(-u[i], xq[k], v[i]);
+        }
+      }
+#pragma unroll
+      for (int k = 7; k >= 0; --k) {
+        v[k] = v[k] / slu[(8 * P + k) * (WP + 1)];
+        const double* u = slu + 8 * P + (8 * P + k) * WP;
+#pragma unroll
+        for (int i = 0; i < k; ++i) v[i] = fma(-u[i], v[k], v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[(8 * P + i) * T] = v[i];
+    }
+    for (int q = 0; q < w; ++q) out[j + q * ldo] = x[q * T];
+  }
+}
+
 // generic width (w > 64): same solves with x in a column-strided global workspace; the factors
 // in shared memory while w*w doubles fit one CTA (w <= 168), else read from global memory
 // (L1/L2-resident: every thread walks them in the same order)
@@ -465,13 +605,35 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
   if (w_max <= 16) {
     return launch_ex(rows_lu_solve_kernel<16>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
-  } else if (w_max <= 32 && env_flag("ITERCUR_ROWS_SOLVE_ROWFORM")) {  // A/B: the row-oriented form
+  } else if (w_max <= 64 && !env_flag("ITERCUR_ROWS_SOLVE_ROWFORM") && !env_flag("ITERCUR_ROWS_SOLVE_COLFORM") &&
+             !env_flag("ITERCUR_ROWS_SOLVE_SMEM")) {
+    // blocked, rows in shared memory (default; A/B switches below)
+    const size_t smem2 = sizeof(double) * (64 * 64 + 64 * 128);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(rows_lu_solve_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem2));
+      attr = true;
+    }
+    return launch_ex(rows_lu_solve_blk_kernel, dim3(blocks), dim3(128), smem2, st, dim3(0, 0, 0), X, ldx, M, lu, ldd,
+                     d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+  } else if (w_max <= 64 && env_flag("ITERCUR_ROWS_SOLVE_SMEM")) {  // A/B: per-FMA shared-memory form
+    const size_t smem2 = sizeof(double) * (64 * 64 + 64 * 128);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(rows_lu_solve_smem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem2));
+      attr = true;
+    }
+    return launch_ex(rows_lu_solve_smem_kernel<64>, dim3(blocks), dim3(128), smem2, st, dim3(0, 0, 0), X, ldx, M, lu,
+                     ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+  } else if (w_max <= 32 && env_flag("ITERCUR_ROWS_SOLVE_ROWFORM")) {  // A/B: the row-oriented register form
     return launch_ex(rows_lu_solve_kernel<32>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
   } else if (w_max <= 64 && env_flag("ITERCUR_ROWS_SOLVE_ROWFORM")) {
     return launch_ex(rows_lu_solve_kernel<64>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
-  } else if (w_max <= 64) {  // lane pairs: 64 rows per 128-thread CTA
+  } else if (w_max <= 64) {  // A/B: lane pairs, column-oriented (64 rows per 128-thread CTA)
     const int blocks2 = static_cast<int>(std::min<int64_t>(ceil_div(M, 64), 148 * 16));
     if (w_max <= 32)
       return launch_ex(rows_lu_solve_col_kernel<32>, dim3(blocks2), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu,
