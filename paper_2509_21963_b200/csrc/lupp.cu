@@ -114,6 +114,7 @@ struct LuppKernelArgs {
   Cand* cand;           // [2][gridDim.x]
   double* norm_part;    // [gridDim.x]
   long long* dbg;       // optional per-step clock64() trace of CTA 0 (panel kernel; benchmarking)
+  unsigned long long* arrivals = nullptr;  // panel kernel: monotonic count of published CTA candidates
 };
 
 __global__ void __launch_bounds__(kLuppThreads) lupp_kernel(LuppKernelArgs ka) {
@@ -1458,8 +1459,12 @@ __device__ __forceinline__ Cand panel_reduce_list(const Cand* cs, int G) {
   const WCand w = warp_argmax(c);
   return w.key ? Cand{key_mag(w.key), w.second, static_cast<int64_t>(w.idx)} : cand_empty();
 }
-// This CTA's candidate to global: warp argmax, then thread 0 merges the warps.
-__device__ __forceinline__ void panel_publish(const Cand& local, WCand* sw, Cand* out) {
+// This CTA's candidate to global: warp argmax, then thread 0 merges the warps. With `arrivals`,
+// thread 0 then announces it with a gpu-scope release increment (the CTA barrier before orders
+// every thread's W stores of this step before it): the next step's readers wait on the count
+// instead of a grid barrier.
+__device__ __forceinline__ void panel_publish(const Cand& local, WCand* sw, Cand* out,
+                                              unsigned long long* arrivals = nullptr) {
   WCand c{0ull, 0x7fffffff, -1.0};
   if (local.idx >= 0) wcand_merge(c, mag_key(local.mag), static_cast<int32_t>(local.idx), local.second);
   const WCand w = warp_argmax(c);
@@ -1470,7 +1475,19 @@ __device__ __forceinline__ void panel_publish(const Cand& local, WCand* sw, Cand
     for (int q = 1; q < kLuppThreads / 32; ++q)
       if (sw[q].key) wcand_merge(r, sw[q].key, sw[q].idx, sw[q].second);
     *out = r.key ? Cand{key_mag(r.key), r.second, static_cast<int64_t>(r.idx)} : cand_empty();
+    if (arrivals) asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(arrivals) : "memory");
   }
+}
+// Wait until `target` CTA candidates have been announced: one poller per CTA (acquire at gpu
+// scope, as cooperative groups' grid barrier polls), then the CTA barrier.
+__device__ __forceinline__ void panel_wait(const unsigned long long* arrivals, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(arrivals) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
 }
 
 // PG: panel width (8; 4 for the 8-rows-per-thread variant, whose multipliers must still fit
@@ -1541,12 +1558,17 @@ __global__ void __launch_bounds__(kLuppThreads, 2) lupp_panel_kernel(LuppKernelA
   }
   Cand bc = block_reduce_cand(local, sc);
   if (threadIdx.x == 0) ka.cand[blockIdx.x] = bc;
+  // the arrival count before any CTA of this launch increments it (increments start after this
+  // barrier): step s waits for base + s * G announcements
+  unsigned long long base = 0;
+  if (ka.arrivals) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(base) : "l"(ka.arrivals) : "memory");
   grid.sync();
 
   int count = 0;
   double first = 0.0;
   long long* const dbg = (ka.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? ka.dbg : nullptr;
   for (int s = 0; s < steps; ++s) {
+    if (ka.arrivals && s > 0) panel_wait(ka.arrivals, base + static_cast<unsigned long long>(s) * G);
     if (dbg) dbg[s * 8 + 0] = clock64();
     // every warp reduces the whole CTA-candidate list itself: no block barrier on this path
     const Cand best = panel_reduce_list(ka.cand + (s & 1) * G, G);
@@ -1640,9 +1662,9 @@ __global__ void __launch_bounds__(kLuppThreads, 2) lupp_panel_kernel(LuppKernelA
       }
     }
     if (dbg) dbg[s * 8 + 4] = clock64();
-    panel_publish(local, sw, ka.cand + ((s + 1) & 1) * G + blockIdx.x);
+    panel_publish(local, sw, ka.cand + ((s + 1) & 1) * G + blockIdx.x, ka.arrivals);
     if (dbg) dbg[s * 8 + 5] = clock64();
-    grid.sync();
+    if (!ka.arrivals) grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *a.d_count = count;
@@ -1677,7 +1699,7 @@ constexpr size_t kLuppSmemBudget = 200 * 1024;
 // scratch: caller-provided device buffer of >= lupp_scratch_bytes(b) bytes
 size_t lupp_scratch_bytes(int b) {
   return sizeof(Cand) * 2 * kMaxLuppGrid + sizeof(double) * kMaxLuppGrid +
-         sizeof(double) * 2 * kMaxLuppGrid * static_cast<size_t>(b + 4);
+         sizeof(double) * 2 * kMaxLuppGrid * static_cast<size_t>(b + 4) + 64;  // + the panel kernel's arrivals
 }
 
 void set_lupp_force_path(int path) { g_force_path = path; }
@@ -1688,7 +1710,10 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
   char* sp = reinterpret_cast<char*>(scratch);
   Cand* cand = reinterpret_cast<Cand*>(sp);
   double* norm_part = reinterpret_cast<double*>(sp + sizeof(Cand) * 2 * kMaxLuppGrid);
-  double* pub = norm_part + kMaxLuppGrid;
+  // the panel kernel's arrival counter (never cleared: each launch reads its base), then the
+  // shared-memory kernel's publication slots
+  unsigned long long* arrivals = reinterpret_cast<unsigned long long*>(norm_part + kMaxLuppGrid);
+  double* pub = norm_part + kMaxLuppGrid + 8;
   const int steps = std::max(a.cols_max, 1);
   // cluster path (W fits in one thread-block cluster's shared memory)
   if (g_force_path == 0 || g_force_path == 1) {
@@ -1745,6 +1770,10 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
   ka.cand = cand;
   ka.norm_part = norm_part;
   ka.dbg = g_lupp_dbg;
+  // the panel kernel's per-step exchange: counted arrivals instead of a grid barrier
+  // (A/B: ITERCUR_LUPP_GRIDSYNC=1 keeps cooperative-groups grid.sync)
+  static const bool gridsync = env_flag("ITERCUR_LUPP_GRIDSYNC");
+  ka.arrivals = gridsync ? nullptr : arrivals;
   void* params[] = {&ka};
   static const bool right_looking = env_flag("ITERCUR_LUPP_RIGHT_LOOKING");  // A/B switch
   if (!right_looking && steps <= 2048) {
