@@ -13,6 +13,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--kinds", default="pageable,pinned")
     args = ap.parse_args()
     import torch
 
@@ -24,12 +25,17 @@ def main():
     kw = dict(epsilon=cfg["epsilon"], b=cfg["b"], seed=0, sketch=cfg["sketch"], max_rank=cfg["max_rank"])
     a = testmat.generate(args.config)
     out = {"config": args.config}
-    for kind in ("pageable", "pinned"):
-        host = torch.empty(n, m, dtype=torch.float64, pin_memory=(kind == "pinned"))
-        host.copy_(a.t())
-        if kind == "pageable":
-            del a
-            torch.cuda.empty_cache()
+    pageable = torch.empty(n, m, dtype=torch.float64)
+    pageable.copy_(a.t())
+    del a
+    torch.cuda.empty_cache()
+    for kind in args.kinds.split(","):
+        if kind == "pinned":
+            host = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+            host.copy_(pageable)
+            del pageable
+        else:
+            host = pageable
         h = engine.MatrixHandle.dense(host.numpy().T)
         engine.iterative_cur(h, **kw)  # warm
         ts = []
