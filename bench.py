@@ -396,18 +396,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference":  # CPU only; the engine is never imported on this arm
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.init_process_group("gloo")
-        rc = run_reference_arm(args, args.config, world)
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-            dist.destroy_process_group()
-        return rc
+    if args.impl == "reference":  # CPU only; the engine is never imported on this arm. Under torchrun
+        # rank 0 alone runs it (no process group: the other ranks exit at once)
+        return run_reference_arm(args, args.config, world)
 
     import numpy as np
     import torch

@@ -1990,13 +1990,30 @@ int itercur_iterative_cur_host(const double* A, int64_t m, int64_t n, int64_t ld
     run->n = n;
     run->lda = std::max<int64_t>(m, 1);
     if (m > 0 && n > 0) {
+      static const bool trace = env_flag("ITERCUR_HOST_TRACE");
+      const auto t0 = std::chrono::steady_clock::now();
       run->A_owned.alloc(static_cast<size_t>(m) * n);
+      const auto t1 = std::chrono::steady_clock::now();
       copy_host_matrix(run->A_owned.p, A, m, n, lda, run->wstream);
+      if (trace) {
+        CK(cudaStreamSynchronize(run->wstream));
+        const auto t2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[itercur host entry] alloc %.1f ms, H2D %.1f ms (%.1f GB/s)\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                8.0 * m * n / std::chrono::duration<double>(t2 - t1).count() / 1e9);
+      }
       run->A = run->A_owned.p;
     }
     run->cfg = cfg ? *cfg : default_config();
+    const auto tr0 = std::chrono::steady_clock::now();
     run_iterative_cur(run.get());
+    const auto tr1 = std::chrono::steady_clock::now();
     if (!run->cfg.keep_device_copy && run->A_owned.p) release_input_copy(run.get());
+    if (env_flag("ITERCUR_HOST_TRACE"))
+      fprintf(stderr, "[itercur host entry] run %.1f ms, release %.1f ms\n",
+              std::chrono::duration<double, std::milli>(tr1 - tr0).count(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr1).count());
     *out = run.release();
   });
 }
