@@ -227,6 +227,13 @@ ITERCUR_API int32_t itercur_run_holds_matrix(const itercur_run* run);
 ITERCUR_API int itercur_copy_to_host(void* dst, const void* d_src, uint64_t bytes);
 /* ||A||_F of a device matrix (proj/src/matrix.cpp:297-302 fro_norm), fixed-order reduction. */
 ITERCUR_API int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda, void* stream, double* out);
+/* The same for a host matrix (streamed through the device in column panels). */
+ITERCUR_API int itercur_fro_norm_host(const double* A, int64_t m, int64_t n, int64_t lda, double* out);
+/* out = X * rhs (transposed = 0) or X^T * rhs (1) for a host r x r matrix X and r x k rhs (column-major,
+   ld r / r / r), computed on the device GEMM: the C++ facade's FactoredPinv for observer snapshots,
+   which hold the materialised core (no host arithmetic in the bindings). */
+ITERCUR_API int itercur_dense_apply_host(const double* X, int64_t r, int32_t transposed, const double* rhs, int64_t k,
+                                         double* out);
 ITERCUR_API int itercur_sketched_residual_device(const itercur_run* run, int64_t b, uint64_t seed, int32_t kind,
                                                  int32_t sparse_nnz, double* out);
 ITERCUR_API void itercur_run_free(itercur_run* run);

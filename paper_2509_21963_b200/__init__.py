@@ -163,7 +163,12 @@ class MatrixHandle:
                 _check(_lib().itercur_fro_norm_device(C.c_void_p(t.data_ptr()), self.rows, self.cols, self.lda,
                                                       C.c_void_p(stream), C.byref(out)))
             return out.value
-        return float(np.linalg.norm(self.to_numpy()))
+        a = self._host if self._csr is None else np.asfortranarray(self._csr[2].reshape(-1, 1))
+        a = np.asfortranarray(a, dtype=np.float64)
+        out = C.c_double()
+        _check(_lib().itercur_fro_norm_host(a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1],
+                                            max(a.shape[0], 1), C.byref(out)))
+        return out.value
 
     def __repr__(self) -> str:
         return f"<MatrixHandle {self.rows}x{self.cols} dense{' device' if self.is_device else ''}>"

@@ -35,7 +35,7 @@ EXPORTED = [
     "itercur_run_holds_matrix", "itercur_copy_to_host",
     "itercur_shard_range", "itercur_iterative_cur_sharded_device", "itercur_iterative_cur_sharded_emulated",
     "itercur_true_relative_error_sharded", "itercur_nccl_unique_id", "itercur_nccl_comm_init",
-    "itercur_nccl_comm_destroy",
+    "itercur_nccl_comm_destroy", "itercur_fro_norm_host", "itercur_dense_apply_host",
 ]
 
 
@@ -121,6 +121,8 @@ def lib() -> C.CDLL:
         "itercur_nccl_unique_id": (C.c_int, [vp]),
         "itercur_nccl_comm_init": (C.c_int, [C.c_int32, vp, C.c_int32, C.POINTER(vp)]),
         "itercur_nccl_comm_destroy": (C.c_int, [vp]),
+        "itercur_fro_norm_host": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, dp]),
+        "itercur_dense_apply_host": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp]),
         "itercur_fro_norm_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, dp]),
         "itercur_sketched_residual_device": (C.c_int, [runp, C.c_int64, C.c_uint64, C.c_int32, C.c_int32, dp]),
         "itercur_run_free": (None, [runp]),

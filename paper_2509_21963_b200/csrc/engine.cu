@@ -2178,6 +2178,76 @@ int itercur_fro_norm_device(const double* dA, int64_t m, int64_t n, int64_t lda,
 }
 void itercur_run_free(itercur_run* run) { delete run; }
 
+int itercur_fro_norm_host(const double* A, int64_t m, int64_t n, int64_t lda, double* out) {
+  return guarded([&] {
+    require_device();
+    if (m < 0 || n < 0 || (m > 0 && n > 0 && lda < m)) fail(ITERCUR_E_INVALID_ARGUMENT, "fro_norm: invalid shape");
+    if (m == 0 || n == 0) {
+      *out = 0.0;
+      return;
+    }
+    cudaStream_t st = work_stream();
+    configure_mempool_once();
+    g_alloc_stream = st;
+    // column panels of <= 512 MB through the device; per-panel sums added in panel order
+    const int64_t w_max = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 26) / m));
+    DevBuf<double> panel;
+    panel.alloc(static_cast<size_t>(m) * w_max);
+    double sq = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += w_max) {
+      const int64_t w = std::min(w_max, n - j0);
+      copy_host_matrix(panel.p, A + j0 * lda, m, w, lda, st);
+      sq += device_sumsq(panel.p, m, w, m, st);
+    }
+    *out = std::sqrt(sq);
+  });
+}
+
+int itercur_dense_apply_host(const double* X, int64_t r, int32_t transposed, const double* rhs, int64_t k,
+                             double* out) {
+  return guarded([&] {
+    require_device();
+    if (r < 0 || k < 0) fail(ITERCUR_E_INVALID_ARGUMENT, "dense_apply: invalid shape");
+    if (r == 0 || k == 0) return;
+    cudaStream_t st = work_stream();
+    configure_mempool_once();
+    g_alloc_stream = st;
+    const int64_t ldop = even(r);
+    DevBuf<double> Xd, op, B, C;
+    Xd.alloc(static_cast<size_t>(r) * r);
+    op.alloc(static_cast<size_t>(ldop) * r);
+    B.alloc(static_cast<size_t>(r) * k);
+    C.alloc(static_cast<size_t>(r) * k);
+    CK(cudaMemcpyAsync(Xd.p, X, sizeof(double) * r * r, cudaMemcpyHostToDevice, st));
+    if (transposed)
+      CK(launch_transpose(Xd.p, r, r, r, op.p, ldop, st));
+    else
+      CK(cudaMemcpy2DAsync(op.p, sizeof(double) * ldop, Xd.p, sizeof(double) * r, sizeof(double) * r, r,
+                           cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(B.p, rhs, sizeof(double) * r * k, cudaMemcpyHostToDevice, st));
+    constexpr int64_t kChunk = 1 << 20;
+    for (int64_t q0 = 0; q0 < k; q0 += kChunk) {
+      TsGemmParams p;
+      p.M = r;
+      p.K = r;
+      p.N = static_cast<int>(std::min(kChunk, k - q0));
+      p.A = op.p;
+      p.lda = ldop;
+      p.B = B.p + q0 * r;
+      p.bsk = 1;
+      p.bsn = r;
+      p.base_mode = kBaseNone;
+      p.alpha = 1.0;
+      p.out_mode = kOutColMajor;
+      p.C0 = C.p + q0 * r;
+      p.ldc0 = r;
+      CK(run_ts_gemm(p, st));
+    }
+    CK(cudaMemcpyAsync(out, C.p, sizeof(double) * r * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
 int itercur_adjusted_threshold(double epsilon, double delta, double alpha, int64_t c, double* out) {
   return guarded([&] { *out = adjusted_threshold_impl(epsilon, delta, alpha, c); });
 }

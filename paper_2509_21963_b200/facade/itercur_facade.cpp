@@ -274,15 +274,15 @@ ITERCUR_FACADE_API double fro_norm(const MatrixHandle& A) {
     check(itercur_fro_norm_device(p.d, p.rows, p.cols, p.ld, nullptr, &out));
     return out;
   }
-  if (p.kind == Kind::Csr) {
-    double s = 0.0;
-    for (double v : p.csr.values) s += v * v;
-    return std::sqrt(s);
+  double out = 0.0;
+  if (p.kind == Kind::Csr) {  // ||values||: the stored entries as one column
+    const Index nnz = static_cast<Index>(p.csr.values.size());
+    if (nnz) check(itercur_fro_norm_host(p.csr.values.data(), nnz, 1, nnz, &out));
+    return out;
   }
   const DenseMatrix& d = detail::host_dense(p);
-  double s = 0.0;
-  for (Index q = 0; q < d.size(); ++q) s += d.data()[q] * d.data()[q];
-  return std::sqrt(s);
+  check(itercur_fro_norm_host(d.data(), d.rows(), d.cols(), std::max<Index>(d.rows(), 1), &out));
+  return out;
 }
 
 // ------------------------------------------------------------------ FactoredPinv
@@ -303,13 +303,9 @@ DenseMatrix apply(const std::shared_ptr<const detail::RunRef>& run, const std::s
     check(itercur_run_core_apply(run->run, transposed ? 1 : 0, rhs.data(), rhs.cols(), r, out.data(), r));
     return out;
   }
-  // observer snapshot: the materialised inverse (copied out of the engine during the callback)
-  const DenseMatrix& X = *host;
-  for (Index j = 0; j < rhs.cols(); ++j)
-    for (Index k = 0; k < r; ++k) {
-      const double b = rhs(k, j);
-      for (Index i = 0; i < r; ++i) out(i, j) += (transposed ? X(k, i) : X(i, k)) * b;
-    }
+  // observer snapshot: the materialised inverse (copied out of the engine during the callback),
+  // applied on the device
+  check(itercur_dense_apply_host(host->data(), r, transposed ? 1 : 0, rhs.data(), rhs.cols(), out.data()));
   return out;
 }
 }  // namespace
