@@ -1568,10 +1568,23 @@ __global__ void __launch_bounds__(kLuppThreads, 2) lupp_panel_kernel(LuppKernelA
   double first = 0.0;
   long long* const dbg = (ka.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? ka.dbg : nullptr;
   for (int s = 0; s < steps; ++s) {
-    if (ka.arrivals && s > 0) panel_wait(ka.arrivals, base + static_cast<unsigned long long>(s) * G);
-    if (dbg) dbg[s * 8 + 0] = clock64();
-    // every warp reduces the whole CTA-candidate list itself: no block barrier on this path
-    const Cand best = panel_reduce_list(ka.cand + (s & 1) * G, G);
+    Cand best;
+    if (ka.arrivals) {
+      // one warp per CTA reads and reduces the CTA-candidate list (every warp reading it put eight
+      // times the requests on the few L2 lines that hold it), then hands the winner to the others
+      if (s > 0) panel_wait(ka.arrivals, base + static_cast<unsigned long long>(s) * G);
+      if (dbg) dbg[s * 8 + 0] = clock64();
+      if (threadIdx.x < 32) {
+        const Cand c = panel_reduce_list(ka.cand + (s & 1) * G, G);
+        if (threadIdx.x == 0) sc[kLuppThreads / 32] = c;
+      }
+      __syncthreads();
+      best = sc[kLuppThreads / 32];
+    } else {
+      if (dbg) dbg[s * 8 + 0] = clock64();
+      // every warp reduces the whole CTA-candidate list itself: no block barrier on this path
+      best = panel_reduce_list(ka.cand + (s & 1) * G, G);
+    }
     if (best.idx < 0 || best.mag <= abs_floor) break;
     if (s == 0)
       first = best.mag;
