@@ -88,7 +88,7 @@ class ClockSampler:
     benchmarking process serialised with its CUDA work (measured: config 2 at 65.6 ms per step
     instead of 32 ms), and spawning nvidia-smi per sample cost ~7% in round 1."""
 
-    def __init__(self, index: int, period: float = 0.2):
+    def __init__(self, index: int, period: float = 0.35):
         self.index = index
         self.period = period
         self.samples = []  # (sm_mhz, sm_max_mhz, hw_slowdown, hw_thermal, sw_thermal, sw_power_cap)
