@@ -639,9 +639,19 @@ void run_iterative_cur(itercur_run* run) {
     CK(cudaMemGetInfo(&free_b, &total_b));
     const int64_t full = max_rank + b;
     const double full_bytes = 8.0 * static_cast<double>(run->ldL + run->ldR + b) * static_cast<double>(full);
-    const int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
-                              ? full
-                              : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
+    int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
+                        ? full
+                        : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
+    if (use_nccl) {
+      // the capacity sizes the packed block every rank allreduces (and the graphs' shapes): the
+      // ranks' free memory differs with their shards, so they agree on the smallest choice
+      double v = static_cast<double>(first);
+      CK(cudaMemcpyAsync(red.p, &v, sizeof(double), cudaMemcpyHostToDevice, st));
+      nck(nc->AllReduce(red.p, red.p, 1, ncclDouble, ncclMin, sh.comm, st), "allreduce capacity");
+      CK(cudaMemcpyAsync(&v, red.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      first = static_cast<int64_t>(v);
+    }
     grow_factors(run, first, st);
   }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
