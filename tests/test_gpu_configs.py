@@ -28,7 +28,7 @@ def _host_gb():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfgno", [2, 3, pytest.param(4, marks=pytest.mark.skipif(not BIG, reason="ITERCUR_FULL_PARITY=1")),
+@pytest.mark.parametrize("cfgno", [1, 2, 3, pytest.param(4, marks=pytest.mark.skipif(not BIG, reason="ITERCUR_FULL_PARITY=1")),
                                    pytest.param(5, marks=pytest.mark.skipif(not BIG, reason="ITERCUR_FULL_PARITY=1"))])
 def test_full_size_config_matches_oracle(engine, oracle, cfgno):
     import parity_configs
