@@ -137,9 +137,29 @@ __device__ __forceinline__ double gemm_base(const TsGemmParams& p, int64_t i, in
   }
 }
 
+// base values of this thread's C fragment (split 0 only): issued before the main loop when
+// p.early_base (the gathers — A(I_k,:) rows at ~1 TB/s of 32-byte sectors — overlap the DMMA
+// loop instead of following it), else in the epilogue
+template <int NT>
+__device__ __forceinline__ void gemm_load_base(const TsGemmParams& p, double (&bv)[NT][4], int64_t r0, int64_t q0,
+                                               int nvalid) {
+  const int t = threadIdx.x & 3;
+  const bool finisher = blockIdx.z == 0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq)
+#pragma unroll
+      for (int dr = 0; dr < 2; ++dr) {
+        const int ql = nt * 8 + 2 * t + dq;
+        const int64_t i = r0 + dr;
+        bv[nt][dr * 2 + dq] = (finisher && ql < nvalid && i < p.M) ? gemm_base(p, i, q0 + ql) : 0.0;
+      }
+}
+
 template <int NT, int WARPS, bool UB = false>
-__device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double* gsm, int64_t i0,
-                                              int64_t q0, int nvalid, int splits) {
+__device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double (&bv)[NT][4],
+                                              double* gsm, int64_t i0, int64_t q0, int nvalid, int splits) {
   constexpr int THREADS = WARPS * 32;
   constexpr int W = NT * 8;
   constexpr int NTY = NT + 1;
@@ -151,17 +171,8 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
   // epilogue operands fetched before the split-K exchange (their latency overlaps it): the
   // base values, and for the U block the Y^T rows to downdate and D_k's factors / Y(:,J_k)
   const bool finisher = blockIdx.z == 0;
-  double bv[NT][4], yv[NTY][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int dq = 0; dq < 2; ++dq)
-#pragma unroll
-      for (int dr = 0; dr < 2; ++dr) {
-        const int ql = nt * 8 + 2 * t + dq;
-        const int64_t i = r0 + dr;
-        bv[nt][dr * 2 + dq] = (finisher && ql < nvalid && i < p.M) ? gemm_base(p, i, q0 + ql) : 0.0;
-      }
+  double yv[NTY][4];
+  if (!p.early_base) gemm_load_base<NT>(p, bv, r0, q0, nvalid);
   double* s_lu = gsm + NT * 4 * THREADS;  // past the split-K exchange buffer
   double* s_yg = s_lu + W * W + W;  // (W reciprocals behind the LU block)
   if constexpr (UB) {
@@ -576,6 +587,8 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
   const int kb = static_cast<int>(blockIdx.z) * per_split;
   const int nk = max(0, min(nk_all - kb, per_split));
   const int64_t kbase = static_cast<int64_t>(kb) * kGemmKT;
+  double bv[NT][4];
+  if (p.early_base) gemm_load_base<NT>(p, bv, i0 + warp * 16 + 2 * g, q0, nvalid);
 #pragma unroll
   for (int s = 0; s < kGemmStages - 1; ++s) {
     if (s < nk)
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_kernel(TsGemmParams p) {
   }
   cp_async_wait<0>();
   griddep_launch_dependents();
-  gemm_epilogue<NT, WARPS>(p, acc, gsm, i0, q0, nvalid, splits);
+  gemm_epilogue<NT, WARPS>(p, acc, bv, gsm, i0, q0, nvalid, splits);
 }
 
 
@@ -725,6 +738,8 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
 
+  double bv[NT][4];
+  if (p.early_base) gemm_load_base<NT>(p, bv, i0 + warp * 16 + 2 * g, q0, nvalid);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load(s, kb + s);
@@ -752,7 +767,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
   }
   cp_async_wait<0>();
   griddep_launch_dependents();
-  gemm_epilogue<NT, WARPS, UB>(p, acc, gsm, i0, q0, nvalid, splits);
+  gemm_epilogue<NT, WARPS, UB>(p, acc, bv, gsm, i0, q0, nvalid, splits);
 }
 
 // CTA height: 64 rows (4 warps) unless overridden; measured best across the row-residual,
@@ -879,7 +894,17 @@ static cudaError_t launch_ublock_nt(const TsGemmParams& p, cudaStream_t st) {
   return e;
 }
 
-cudaError_t run_ts_gemm_ublock(const TsGemmParams& p, cudaStream_t st) {
+// early base loads for blocks up to 32 wide (config 2: 33.2 -> 32.7 ms); wider blocks keep them in
+// the epilogue (config 4: no change; config 5, N = 64: 80.3 -> 82 ms, the extra 64 live registers)
+static TsGemmParams resolve_early_base(const TsGemmParams& p0) {
+  static const int env = env_int("ITERCUR_GEMM_EARLY_BASE", -1);  // A/B: 0 off, 1 on
+  TsGemmParams p = p0;
+  if (p.early_base < 0) p.early_base = env >= 0 ? env : (p.N <= 32 ? 1 : 0);
+  return p;
+}
+
+cudaError_t run_ts_gemm_ublock(const TsGemmParams& p0, cudaStream_t st) {
+  const TsGemmParams p = resolve_early_base(p0);
   if (!ts_gemm_ublock_supported(p)) return cudaErrorNotSupported;
   if (p.M <= 0) return cudaSuccess;
   switch (ts_gemm_nt_host(p.N)) {
@@ -912,7 +937,8 @@ int ts_gemm_planned_splits(const TsGemmParams& p, bool ublock) {
   return g_planned_z;
 }
 
-cudaError_t run_ts_gemm(const TsGemmParams& p, cudaStream_t st) {
+cudaError_t run_ts_gemm(const TsGemmParams& p0, cudaStream_t st) {
+  const TsGemmParams p = resolve_early_base(p0);
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   switch (ts_gemm_nt(p.N)) {
     case 1: return launch_nt<1>(p, st);

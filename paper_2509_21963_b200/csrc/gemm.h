@@ -54,6 +54,7 @@ struct TsGemmParams {
   CommitArgs commit;        // U block: when commit.ctl is set, the last CTA also commits the iteration
   int64_t k_plan = 0;        // host-side hint: the K the split count is planned for (0: K)
   int64_t dbg_k = 0;         // ... recorded at iteration ctl->k == dbg_k
+  int early_base = -1;       // base values loaded before the main loop (-1: by width, see gemm.cu)
   long long* dbg = nullptr;  // optional trace (U block): [0..15] clock64 phases of CTA (0,0,0); [32+2c] globaltimer entry/exit of CTA c
   int k_from_r = 0;
   int64_t a_off_per_r = 0;
