@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -593,6 +594,7 @@ void run_iterative_cur(itercur_run* run) {
   CK(cudaMemsetAsync(ws.col_mask.p, 0, n_glob, st));
   CK(cudaMemsetAsync(ws.row_mask.p, 0, m, st));
   ws.lupp_scratch.alloc(lupp_scratch_bytes(B));
+  CK(lupp_scratch_init(ws.lupp_scratch.p, st));
   const bool col_qrcp = cfg.col_method == ITERCUR_PIVOT_QRCP, row_qrcp = cfg.row_method == ITERCUR_PIVOT_QRCP;
   if (sh.active && (col_qrcp || row_qrcp))
     fail(ITERCUR_E_INVALID_ARGUMENT, "column-sharded runs support LUPP selection only");
@@ -2371,6 +2373,7 @@ static int select_impl(const double* dM, int64_t rows, int64_t cols, int64_t ldm
     mask.alloc(wrows);
     CK(cudaMemcpyAsync(mask.p, hmask.data(), wrows, cudaMemcpyHostToDevice, st));
     scratch.alloc(lupp_scratch_bytes(static_cast<int>(steps)));
+    CK(lupp_scratch_init(scratch.p, st));
     const int S = static_cast<int>(steps);
     outs.alloc(sizeof(int64_t) * S * 3 + 16);
     int64_t* d_idx = reinterpret_cast<int64_t*>(outs.p);
@@ -2520,6 +2523,7 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
     CK(cudaMemsetAsync(mask.p, 0, rows, st));
     DevBuf<char> scratch, outs;
     scratch.alloc(lupp_scratch_bytes(steps));
+    CK(lupp_scratch_init(scratch.p, st));
     outs.alloc(sizeof(int64_t) * steps * 3 + 16);
     LuppArgs la{};
     la.W = W.p;
@@ -2568,7 +2572,18 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
       std::vector<long long> h(static_cast<size_t>(steps) * 16);
       CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 16, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      if (used <= -200000) {  // panel kernel (8 slots per step)
+      if (used <= -300000) {  // resident kernel, per step s: [0] t0 after B1, [1] t0 after B2, [2] t32 pick done,
+        // [3] t32 after the publish barrier, [4] t32 update done, [5] t0 published, [6] headers, [7] tail
+        for (int q = 0; q + 1 < steps; ++q) {
+          const long long* v = h.data() + q * 8;
+          const long long* w = v + 8;
+          fprintf(stderr,
+                  "lupp resident step %d: [t0] B1->B2 %lld publish %lld headers %lld tail %lld B1 %lld | [t32] B1->picked "
+                  "%lld ->bar1 %lld update %lld | step %lld\n",
+                  q, v[1] - v[0], v[5] - v[1], w[6] - v[5], w[7] - w[6], w[0] - w[7], v[2] - v[0], v[3] - v[2],
+                  v[4] - v[3], w[0] - v[0]);
+        }
+      } else if (used <= -200000) {  // panel kernel (8 slots per step)
         for (int q = 0; q + 1 < steps; ++q) {
           const long long* v = h.data() + q * 8;
           fprintf(stderr,
@@ -2593,6 +2608,43 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
                 "B1(after exch) %lld step %lld\n",
                 q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[4] - v[3], v[5] - v[4], v[6] - v[2], v[7] - v[5],
                 v[8] - v[0]);
+      }
+    }
+    if (env_flag("ITERCUR_LUPP_GTRACE")) {  // resident path: skew of the per-step exchange over the CTAs
+      const int G = kNumSMs;
+      DevBuf<long long> tr;
+      tr.alloc(static_cast<size_t>(steps) * G * 4);
+      CK(cudaMemsetAsync(tr.p, 0, sizeof(long long) * steps * G * 4, st));
+      set_lupp_force_path(force_path);
+      set_lupp_grid_trace(tr.p);
+      CK(cudaMemcpyAsync(W.p, W0.p, sizeof(double) * ldw * steps, cudaMemcpyDeviceToDevice, st));
+      CK(run_lupp_with_scratch(la, scratch.p, st, &used));
+      set_lupp_grid_trace(nullptr);
+      set_lupp_force_path(0);
+      std::vector<long long> h(static_cast<size_t>(steps) * G * 4);
+      CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const int Gu = used <= -300000 ? -used - 300000 : G;
+      for (int q = 1; q + 1 < steps; ++q) {
+        long long pmin = LLONG_MAX, pmax = 0, hmin = LLONG_MAX, hmax = 0, tmin = LLONG_MAX, tmax = 0, last = 0;
+        long long cmax = 0, csum = 0;
+        for (int g = 0; g < Gu; ++g) {
+          const long long* v = h.data() + (static_cast<size_t>(q) * G + g) * 4;
+          const long long* pv = h.data() + (static_cast<size_t>(q - 1) * G + g) * 4;
+          if (v[0] > pmax) pmax = v[0], last = g;
+          pmin = std::min(pmin, v[0]);
+          hmin = std::min(hmin, v[1]);
+          hmax = std::max(hmax, v[1]);
+          tmin = std::min(tmin, v[2]);
+          tmax = std::max(tmax, v[2]);
+          const long long c = v[0] - pv[2];  // this CTA: tail of step q-1 seen -> record q published
+          cmax = std::max(cmax, c);
+          csum += c;
+        }
+        fprintf(stderr,
+                "gtrace step %d: publish spread %lld ns (last CTA %lld) | last publish -> headers seen %lld..%lld ns | "
+                "headers -> tail %lld..%lld ns | tail seen -> publish mean %lld max %lld ns\n",
+                q, pmax - pmin, last, hmin - pmax, hmax - pmax, tmin - hmin, tmax - hmax, csum / Gu, cmax);
       }
     }
     cudaEventDestroy(e0);

@@ -175,6 +175,7 @@ cudaError_t run_qrcp(double* W, int64_t ncand, int len, const int* d_len, int64_
 // begin_ctl / post gathers; the other paths ignore them and the caller launches them itself)
 bool lupp_fuses_iteration_work(const LuppArgs& a);
 size_t lupp_scratch_bytes(int b);
+cudaError_t lupp_scratch_init(void* scratch, cudaStream_t st);  // after every allocation
 // column-sharded engine building blocks (shard.cu)
 cudaError_t launch_lupp_dist_step(double* W, int64_t rows, int64_t ldw, int steps, int s, const double* P,
                                   int64_t piv_local, uint8_t* live, int64_t row_offset, double* cand,
@@ -185,5 +186,6 @@ cudaError_t launch_clear_epochs(uint8_t* mask, int64_t count, cudaStream_t st);
 // benchmarking: 0 automatic, 1 cluster only, 2 grid shared-memory only, 3 global only
 void set_lupp_force_path(int path);
 void set_lupp_debug_trace(long long* dbg);  // per-step clock64() trace of CTA 0 (grid path)
+void set_lupp_grid_trace(long long* gdbg);  // resident path: globaltimer stamps of every CTA per step
 
 }  // namespace itercur_b200

@@ -776,6 +776,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
 
 
 static long long* g_lupp_dbg = nullptr;
+static long long* g_lupp_gdbg = nullptr;
 static int g_force_path = 0;  // benchmarking: 0 automatic, 1 cluster, 2 grid smem, 3 global
 
 // ---------------------------------------------------------------------------------
@@ -1685,6 +1686,563 @@ __global__ void __launch_bounds__(kLuppThreads, 2) lupp_panel_kernel(LuppKernelA
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Resident grid LUPP (round 2): the whole slab stays on chip for the call — one CTA per SM owns
+// a contiguous block of at most 704 rows, one row per thread, the row's last KR columns in that
+// thread's registers and its leading columns in shared memory (config 4: 100000 x 50 = 40 MB
+// over 148 SMs' registers + shared memory). Per pivot step the slab is never re-read from L2;
+// the only global traffic is the candidate exchange, and that exchange needs no fence, atomic
+// or barrier: every (step, CTA) has its own record (header + the candidate row's tail) in a
+// region cleared to an all-ones sentinel before the call (by the previous call, which clears
+// the other of two regions), each word is written exactly once, so a reader that sees a word
+// different from the sentinel sees its final value. One warp per CTA polls the step's headers,
+// reduces them in the reference's order, then polls the winner's tail (two L2 round trips).
+//   step s: [B1] f = W(i,s)/pivot (Markstein), column s+1 updated first, warp argmax; [B2] the
+//   CTA winner's owner publishes its tail (columns > s+1 updated on the fly) while every row
+//   applies the rest of the step's update — overlapped with the exchange of step s+1.
+// Same per-element arithmetic as the kernels above (separate multiply and subtract roundings,
+// correctly rounded division), so the pivot sequence is the reference's bit for bit. The pivot
+// rows' LU factors (row s of D_k = multipliers of steps < s, then the pivot row) are written
+// by the thread that owns the pivot row.
+// ---------------------------------------------------------------------------------
+constexpr int kResThreads = 384;  // warp 0: exchange; warps 1..11: two rows per thread
+constexpr int kResWarps = kResThreads / 32;
+constexpr int kResRowThreads = kResThreads - 32;
+constexpr int kResRPT = 2;  // rows per row thread: local rows lr and lr + kResRowThreads
+constexpr int kResKR = 16;  // trailing columns per row held in registers
+constexpr int kResMaxSteps = 64;
+constexpr int kResPanel = 4;              // shared-memory columns updated once per 4 pivot steps
+constexpr int kResRing = 8;  // pivot rows kept (>= kResPanel + 1; a power of two: slot = step & 7)
+constexpr int kResMaxG = 148;
+constexpr int kResRec = 4 + kResMaxSteps;  // header (key, row, runner-up key, 0) + row tail
+constexpr size_t kResRegionWords = kResMaxG + static_cast<size_t>(kResMaxSteps) * kResMaxG * kResRec;
+constexpr uint64_t kResEmpty = ~0ull;
+constexpr uint64_t kResMagic = 0x1C0B200A5A5E0002ull;
+constexpr size_t kResScratchBytes = 64 + 2 * kResRegionWords * sizeof(uint64_t);
+
+struct LuppResArgs {
+  LuppArgs a;
+  uint64_t* ctl;     // [0] magic, [1] call counter (region parity), [2] exchange time-out flag
+  uint64_t* region;  // two regions of kResRegionWords: norm partials [kResMaxG], records [step][CTA]
+  int rows_per_cta;
+  long long* dbg;    // optional per-step clock64() trace of CTA 0 (8 slots per step)
+  long long* gdbg;   // optional per-step globaltimer stamps of every CTA: [step][CTA][published, headers, tail]
+  int backoff_ns;    // experiments: sleep between polls of an unpublished record
+};
+
+#if defined(ITERCUR_RES_LD_CG)
+#define ITERCUR_RES_LD "ld.global.cg"
+#elif defined(ITERCUR_RES_LD_VOLATILE)
+#define ITERCUR_RES_LD "ld.volatile.global"
+#else
+#define ITERCUR_RES_LD "ld.relaxed.gpu.global"
+#endif
+__device__ __forceinline__ uint64_t res_ld(const uint64_t* p) {
+  uint64_t v;
+  asm volatile(ITERCUR_RES_LD ".u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void res_ld2(const uint64_t* p, uint64_t& x, uint64_t& y) {
+  asm volatile(ITERCUR_RES_LD ".v2.u64 {%0, %1}, [%2];\n" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void res_st(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void res_st2(uint64_t* p, uint64_t x, uint64_t y) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+// a row value as a record word: never the sentinel (a NaN with every bit set becomes the
+// canonical quiet NaN; finite inputs never produce it)
+__device__ __forceinline__ uint64_t res_enc(double v) {
+  const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+  return u == kResEmpty ? 0x7FF8000000000000ull : u;
+}
+__device__ __forceinline__ uint64_t res_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+constexpr uint64_t kResTimeoutNs = 2000000000ull;  // a lost record ends the call instead of hanging
+
+// Shared-memory column t of the resident LUPP is brought current at the steps s' = t (mod
+// kResPanel) with s' <= t - 2; before the update pass of step s it is current through the last
+// such s' <= s - 1 (-1: still the input). Its pending steps are (res_last_update(t, s), s].
+__device__ __forceinline__ int res_last_update(int t, int s) {
+  const int m = min(s - 1, t - 2);
+  if (m < 0) return -1;
+  int r = (m - t) % kResPanel;
+  if (r < 0) r += kResPanel;
+  return m - r < 0 ? -1 : m - r;
+}
+
+template <int KR>
+__global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResArgs ka) {
+  const LuppArgs& a = ka.a;
+  extern __shared__ double Ws[];  // [R0][ldS]: columns 0..R0-1 of the CTA's rows (odd ldS: no bank conflicts along a row)
+  __shared__ double Pr[kResRing][kResMaxSteps];  // pivot rows of the open panel + the next step
+  __shared__ double stage[kResWarps][kResKR + 2];  // each row warp's winner: register columns, multiplier, next-column value
+  __shared__ double emit[kResKR];  // the retired pivot row's register columns (its LU row)
+  __shared__ WCand wc[kResWarps];
+  __shared__ WCand s_best;
+  __shared__ double s_y, s_nsq;
+  __shared__ double s_red[kResWarps];
+  __shared__ int s_abort;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = threadIdx.x - 32;  // row threads: local rows lr and lr + kResRowThreads
+  const int Rb = ka.rows_per_cta, ldS = Rb | 1;
+  const int64_t r0 = static_cast<int64_t>(g) * Rb;
+  int64_t nr64 = a.rows - r0;
+  nr64 = nr64 < 0 ? 0 : (nr64 > Rb ? Rb : nr64);
+  const int nr = static_cast<int>(nr64);
+  int steps = a.cols_max;
+  if (a.d_steps) steps = min(steps, *a.d_steps);
+  if (steps <= 0) {
+    if (g == 0 && threadIdx.x == 0) {
+      *a.d_count = 0;
+      if (a.d_width_out) *a.d_width_out = 0;
+    }
+    return;
+  }
+  const int R0 = steps > KR ? steps - KR : 0;  // columns [R0, steps) live in registers
+  const int64_t ldw = a.ldw;
+
+  // region of this call (parity of the call counter); the other region is cleared for the next
+  // call. First use of a scratch buffer (no magic yet): clear this call's region too, grid-wide.
+  const uint64_t magic = res_ld(ka.ctl), callno = res_ld(ka.ctl + 1);
+  const bool fresh = magic != kResMagic;
+  const int par = fresh ? 0 : static_cast<int>(callno & 1);
+  uint64_t* reg = ka.region + static_cast<size_t>(par) * kResRegionWords;
+  auto clear_region = [&](uint64_t* base) {
+    constexpr size_t n2 = kResRegionWords / 2;
+    const size_t per = (n2 + G - 1) / G, lo = static_cast<size_t>(g) * per, hi = min(n2, lo + per);
+    for (size_t u = lo + threadIdx.x; u < hi; u += kResThreads) res_st2(base + 2 * u, kResEmpty, kResEmpty);
+  };
+  if (fresh) {
+    clear_region(reg);
+    cg::this_grid().sync();
+  }
+  clear_region(ka.region + static_cast<size_t>(par ^ 1) * kResRegionWords);
+  uint64_t* const norms = reg;
+  auto rec = [&](int s, int q) { return reg + kResMaxG + (static_cast<size_t>(s) * kResMaxG + q) * kResRec; };
+
+  // ---- load: row thread lr owns local rows lr + k * kResRowThreads (k < kResRPT) ----
+  double xr[kResRPT][KR];
+  bool live[kResRPT], has[kResRPT];
+#pragma unroll
+  for (int k = 0; k < kResRPT; ++k) {
+    const int l = lr + k * kResRowThreads;
+    has[k] = warp > 0 && l < nr;
+    live[k] = false;
+    if (has[k]) {
+      const double* src = a.W + r0 + l;
+      double* w = Ws + l;
+#pragma unroll 8
+      for (int t = 0; t < R0; ++t) w[t * ldS] = src[t * ldw];
+#pragma unroll
+      for (int j = 0; j < KR; ++j) xr[k][j] = R0 + j < steps ? src[(R0 + j) * ldw] : 0.0;
+      const uint8_t mk = a.mask[r0 + l];
+      live[k] = !(mk == 1 || mk == a.epoch);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KR; ++j) xr[k][j] = 0.0;
+    }
+  }
+  const bool need_norm = a.d_norm_sq == nullptr;
+  if (need_norm) {  // ||W(:, 0:steps)||_F^2: this CTA's partial, published for every CTA
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < kResRPT; ++k)
+      if (has[k]) {
+        const double* w = Ws + lr + k * kResRowThreads;
+        for (int t = 0; t < R0; ++t) sq = fma(w[t * ldS], w[t * ldS], sq);
+#pragma unroll
+        for (int j = 0; j < KR; ++j)
+          if (R0 + j < steps) sq = fma(xr[k][j], xr[k][j], sq);
+      }
+    const double b = block_sum<kResThreads>(sq, s_red);
+    if (threadIdx.x == 0) res_st(norms + g, res_enc(b));
+  }
+
+#ifdef ITERCUR_RES_TRACE
+  long long* const dbg = (ka.dbg && g == 0) ? ka.dbg : nullptr;
+#else
+  constexpr long long* dbg = nullptr;
+#endif
+  const int backoff = ka.backoff_ns;
+  // ---- the exchange (warp 0): step s's CTA headers -> winner; its record -> the pivot row
+  //      Pr[s % ring], its reciprocal and the runner-up ----
+  auto exchange = [&](int s) {
+    const uint64_t t0 = res_now();
+    bool timed_out = false;
+    auto wait = [&](uint64_t& spins) {
+      if ((++spins & 255) == 0 && res_now() - t0 > kResTimeoutNs) timed_out = true;
+      if (backoff) __nanosleep(backoff);
+      return !timed_out;
+    };
+    // every header of the step polled at once (one L2 round trip when they are all there; a lane
+    // re-polls only its missing ones); headers carry (key, row) only: the CTA keys give the winner
+    // and the runner-up among CTA winners, the winning CTA's own runner-up is read with its row
+    constexpr int QN = (kResMaxG + 31) / 32;
+    unsigned pending = 0;
+#pragma unroll
+    for (int u = 0; u < QN; ++u)
+      if (lane + 32 * u < G) pending |= 1u << u;
+    WCand c{0ull, 0x7fffffff, -1.0};
+    uint64_t spins = 0;
+    while (true) {
+      uint64_t k[QN], ix[QN];
+#pragma unroll
+      for (int u = 0; u < QN; ++u)
+        if (pending >> u & 1) res_ld2(rec(s, lane + 32 * u), k[u], ix[u]);
+#pragma unroll
+      for (int u = 0; u < QN; ++u)
+        if ((pending >> u & 1) && k[u] != kResEmpty && ix[u] != kResEmpty) {
+          pending &= ~(1u << u);
+          wcand_merge(c, k[u], static_cast<int32_t>(ix[u]), -1.0);
+        }
+      if (!pending || !wait(spins)) break;
+    }
+    WCand best = warp_argmax(c);
+    if (dbg && lane == 0) dbg[s * 8 + 6] = clock64();
+#ifdef ITERCUR_RES_TRACE
+    if (ka.gdbg && lane == 0) ka.gdbg[(static_cast<size_t>(s) * G + g) * 4 + 1] = static_cast<long long>(res_now());
+#endif
+    double* Pn = Pr[s & (kResRing - 1)];
+    double y = 0.0;
+    if (best.key) {  // words 2, 3: runner-up key, RN(1/pivot); 4 + t: the row
+      const uint64_t* wr = rec(s, static_cast<int>(best.idx / Rb));
+      const int t0 = s + lane, t1 = s + lane + 32;
+      uint64_t u0 = 0, u1 = 0, uh0 = 0, uh1 = 0;
+      bool w0 = t0 < steps, w1 = t1 < steps, wh = lane == 0;
+      spins = 0;
+      while (true) {
+        if (w0) u0 = res_ld(wr + 4 + t0);
+        if (w1) u1 = res_ld(wr + 4 + t1);
+        if (wh) res_ld2(wr + 2, uh0, uh1);
+        w0 = w0 && u0 == kResEmpty;
+        w1 = w1 && u1 == kResEmpty;
+        wh = wh && (uh0 == kResEmpty || uh1 == kResEmpty);
+        if (!(w0 || w1 || wh) || !wait(spins)) break;
+      }
+      if (t0 < steps) Pn[t0] = __longlong_as_double(static_cast<long long>(u0));
+      if (t1 < steps) Pn[t1] = __longlong_as_double(static_cast<long long>(u1));
+      if (lane == 0) {
+        if (uh0) best.second = fmax(best.second, key_mag(uh0));
+        y = __longlong_as_double(static_cast<long long>(uh1));
+      }
+    }
+    if (s == 0 && need_norm) {  // the CTA partials in a fixed tree: every CTA forms the same sum
+      uint64_t nv[QN];
+      unsigned pn = 0;
+#pragma unroll
+      for (int u = 0; u < QN; ++u)
+        if (lane + 32 * u < G) pn |= 1u << u;
+      spins = 0;
+      while (true) {
+#pragma unroll
+        for (int u = 0; u < QN; ++u)
+          if (pn >> u & 1) nv[u] = res_ld(norms + lane + 32 * u);
+#pragma unroll
+        for (int u = 0; u < QN; ++u)
+          if ((pn >> u & 1) && nv[u] != kResEmpty) pn &= ~(1u << u);
+        if (!pn || !wait(spins)) break;
+      }
+      double v = 0.0;
+#pragma unroll
+      for (int u = 0; u < QN; ++u)
+        if (lane + 32 * u < G) v += __longlong_as_double(static_cast<long long>(nv[u]));
+      v = warp_sum(v);
+      if (lane == 0) s_nsq = v;
+    }
+    const bool abort = __any_sync(0xffffffffu, timed_out);
+    if (dbg && lane == 0) dbg[s * 8 + 7] = clock64();
+#ifdef ITERCUR_RES_TRACE
+    if (ka.gdbg && lane == 0) ka.gdbg[(static_cast<size_t>(s) * G + g) * 4 + 2] = static_cast<long long>(res_now());
+#endif
+    if (lane == 0) {
+      s_best = best;
+      s_y = y;
+      s_abort = abort ? 1 : 0;
+      if (abort) atomicExch(reinterpret_cast<unsigned long long*>(ka.ctl + 2), 1ull);
+    }
+  };
+  // ---- record sp of this CTA (warp 0, after [B2]): the CTA winner over the row warps' winners;
+  //      header (key, row); runner-up and RN(1/value); the winner's row, current: shared-memory
+  //      columns with the open panel's terms p0..pe in step order, register columns and the
+  //      next-column value as its warp staged them ----
+  auto publish = [&](int sp) {
+    const WCand c = lane < kResWarps ? wc[lane] : WCand{0ull, 0x7fffffff, -1.0};
+    const WCand cb = warp_argmax(c);
+    uint64_t* r = rec(sp, g);
+    if (cb.key) {
+      const int olr = static_cast<int>(cb.idx - r0), w = (olr % kResRowThreads) / 32 + 1;
+      const double* orow = Ws + olr;
+      if (lane == 0) res_st2(r, cb.key, static_cast<uint64_t>(cb.idx));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = sp + lane + 32 * h;
+        if (t >= steps) continue;
+        double v;
+        if (t == sp) {
+          v = stage[w][KR + 1];
+        } else if (t < R0) {  // shared-memory column: its pending steps (res_last_update(t, sp - 1), sp - 1]
+          v = orow[t * ldS];
+          for (int j = res_last_update(t, sp - 1) + 1; j < sp; ++j)
+            v = __dsub_rn(v, __dmul_rn(orow[j * ldS], Pr[j & (kResRing - 1)][t]));
+        } else {  // register column: current through step sp - 2, step sp - 1's term owed
+          v = stage[w][t - R0];
+          if (sp > 0) v = __dsub_rn(v, __dmul_rn(stage[w][KR], Pr[(sp - 1) & (kResRing - 1)][t]));
+        }
+        res_st(r + 4 + t, res_enc(v));
+      }
+      if (lane == 1)
+        res_st2(r + 2, cb.second >= 0.0 ? mag_key(cb.second) : 0ull,
+                static_cast<uint64_t>(__double_as_longlong(__drcp_rn(stage[w][KR + 1]))));
+    } else if (lane == 0) {
+      res_st2(r, 0ull, 0ull);
+      res_st2(r + 2, 0ull, 0ull);
+    }
+#ifdef ITERCUR_RES_TRACE
+    if (ka.gdbg && lane == 0) ka.gdbg[(static_cast<size_t>(sp) * G + g) * 4] = static_cast<long long>(res_now());
+#endif
+  };
+  // row warps: this thread's candidate over its rows (ascending local row: ties keep the lower),
+  // the warp argmax, and the warp winner's registers + next-column value staged for the publish
+  double cur[kResRPT];
+#pragma unroll
+  for (int k = 0; k < kResRPT; ++k) cur[k] = 0.0;
+  double fk[kResRPT];
+#pragma unroll
+  for (int k = 0; k < kResRPT; ++k) fk[k] = 0.0;
+  auto warp_pick = [&]() {
+    WCand mine{0ull, 0x7fffffff, -1.0};
+#pragma unroll
+    for (int k = 0; k < kResRPT; ++k)
+      if (live[k]) mine = wcand_merge_row(mine, fabs(cur[k]), static_cast<int32_t>(r0 + lr + k * kResRowThreads));
+    const WCand w = warp_argmax(mine);
+    if (w.key) {
+#pragma unroll
+      for (int k = 0; k < kResRPT; ++k)
+        if (live[k] && static_cast<int64_t>(w.idx) == r0 + lr + k * kResRowThreads) {
+#pragma unroll
+          for (int j = 0; j < KR; ++j) stage[warp][j] = xr[k][j];
+          stage[warp][KR] = fk[k];
+          stage[warp][KR + 1] = cur[k];
+        }
+    }
+    if (lane == 0) wc[warp] = w;
+  };
+
+  // ---- step-0 candidates (column 0) ----
+  if (warp > 0) {
+#pragma unroll
+    for (int k = 0; k < kResRPT; ++k)
+      if (live[k]) cur[k] = R0 > 0 ? Ws[lr + k * kResRowThreads] : xr[k][0];
+    warp_pick();
+  } else if (lane == 0) {
+    wc[0] = WCand{0ull, 0x7fffffff, -1.0};
+  }
+  __syncthreads();
+  if (warp == 0) publish(0);
+
+  double* lu_blk = a.lu_out ? a.lu_out + (a.d_lu_r ? *a.d_lu_r : 0) * a.lu_ld : nullptr;
+  int count = 0;
+  double first = 0.0, abs_floor = 0.0;
+  for (int s = 0; s < steps; ++s) {
+    if (warp == 0) exchange(s);
+    __syncthreads();  // B1
+    if (dbg && threadIdx.x == 0) dbg[s * 8 + 0] = clock64() + 0 * s_best.key;
+    if (s_abort) break;
+    if (s == 0) abs_floor = 1e2 * 2.220446049250313e-16 * sqrt(need_norm ? s_nsq : *a.d_norm_sq);
+    const WCand best = s_best;
+    const double bm = key_mag(best.key);
+    if (best.key == 0 || bm <= abs_floor) break;
+    if (s == 0)
+      first = bm;
+    else if (bm < a.pivot_floor * first)
+      break;
+    if (g == 0 && threadIdx.x == 0) {
+      a.d_idx[s] = best.idx;
+      a.d_best[s] = bm;
+      a.d_second[s] = best.second;
+    }
+    ++count;
+    const double* Pc = Pr[s & (kResRing - 1)];
+    const bool mine_pivot = best.idx >= r0 && best.idx < r0 + nr;
+#pragma unroll
+    for (int k = 0; k < kResRPT; ++k)
+      if (live[k] && r0 + lr + k * kResRowThreads == best.idx) {  // the pivot row retires; its
+        live[k] = false;                                           // register columns for its LU row
+        if (lu_blk) {
+#pragma unroll
+          for (int j = 0; j < KR; ++j) emit[j] = xr[k][j];
+        }
+      }
+    if (s + 1 >= steps) {
+      if (lu_blk && mine_pivot) {
+        __syncthreads();
+        if (warp == 0) {
+          const int olr = static_cast<int>(best.idx - r0);
+          for (int t = lane; t < steps; t += 32)
+            lu_blk[s + t * a.lu_ld] = t >= s ? Pc[t] : (t < R0 ? Ws[olr + t * ldS] : emit[t - R0]);
+        }
+      }
+      break;
+    }
+    if (warp > 0) {
+      const double pivot = Pc[s], ys = s_y;
+      const bool p_ok = pivot_in_range(pivot);
+      const int t1 = s + 1, j1 = res_last_update(t1, s) + 1;  // column t1's pending steps j1..s
+#pragma unroll
+      for (int k = 0; k < kResRPT; ++k) {
+        if (!live[k]) continue;
+        double* w = Ws + lr + k * kResRowThreads;
+        const double f = div_by_pivot(cur[k], pivot, ys, p_ok);
+        fk[k] = f;
+        if (s < R0) {
+          w[s * ldS] = f;
+        } else {
+#pragma unroll
+          for (int j = 0; j < KR; ++j)
+            if (R0 + j == s) xr[k][j] = f;
+        }
+        // the next pivot column, current through step s: a shared-memory column (its pending
+        // steps, in step order) or a register column (the others receive step s after [B2])
+        if (t1 < R0) {
+          double v = w[t1 * ldS];
+          for (int j = j1; j <= s; ++j)
+            v = __dsub_rn(v, __dmul_rn(w[j * ldS], Pr[j & (kResRing - 1)][t1]));
+          cur[k] = v;
+        } else {
+#pragma unroll
+          for (int j = 0; j < KR; ++j)
+            if (R0 + j == t1) {
+              xr[k][j] = __dsub_rn(xr[k][j], __dmul_rn(f, Pc[t1]));
+              cur[k] = xr[k][j];
+            }
+        }
+      }
+      warp_pick();
+    }
+    if (dbg && threadIdx.x == 32) dbg[s * 8 + 2] = clock64();
+    __syncthreads();  // B2
+    if (dbg && threadIdx.x == 0) dbg[s * 8 + 1] = clock64() + 0 * wc[1].key;
+    if (warp == 0) {
+      publish(s + 1);
+      // the update pass below rewrites shared-memory columns the record was read from
+      asm volatile("bar.arrive 1, %0;\n" ::"r"(kResThreads) : "memory");
+      // this CTA owns pivot s: its LU row (multipliers of steps < s, then the pivot row)
+      if (lu_blk && mine_pivot) {
+        const int olr = static_cast<int>(best.idx - r0);
+        for (int t = lane; t < steps; t += 32)
+          lu_blk[s + t * a.lu_ld] = t >= s ? Pc[t] : (t < R0 ? Ws[olr + t * ldS] : emit[t - R0]);
+      }
+    }
+    if (dbg && threadIdx.x == 0) dbg[s * 8 + 5] = clock64();
+    if (warp > 0) {
+      asm volatile("bar.sync 1, %0;\n" ::"r"(kResThreads) : "memory");
+      if (dbg && threadIdx.x == 32) dbg[s * 8 + 3] = clock64();
+      // step s's term for the register columns after s + 1, and the shared-memory columns
+      // t = s + kResPanel, s + 2 kResPanel, ... brought current through step s (each column is
+      // touched once per kResPanel steps with its pending terms; the work is spread evenly)
+#pragma unroll
+      for (int k = 0; k < kResRPT; ++k) {
+        if (!live[k]) continue;
+        const double f = fk[k];
+#pragma unroll
+        for (int j = 0; j < KR; ++j)
+          if (R0 + j > s + 1) xr[k][j] = __dsub_rn(xr[k][j], __dmul_rn(f, Pc[R0 + j]));
+        if (s + kResPanel >= R0) continue;  // no shared-memory column left to bring current
+        double* w = Ws + lr + k * kResRowThreads;
+        const int j0 = res_last_update(s + kResPanel, s) + 1;  // the same for every column updated now
+        double fp[kResPanel];
+        const double* pj[kResPanel];
+#pragma unroll
+        for (int q = 0; q < kResPanel; ++q) {
+          const int j = j0 + q <= s ? j0 + q : s;
+          fp[q] = w[j * ldS];
+          pj[q] = Pr[j & (kResRing - 1)];
+        }
+        const int nt = s + 1 - j0;  // terms (<= kResPanel)
+        int t = s + kResPanel;
+        for (; t + kResPanel < R0; t += 2 * kResPanel) {  // two columns in flight
+          double v0 = w[t * ldS], v1 = w[(t + kResPanel) * ldS];
+#pragma unroll
+          for (int q = 0; q < kResPanel; ++q)
+            if (q < nt) {
+              v0 = __dsub_rn(v0, __dmul_rn(fp[q], pj[q][t]));
+              v1 = __dsub_rn(v1, __dmul_rn(fp[q], pj[q][t + kResPanel]));
+            }
+          w[t * ldS] = v0;
+          w[(t + kResPanel) * ldS] = v1;
+        }
+        if (t < R0) {
+          double v0 = w[t * ldS];
+#pragma unroll
+          for (int q = 0; q < kResPanel; ++q)
+            if (q < nt) v0 = __dsub_rn(v0, __dmul_rn(fp[q], pj[q][t]));
+          w[t * ldS] = v0;
+        }
+      }
+    }
+    if (dbg && threadIdx.x == 32) dbg[s * 8 + 4] = clock64();
+  }
+  if (g == 0 && threadIdx.x == 0) {
+    *a.d_count = count;
+    if (a.d_width_out) *a.d_width_out = min(count, *a.d_width_cap);
+    // every CTA read the control words before publishing its step-0 record, which this CTA
+    // has seen: the next call may now use the other region
+    res_st(ka.ctl + 1, fresh ? 1ull : callno + 1);
+    res_st(ka.ctl, kResMagic);
+  }
+}
+
+static cudaError_t try_lupp_resident(const LuppArgs& a, void* res_scratch, cudaStream_t st, int* grid_used) {
+  static const bool off = env_flag("ITERCUR_LUPP_NO_RESIDENT");
+  if (off || a.cols_max > kResMaxSteps || a.cols_max < 1 || a.rows < 1 || a.rows >= (1ll << 31) - 1)
+    return cudaErrorNotSupported;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int G = std::min(sms, kResMaxG);
+  const int64_t Rb = ceil_div(a.rows, static_cast<int64_t>(G));
+  if (Rb > kResRPT * kResRowThreads) return cudaErrorNotSupported;
+  G = static_cast<int>(ceil_div(a.rows, Rb));
+  const int R0 = std::max(a.cols_max - kResKR, 0);
+  const size_t smem = sizeof(double) * static_cast<size_t>(R0) * (Rb | 1);
+  constexpr size_t kDynMax = 208 * 1024;
+  if (smem > kDynMax) return cudaErrorNotSupported;
+  const void* fn = reinterpret_cast<const void*>(lupp_resident_kernel<kResKR>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDynMax));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kResThreads, smem);
+  if (per_sm < 1 || per_sm * sms < G) return cudaErrorNotSupported;
+  LuppResArgs ka;
+  ka.a = a;
+  ka.ctl = reinterpret_cast<uint64_t*>(res_scratch);
+  ka.region = ka.ctl + 8;
+  ka.rows_per_cta = static_cast<int>(Rb);
+  ka.dbg = g_lupp_dbg;
+  ka.gdbg = g_lupp_gdbg;
+  static const int backoff = [] {
+    const char* e = getenv("ITERCUR_RES_BACKOFF_NS");
+    return e ? atoi(e) : 0;
+  }();
+  ka.backoff_ns = backoff;
+  void* params[] = {&ka};
+  if (grid_used) *grid_used = -(300000 + G);  // negative: emits the LU factors itself
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kResThreads), params, smem, st);
+}
+
 // Clear in-call ban marks (any value other than 1) when the epoch counter wraps.
 __global__ void clear_epochs_kernel(uint8_t* mask, int64_t count) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
@@ -1710,17 +2268,27 @@ constexpr int kMaxLuppGrid = 1024;
 constexpr size_t kLuppSmemBudget = 200 * 1024;
 
 // scratch: caller-provided device buffer of >= lupp_scratch_bytes(b) bytes
-size_t lupp_scratch_bytes(int b) {
+static size_t lupp_scratch_base_bytes(int b) {
   return sizeof(Cand) * 2 * kMaxLuppGrid + sizeof(double) * kMaxLuppGrid +
          sizeof(double) * 2 * kMaxLuppGrid * static_cast<size_t>(b + 4) + 64;  // + the panel kernel's arrivals
+}
+// the resident kernel's control words and exchange regions first (a fixed offset for every call
+// sharing the buffer), then the other kernels' slots
+size_t lupp_scratch_bytes(int b) { return kResScratchBytes + lupp_scratch_base_bytes(b); }
+// A freshly allocated scratch may hold anything (pool memory reused from other buffers): the
+// resident kernel's control words and regions are set to the sentinel before first use.
+cudaError_t lupp_scratch_init(void* scratch, cudaStream_t st) {
+  return cudaMemsetAsync(scratch, 0xFF, kResScratchBytes, st);
 }
 
 void set_lupp_force_path(int path) { g_force_path = path; }
 void set_lupp_debug_trace(long long* dbg) { g_lupp_dbg = dbg; }
+void set_lupp_grid_trace(long long* gdbg) { g_lupp_gdbg = gdbg; }
 
 cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t st, int* grid_used) {
   if (a.cols_max > 2048) return cudaErrorInvalidValue;
-  char* sp = reinterpret_cast<char*>(scratch);
+  char* const res_scratch = reinterpret_cast<char*>(scratch);
+  char* sp = res_scratch + kResScratchBytes;
   Cand* cand = reinterpret_cast<Cand*>(sp);
   double* norm_part = reinterpret_cast<double*>(sp + sizeof(Cand) * 2 * kMaxLuppGrid);
   // the panel kernel's arrival counter (never cleared: each launch reads its base), then the
@@ -1734,6 +2302,11 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
     if (e != cudaErrorNotSupported) return e;
     e = try_lupp_cluster(a, st, grid_used);
     if (e != cudaErrorNotSupported) return e;
+  }
+  // on-chip resident grid path (slab in registers + shared memory, fence-free exchange)
+  if (g_force_path == 0 || g_force_path == 4) {
+    cudaError_t e = try_lupp_resident(a, res_scratch, st, grid_used);
+    if (e != cudaErrorNotSupported || g_force_path == 4) return e;
   }
   // shared-memory-resident path: one CTA per SM, slab of rows_per_cta x steps doubles
   if (g_force_path == 0 || g_force_path == 2) {

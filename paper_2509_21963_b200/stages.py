@@ -107,7 +107,8 @@ def time_sketch_kernel(a: torch.Tensor, b: int, kind: str = "gaussian", reps: in
 
 
 def time_lupp(rows: int, steps: int, reps: int = 10, force_path: int = 0):
-    """Mean microseconds per LUPP launch on a random rows x steps W (0 auto, 1 cluster, 2 grid, 3 global)."""
+    """Mean microseconds per LUPP launch on a random rows x steps W (0 auto, 1 cluster, 2 grid, 3 global,
+    4 resident)."""
     us = C.c_double()
     used = C.c_int32()
     _check(_capi.lib().itercur_time_lupp(int(rows), int(steps), int(reps), int(force_path),

@@ -187,6 +187,33 @@ def test_lupp_bit_exact_vs_oracle(engine, oracle, rows, cols, b, is_columns):
     assert got.truncated == want.truncated
 
 
+@pytest.mark.parametrize("rows,steps", [(100000, 50), (50000, 64), (60000, 12), (104000, 40)])
+def test_lupp_resident_bit_exact_vs_oracle(engine, oracle, rows, steps):
+    """The on-chip resident grid LUPP (config-4 slab: 100000 x 50 over 148 SMs; all-register
+    slabs at <= 16 steps; the widest slab it takes) selects the oracle's pivots bit for bit."""
+    S = _stages()
+    m = oracle.random_gaussian(rows, steps, rows + 3 * steps)
+    ex = [0, 5, rows // 2, rows - 1]
+    got = S.select_rows(S.colmajor(m), steps, exclude=ex)
+    want = oracle.select_rows(m, steps, exclude=ex)
+    assert got.indices == want.indices
+    assert got.best == want.best
+    assert got.truncated == want.truncated
+
+
+def test_lupp_resident_ties_across_ctas(engine, oracle):
+    """Exact ties between rows owned by different CTAs: the lowest row index wins, as in the
+    reference's ascending scan (select.cpp:40-48)."""
+    S = _stages()
+    rows, steps = 90000, 30
+    base = oracle.random_gaussian(rows // 6, steps, 901)
+    m = np.asfortranarray(np.vstack([base] * 6))  # every row repeated 6 times, 15000 rows apart
+    got = S.select_rows(S.colmajor(m), steps)
+    want = oracle.select_rows(m, steps)
+    assert got.indices == want.indices
+    assert got.best == want.best
+
+
 def test_lupp_reference_cases(engine, oracle):
     """proj/tests/test_select.cpp cases on the device."""
     S = _stages()

@@ -1,6 +1,6 @@
 """One stage kernel timed alone (CUDA events), for quick checks and ncu captures:
 
-    python tools/time_stage.py lupp ROWS STEPS [PATH] [REPS]   # PATH 0 auto, 1 cluster, 2 grid smem, 3 panel/global
+    python tools/time_stage.py lupp ROWS STEPS [PATH] [REPS]   # PATH 0 auto, 1 cluster, 2 grid smem, 3 panel/global, 4 resident
     python tools/time_stage.py gemm M N K [REPS]                # row-residual shape C = A(:,idx) - L B
     python tools/time_stage.py sketch M N B KIND [REPS]         # KIND gaussian | sparse_sign, random A
     python tools/time_stage.py h2d [GB]                         # host->device copy rate, pageable vs pinned
