@@ -2572,16 +2572,16 @@ int itercur_time_lupp(int64_t rows, int32_t steps, int32_t reps, int32_t force_p
       std::vector<long long> h(static_cast<size_t>(steps) * 16);
       CK(cudaMemcpyAsync(h.data(), tr.p, sizeof(long long) * steps * 16, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      if (used <= -300000) {  // resident kernel, per step s: [0] t0 after B1, [1] t0 after B2, [2] t32 pick done,
-        // [3] t32 after the publish barrier, [4] t32 update done, [5] t0 published, [6] headers, [7] tail
+      if (used <= -300000) {  // resident kernel, per step s (thread 0 unless noted): [0] after B1, [1] after B2,
+        // [2] CTA argmax, [3] record row stored, [4] lane 1 reciprocal stored, [5] published, [6] headers, [7] tail
         for (int q = 0; q + 1 < steps; ++q) {
           const long long* v = h.data() + q * 8;
           const long long* w = v + 8;
           fprintf(stderr,
-                  "lupp resident step %d: [t0] B1->B2 %lld publish %lld headers %lld tail %lld B1 %lld | [t32] B1->picked "
-                  "%lld ->bar1 %lld update %lld | step %lld\n",
-                  q, v[1] - v[0], v[5] - v[1], w[6] - v[5], w[7] - w[6], w[0] - w[7], v[2] - v[0], v[3] - v[2],
-                  v[4] - v[3], w[0] - v[0]);
+                  "lupp resident step %d: B1->B2 %lld argmax %lld row %lld (rcp %lld) pub-end %lld headers %lld tail %lld "
+                  "->B1 %lld | step %lld\n",
+                  q, v[1] - v[0], v[2] - v[1], v[3] - v[2], v[4] - v[2], v[5] - v[3], w[6] - v[5], w[7] - w[6],
+                  w[0] - w[7], w[0] - v[0]);
         }
       } else if (used <= -200000) {  // panel kernel (8 slots per step)
         for (int q = 0; q + 1 < steps; ++q) {

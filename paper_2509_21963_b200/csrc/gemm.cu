@@ -841,10 +841,13 @@ static bool lean_ok(const TsGemmParams& p) {
 
 template <int NT>
 static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
-  // 0 off, 1: KT16 x4, 2: KT32 x3, 3: KT32 x4; default by shape (tools/bench_gemm.py on B200:
-  // the lean loop wins for N <= 32, KT32 x3 for the taller M, the generic loop for wide N)
+  // 0 off, 1: KT16 x4, 2: KT32 x3, 3: KT32 x4, 4: KT16 x3, 5: KT32 x2; default by shape
+  // (tools/time_stage.py gemm sweeps on B200: the lean loop wins for N <= 32 (KT32 x3 for the
+  // taller M); for 33..72-wide blocks KT16 x3 / KT32 x2 beat the generic loop by 25-35%, e.g.
+  // 100000 x 50 x 256: 130 vs 201 us, 200000 x 64 x 1024: 958 vs 1193 us)
   static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
-  const int lean = forced >= 0 ? forced : (NT > 4 ? 0 : (p.M >= 16000 ? 2 : 1));
+  const int64_t kp = p.k_plan > 0 ? p.k_plan : p.K;
+  const int lean = forced >= 0 ? forced : (NT > 4 ? (kp >= 512 ? 5 : 4) : (p.M >= 16000 ? 2 : 1));
   if (lean > 0 && lean_ok(p) && gemm_warps(p.M) == 4) {
     switch (lean) {
       case 1: return launch_lean<NT, 4, 16, 4>(p, st);

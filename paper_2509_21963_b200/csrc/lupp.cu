@@ -740,8 +740,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) lupp_cluster_kernel(LuppCl
       __syncwarp();
       if (dbg && threadIdx.x == 32) dbg[s * 8 + 1] = clock64();
       warp_candidate(mine, s + 1, true, P);
-      if (dbg && threadIdx.x == 32) dbg[s * 8 + 2] = clock64();
-    }
+      }
     __syncthreads();
     if (warp == 0) {
       if (dbg && threadIdx.x == 0) dbg[s * 8 + 3] = clock64();
@@ -1715,7 +1714,10 @@ constexpr int kResPanel = 4;              // shared-memory columns updated once 
 constexpr int kResRing = 8;  // pivot rows kept (>= kResPanel + 1; a power of two: slot = step & 7)
 constexpr int kResMaxG = 148;
 constexpr int kResRec = 4 + kResMaxSteps;  // header (key, row, runner-up key, 0) + row tail
-constexpr size_t kResRegionWords = kResMaxG + static_cast<size_t>(kResMaxSteps) * kResMaxG * kResRec;
+// region: norm partials [kResMaxG], compact headers [step][CTA][2] (a warp's poll touches 4 lines),
+// records [step][CTA][kResRec] (word 2 runner-up key, 3 RN(1/pivot), 4 + t the row)
+constexpr size_t kResHdrWords = static_cast<size_t>(kResMaxSteps) * kResMaxG * 2;
+constexpr size_t kResRegionWords = kResMaxG + kResHdrWords + static_cast<size_t>(kResMaxSteps) * kResMaxG * kResRec;
 constexpr uint64_t kResEmpty = ~0ull;
 constexpr uint64_t kResMagic = 0x1C0B200A5A5E0002ull;
 constexpr size_t kResScratchBytes = 64 + 2 * kResRegionWords * sizeof(uint64_t);
@@ -1824,7 +1826,10 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
   }
   clear_region(ka.region + static_cast<size_t>(par ^ 1) * kResRegionWords);
   uint64_t* const norms = reg;
-  auto rec = [&](int s, int q) { return reg + kResMaxG + (static_cast<size_t>(s) * kResMaxG + q) * kResRec; };
+  auto hdr = [&](int s, int q) { return reg + kResMaxG + (static_cast<size_t>(s) * kResMaxG + q) * 2; };
+  auto rec = [&](int s, int q) {
+    return reg + kResMaxG + kResHdrWords + (static_cast<size_t>(s) * kResMaxG + q) * kResRec;
+  };
 
   // ---- load: row thread lr owns local rows lr + k * kResRowThreads (k < kResRPT) ----
   double xr[kResRPT][KR];
@@ -1894,7 +1899,7 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
       uint64_t k[QN], ix[QN];
 #pragma unroll
       for (int u = 0; u < QN; ++u)
-        if (pending >> u & 1) res_ld2(rec(s, lane + 32 * u), k[u], ix[u]);
+        if (pending >> u & 1) res_ld2(hdr(s, lane + 32 * u), k[u], ix[u]);
 #pragma unroll
       for (int u = 0; u < QN; ++u)
         if ((pending >> u & 1) && k[u] != kResEmpty && ix[u] != kResEmpty) {
@@ -1974,11 +1979,12 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
   auto publish = [&](int sp) {
     const WCand c = lane < kResWarps ? wc[lane] : WCand{0ull, 0x7fffffff, -1.0};
     const WCand cb = warp_argmax(c);
+    if (dbg && lane == 0 && sp > 0) dbg[(sp - 1) * 8 + 2] = clock64() + (cb.key & 0);
     uint64_t* r = rec(sp, g);
     if (cb.key) {
       const int olr = static_cast<int>(cb.idx - r0), w = (olr % kResRowThreads) / 32 + 1;
       const double* orow = Ws + olr;
-      if (lane == 0) res_st2(r, cb.key, static_cast<uint64_t>(cb.idx));
+      if (lane == 0) res_st2(hdr(sp, g), cb.key, static_cast<uint64_t>(cb.idx));
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int t = sp + lane + 32 * h;
@@ -1996,11 +2002,13 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
         }
         res_st(r + 4 + t, res_enc(v));
       }
+      if (dbg && lane == 0 && sp > 0) dbg[(sp - 1) * 8 + 3] = clock64();
       if (lane == 1)
         res_st2(r + 2, cb.second >= 0.0 ? mag_key(cb.second) : 0ull,
                 static_cast<uint64_t>(__double_as_longlong(__drcp_rn(stage[w][KR + 1]))));
+      if (dbg && lane == 1 && sp > 0) dbg[(sp - 1) * 8 + 4] = clock64();
     } else if (lane == 0) {
-      res_st2(r, 0ull, 0ull);
+      res_st2(hdr(sp, g), 0ull, 0ull);
       res_st2(r + 2, 0ull, 0ull);
     }
 #ifdef ITERCUR_RES_TRACE
@@ -2125,7 +2133,6 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
       }
       warp_pick();
     }
-    if (dbg && threadIdx.x == 32) dbg[s * 8 + 2] = clock64();
     __syncthreads();  // B2
     if (dbg && threadIdx.x == 0) dbg[s * 8 + 1] = clock64() + 0 * wc[1].key;
     if (warp == 0) {
@@ -2142,7 +2149,6 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
     if (dbg && threadIdx.x == 0) dbg[s * 8 + 5] = clock64();
     if (warp > 0) {
       asm volatile("bar.sync 1, %0;\n" ::"r"(kResThreads) : "memory");
-      if (dbg && threadIdx.x == 32) dbg[s * 8 + 3] = clock64();
       // step s's term for the register columns after s + 1, and the shared-memory columns
       // t = s + kResPanel, s + 2 kResPanel, ... brought current through step s (each column is
       // touched once per kResPanel steps with its pending terms; the work is spread evenly)
@@ -2186,7 +2192,6 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
         }
       }
     }
-    if (dbg && threadIdx.x == 32) dbg[s * 8 + 4] = clock64();
   }
   if (g == 0 && threadIdx.x == 0) {
     *a.d_count = count;
