@@ -381,7 +381,7 @@ static int apply_sketch(const double* A, int64_t m, int64_t n, int64_t lda, int 
 }
 
 struct Workspace {
-  DevBuf<double> Y, Wc, Wr, Bg, Ut, Yg, lu, part, sk_ws, S;
+  DevBuf<double> Y, Wc, Wr, Bg, Ut, Yg, YgT, lu, part, sk_ws, S;
   DevBuf<uint8_t> col_mask, row_mask;
   DevBuf<char> state, lupp_scratch, qrcp_scratch;
   DevBuf<double> Wq;  // Y copy for the QRCP column selection (qrcp_pivot_cols takes W by value)
@@ -589,6 +589,7 @@ void run_iterative_cur(itercur_run* run) {
   ws.Wr.alloc(static_cast<size_t>(ldm) * B);
   ws.Ut.alloc(static_cast<size_t>(ldn) * B);
   ws.Yg.alloc(static_cast<size_t>(B) * cp);
+  ws.YgT.alloc(static_cast<size_t>(even(B)) * cp);  // Y(:, J_k)^T for the unfused downdate (k-contiguous)
   ws.col_mask.alloc(n_glob);
   ws.row_mask.alloc(m);
   CK(cudaMemsetAsync(ws.col_mask.p, 0, n_glob, st));
@@ -1155,8 +1156,12 @@ void run_iterative_cur(itercur_run* run) {
 
         // (5) downdate Y -= Y(:,J_k) * Rt_k in place (downdate_col_residual, sketch.cpp:26-41),
         //     ||Y||^2 fused, Wc = Y^T(:, 0:b) for the next column selection
-        if (!sh.active)
-          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.Yg.p, cp, st, d_ctl, false));
+        // Y(:, J_k) gathered transposed (w x cp, k-contiguous): the downdate then runs the lean
+        // cp.async loop instead of the generic loader (config 4: 118 -> ~60 us per iteration)
+        const int64_t ldq = even(B);
+        if (!sh.active) {
+          CK(launch_gather(ws.Y.p, 1, cp, cp, arr.col_idx, &slot->width, B, ws.YgT.p, ldq, st, d_ctl, false, true));
+        }
         for (int sI = 0; sI < nloc; ++sI) {
           const int64_t lo = loc(sI);
           TsGemmParams p;
@@ -1168,9 +1173,15 @@ void run_iterative_cur(itercur_run* run) {
           p.A = run->Rt.p + lo;
           p.a_off_per_r = run->ldR;
           p.lda = run->ldR;
-          p.B = sh.active ? packY() : ws.Yg.p;  // B(q, h) = Y(h, J[q]) = Yg[h + q * cp]
-          p.bsk = cp;
-          p.bsn = 1;
+          if (sh.active) {
+            p.B = packY();  // B(q, h) = Y(h, J[q]) = PackY[h + q * cp]
+            p.bsk = cp;
+            p.bsn = 1;
+          } else {
+            p.B = ws.YgT.p;  // B(q, h) = Y(h, J[q]) = YgT[q + h * ldq]
+            p.bsk = 1;
+            p.bsn = ldq;
+          }
           p.base_mode = kBaseInPlaceRowMajor;
           p.alpha = -1.0;
           p.out_mode = kOutRowMajor;

@@ -61,7 +61,8 @@ cudaError_t launch_transpose(const double* A, int64_t m, int64_t n, int64_t lda,
 // out(k, q) = src[k * row_stride + idx[q] * col_stride] for k < K, q < w (dynamic), zero for q >= w
 __global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride, int64_t col_stride, int64_t Kmax,
                               const int64_t* __restrict__ idx, const int* __restrict__ d_w, int w_max,
-                              double* __restrict__ out, int64_t ldo, const IterCtl* __restrict__ ctl, int k_from_r) {
+                              double* __restrict__ out, int64_t ldo, const IterCtl* __restrict__ ctl, int k_from_r,
+                              int transposed) {
   griddep_wait();
   griddep_launch_dependents();
   if (ctl && ctl->done) return;
@@ -70,7 +71,11 @@ __global__ void gather_kernel(const double* __restrict__ src, int64_t row_stride
   const int64_t total = K * w_max;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = e / K, k = e - q * K;
-    out[k + q * ldo] = q < w ? src[k * row_stride + idx[q] * col_stride] : 0.0;
+    const double v = q < w ? src[k * row_stride + idx[q] * col_stride] : 0.0;
+    if (transposed)
+      out[q + k * ldo] = v;  // index-list dimension contiguous (a k-contiguous GEMM B operand)
+    else
+      out[k + q * ldo] = v;
   }
 }
 
@@ -85,12 +90,12 @@ cudaError_t launch_transpose_rows(const double* Y, int64_t cp, int64_t n, int ro
 
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
                           const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st, const IterCtl* ctl,
-                          bool k_from_r) {
+                          bool k_from_r, bool transposed) {
   const int64_t total = K * w_max;
   if (total <= 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
   return launch_ex(gather_kernel, dim3(blocks), dim3(256), 0, st, dim3(0, 0, 0), src, row_stride, col_stride, K, d_idx,
-                   d_w, w_max, out, ldo, ctl, k_from_r ? 1 : 0);
+                   d_w, w_max, out, ldo, ctl, k_from_r ? 1 : 0, transposed ? 1 : 0);
 }
 
 // Two gathers of the same (dynamic) width in one launch: the U block's operands L(I_k, :)^T and

@@ -138,7 +138,7 @@ cudaError_t launch_gather_pair(const double* src0, int64_t rs0, int64_t cs0, int
                                bool k_from_r1, const int* d_w, int w_max, cudaStream_t st, const IterCtl* ctl);
 cudaError_t launch_gather(const double* src, int64_t row_stride, int64_t col_stride, int64_t K, const int64_t* d_idx,
                           const int* d_w, int w_max, double* out, int64_t ldo, cudaStream_t st,
-                          const IterCtl* ctl = nullptr, bool k_from_r = false);
+                          const IterCtl* ctl = nullptr, bool k_from_r = false, bool transposed = false);
 // out(k, q) = src[idx[k] + q * ld] for k < K, q < w (row-indexed gather)
 cudaError_t launch_gather2(const double* src, int64_t ld, const int64_t* d_idx, int64_t K, int w, double* out,
                            int64_t ldo, cudaStream_t st);
