@@ -2102,6 +2102,27 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
       const double pivot = Pc[s], ys = s_y;
       const bool p_ok = pivot_in_range(pivot);
       const int t1 = s + 1, j1 = res_last_update(t1, s) + 1;  // column t1's pending steps j1..s
+      // the next pivot column's pending terms before step s do not need f: formed first, beside
+      // the division (at most kResPanel - 1 of them, loads issued together)
+      double vpart[kResRPT];
+#pragma unroll
+      for (int k = 0; k < kResRPT; ++k) {
+        vpart[k] = 0.0;
+        if (!live[k] || t1 >= R0) continue;
+        const double* w = Ws + lr + k * kResRowThreads;
+        double m[kResPanel - 1], pv[kResPanel - 1];
+#pragma unroll
+        for (int q = 0; q < kResPanel - 1; ++q) {
+          const int j = j1 + q < s ? j1 + q : s;
+          m[q] = w[j * ldS];
+          pv[q] = Pr[j & (kResRing - 1)][t1];
+        }
+        double v = w[t1 * ldS];
+#pragma unroll
+        for (int q = 0; q < kResPanel - 1; ++q)
+          if (j1 + q < s) v = __dsub_rn(v, __dmul_rn(m[q], pv[q]));
+        vpart[k] = v;
+      }
 #pragma unroll
       for (int k = 0; k < kResRPT; ++k) {
         if (!live[k]) continue;
@@ -2118,10 +2139,7 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
         // the next pivot column, current through step s: a shared-memory column (its pending
         // steps, in step order) or a register column (the others receive step s after [B2])
         if (t1 < R0) {
-          double v = w[t1 * ldS];
-          for (int j = j1; j <= s; ++j)
-            v = __dsub_rn(v, __dmul_rn(w[j * ldS], Pr[j & (kResRing - 1)][t1]));
-          cur[k] = v;
+          cur[k] = __dsub_rn(vpart[k], __dmul_rn(f, Pc[t1]));
         } else {
 #pragma unroll
           for (int j = 0; j < KR; ++j)

@@ -470,7 +470,133 @@ __global__ void __launch_bounds__(128) rows_lu_solve_smem_kernel(const double* _
   }
 }
 
-// Blocked form (default for 16 < w <= 64): the row in shared memory in chunks of 8 entries, the
+// Tensor-core form (default for 16 < w <= 64): R~_k rows = the rows of U_k^T solved against
+// D_k = Lhat Uhat, as a blocked triangular solve on DMMA. A warp owns 16 rows as the C fragments
+// of ceil(w/8) column chunks; chunk P is first updated by every finished chunk Q with one
+// m16n8k8 per (P, Q) pair — the finished chunk's C fragment is the A operand as it stands (the
+// k permutation logical t <-> column 2t, t+4 <-> 2t+1 of the GEMMs), B = -L(P, Q)^T staged in
+// shared memory — then solved within its 8 x 8 diagonal block by substitution on the fragment
+// (the row's 8 entries live in a quad: x_p broadcast with shuffles). Division by U's diagonal
+// through its correctly rounded reciprocal (Markstein; IEEE division for the warp outside the
+// safe exponent window), i.e. the IEEE quotient. Backward-stable like the row substitutions it
+// replaces (no explicit inverse: D_k's condition number reaches 1e9+ near the noise floor).
+template <int NT>
+__global__ void __launch_bounds__(128) rows_lu_solve_mma_kernel(const double* __restrict__ X, int64_t ldx, int64_t M,
+                                                                const double* __restrict__ lu, int64_t ldd,
+                                                                const int* __restrict__ d_w, int w_max,
+                                                                double* __restrict__ out, int64_t ldo,
+                                                                const IterCtl* __restrict__ ctl, int64_t out_off_per_r,
+                                                                const int* __restrict__ perm) {
+  constexpr int W = NT * 8, WP = W + 4;  // negated factors, row pitch WP (16-byte fragment loads)
+  __shared__ __align__(16) double sneg[W * WP];  // sneg[q * WP + p] = -LU(q, p), identity-padded
+  __shared__ double srcp[W];                     // RN(1 / U(p, p))
+  __shared__ int sperm[W];
+  griddep_wait();
+  griddep_launch_dependents();
+  if (ctl) {
+    if (ctl->done) return;
+    lu += ctl->r * ldd;
+    out += ctl->r * out_off_per_r;
+    if (perm) perm += ctl->r;
+  }
+  const int w = d_w ? min(*d_w, w_max) : w_max;
+  for (int e = threadIdx.x; e < W * W; e += 128) {
+    const int q = e % W, p = e / W;
+    const double v = (q < w && p < w) ? lu[q + p * ldd] : (q == p ? 1.0 : 0.0);
+    sneg[q * WP + p] = -v;
+  }
+  for (int p = threadIdx.x; p < W; p += 128) {
+    srcp[p] = p < w ? __drcp_rn(lu[p + p * ldd]) : 1.0;
+    sperm[p] = (perm && p < w) ? perm[p] : p;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3, qbase = lane & ~3;
+  auto out_of_range = [](double v) {  // zero, or biased exponent inside [56, 1990]
+    const unsigned hi = static_cast<unsigned>(__double_as_longlong(v) >> 32) & 0x7fffffffu;
+    const unsigned e = hi >> 20;
+    return static_cast<unsigned>((e - 56u) > (1990u - 56u)) & static_cast<unsigned>(v != 0.0);
+  };
+  for (int64_t tile = blockIdx.x; tile * 64 < M; tile += gridDim.x) {
+    const int64_t r0 = tile * 64 + warp * 16 + g;  // rows r0, r0 + 8
+    double x[NT][4];  // x[P][v0 + 2 v1] = X(r0 + 8 v1, 8P + 2t + v0)
+#pragma unroll
+    for (int P = 0; P < NT; ++P)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int q = 8 * P + 2 * t + (v & 1);
+        const int64_t j = r0 + 8 * (v >> 1);
+        x[P][v] = (q < w && j < M) ? X[j + sperm[q] * ldx] : 0.0;
+      }
+    // forward: Lhat y = u (unit lower)
+#pragma unroll
+    for (int P = 0; P < NT; ++P) {
+#pragma unroll
+      for (int Q = 0; Q < P; ++Q) {
+        const double2 b = *reinterpret_cast<const double2*>(sneg + (8 * P + g) * WP + 8 * Q + 2 * t);
+        dmma_16x8x8(x[P], x[Q][0], x[Q][2], x[Q][1], x[Q][3], b.x, b.y);
+      }
+#pragma unroll
+      for (int pp = 0; pp < 7; ++pp) {
+        const double y0 = __shfl_sync(0xffffffffu, x[P][pp & 1], qbase | (pp >> 1));
+        const double y1 = __shfl_sync(0xffffffffu, x[P][2 + (pp & 1)], qbase | (pp >> 1));
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq)
+          if (2 * t + dq > pp) {
+            const double l = sneg[(8 * P + 2 * t + dq) * WP + 8 * P + pp];
+            x[P][dq] = fma(l, y0, x[P][dq]);
+            x[P][2 + dq] = fma(l, y1, x[P][2 + dq]);
+          }
+      }
+    }
+    // back: Uhat x = y
+#pragma unroll
+    for (int P = NT - 1; P >= 0; --P) {
+#pragma unroll
+      for (int Q = NT - 1; Q > P; --Q) {
+        const double2 b = *reinterpret_cast<const double2*>(sneg + (8 * P + g) * WP + 8 * Q + 2 * t);
+        dmma_16x8x8(x[P], x[Q][0], x[Q][2], x[Q][1], x[Q][3], b.x, b.y);
+      }
+#pragma unroll
+      for (int pp = 7; pp >= 0; --pp) {
+        const int p = 8 * P + pp;
+        const double upp = -sneg[p * WP + p], yr = srcp[p];
+        const double a0 = __shfl_sync(0xffffffffu, x[P][pp & 1], qbase | (pp >> 1));
+        const double a1 = __shfl_sync(0xffffffffu, x[P][2 + (pp & 1)], qbase | (pp >> 1));
+        double x0 = __dmul_rn(a0, yr), x1 = __dmul_rn(a1, yr);
+        x0 = __fma_rn(__fma_rn(-x0, upp, a0), yr, x0);
+        x1 = __fma_rn(__fma_rn(-x1, upp, a1), yr, x1);
+        const unsigned bad = out_of_range(a0) | out_of_range(a1) | out_of_range(x0) | out_of_range(x1) |
+                             static_cast<unsigned>(!pivot_in_range(upp));
+        if (__any_sync(0xffffffffu, bad)) {
+          x0 = ieee_div(a0, upp);
+          x1 = ieee_div(a1, upp);
+        }
+        if (t == (pp >> 1)) {
+          x[P][pp & 1] = x0;
+          x[P][2 + (pp & 1)] = x1;
+        }
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq)
+          if (2 * t + dq < pp) {
+            const double u = sneg[(8 * P + 2 * t + dq) * WP + p];
+            x[P][dq] = fma(u, x0, x[P][dq]);
+            x[P][2 + dq] = fma(u, x1, x[P][2 + dq]);
+          }
+      }
+    }
+#pragma unroll
+    for (int P = 0; P < NT; ++P)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int q = 8 * P + 2 * t + (v & 1);
+        const int64_t j = r0 + 8 * (v >> 1);
+        if (q < w && j < M) out[j + q * ldo] = x[P][v];
+      }
+  }
+}
+
+// Blocked form (A/B: ITERCUR_ROWS_SOLVE_BLK=1): the row in shared memory in chunks of 8 entries, the
 // factors zero-padded to 64 x 64. Each chunk of 8 unknowns is updated by every earlier (forward) /
 // later (back) chunk with an unrolled 8 x 8 block of FMAs on registers — eight shared-memory reads
 // of x per 64 FMAs instead of one per FMA (the per-FMA form above is bound by shared-memory
@@ -611,7 +737,24 @@ cudaError_t launch_rows_lu_solve(const double* X, int64_t ldx, int64_t M, const 
     return launch_ex(rows_lu_solve_kernel<16>, dim3(blocks), dim3(128), smem, st, dim3(0, 0, 0), X, ldx, M, lu, ldd, d_w,
                      w_max, out, ldo, ctl, out_off_per_r, perm);
   } else if (w_max <= 64 && !env_flag("ITERCUR_ROWS_SOLVE_ROWFORM") && !env_flag("ITERCUR_ROWS_SOLVE_COLFORM") &&
-             !env_flag("ITERCUR_ROWS_SOLVE_SMEM")) {
+             !env_flag("ITERCUR_ROWS_SOLVE_SMEM") && !env_flag("ITERCUR_ROWS_SOLVE_BLK")) {
+    // tensor-core blocked solve: 64 rows per CTA, persistent over the row tiles
+    const int tiles = static_cast<int>(std::min<int64_t>(ceil_div(M, 64), 148 * 8));
+    switch ((w_max + 7) / 8) {
+      case 3: return launch_ex(rows_lu_solve_mma_kernel<3>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M, lu,
+                               ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+      case 4: return launch_ex(rows_lu_solve_mma_kernel<4>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M, lu,
+                               ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+      case 5: return launch_ex(rows_lu_solve_mma_kernel<5>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M, lu,
+                               ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+      case 6: return launch_ex(rows_lu_solve_mma_kernel<6>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M, lu,
+                               ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+      case 7: return launch_ex(rows_lu_solve_mma_kernel<7>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M, lu,
+                               ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+      default: return launch_ex(rows_lu_solve_mma_kernel<8>, dim3(tiles), dim3(128), 0, st, dim3(0, 0, 0), X, ldx, M,
+                                lu, ldd, d_w, w_max, out, ldo, ctl, out_off_per_r, perm);
+    }
+  } else if (w_max <= 64 && env_flag("ITERCUR_ROWS_SOLVE_BLK")) {  // A/B: blocked rows in shared memory
     // blocked, rows in shared memory (default; A/B switches below)
     const size_t smem2 = sizeof(double) * (64 * 64 + 64 * 128);
     static bool attr = false;

@@ -123,3 +123,14 @@ def time_gemm(M: int, N: int, K: int, reps: int = 10) -> float:
     _check(_capi.lib().itercur_time_gemm(int(M), int(N), int(K), int(reps),
                                          C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(us)))
     return us.value
+
+
+def rows_lu_solve(x: torch.Tensor, lu: torch.Tensor) -> torch.Tensor:
+    """out(j, :) = D^{-1} x_j for every row j of x (M x w, column-major CUDA), D = Lhat Uhat packed
+    in lu (w x w, unit-lower Lhat below the diagonal, Uhat on and above)."""
+    M, w = x.shape
+    out = torch.zeros(w, M, dtype=torch.float64, device=x.device).t()
+    _check(_capi.lib().itercur_rows_lu_solve_device(C.c_void_p(x.data_ptr()), _colmajor_ld(x), M,
+                                                    C.c_void_p(lu.data_ptr()), _colmajor_ld(lu), w,
+                                                    C.c_void_p(out.data_ptr()), _colmajor_ld(out), _stream(x)))
+    return out

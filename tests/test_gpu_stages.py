@@ -288,3 +288,22 @@ def test_gaussian_sketch_bitwise_deterministic_at_config3_shape(engine, oracle):
     assert np.allclose(y0[:, :64].cpu().numpy(), y_or, rtol=1e-12, atol=1e-12 * np.abs(y_or).max())
     del a
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("M,w", [(1000, 17), (12345, 24), (777, 33), (20000, 50), (4096, 64), (65, 40)])
+def test_rows_lu_solve_matches_dense_solve(engine, monkeypatch, M, w):
+    """The tensor-core blocked row solve (default for 16 < w <= 64) and the scalar blocked form
+    (ITERCUR_ROWS_SOLVE_BLK=1) both equal D^{-1} x_j to solve accuracy, D = Lhat Uhat."""
+    S = _stages()
+    rng = np.random.default_rng(M + w)
+    L = np.tril(rng.standard_normal((w, w)) * 0.3, -1) + np.eye(w)
+    U = np.triu(rng.standard_normal((w, w)) * 0.3, 1) + np.diag(rng.uniform(0.5, 2.0, w) * rng.choice([-1, 1], w))
+    lu = np.tril(L, -1) + U
+    X = rng.standard_normal((M, w))
+    want = np.linalg.solve(L @ U, X.T).T
+    outs = []
+    for blk in ("0", "1"):
+        monkeypatch.setenv("ITERCUR_ROWS_SOLVE_BLK", blk) if blk == "1" else monkeypatch.delenv("ITERCUR_ROWS_SOLVE_BLK", raising=False)
+        got = S.rows_lu_solve(S.colmajor(X), S.colmajor(lu)).cpu().numpy()
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want), (blk, np.linalg.norm(got - want))
+        outs.append(got)
