@@ -157,7 +157,20 @@ __device__ __forceinline__ void gemm_load_base(const TsGemmParams& p, double (&b
       }
 }
 
-template <int NT, int WARPS, bool UB = false>
+// base values staged in shared memory by cp.async (BSM) instead of registers: the wide blocks'
+// 4 NT base registers per thread would otherwise stay allocated through the whole kernel
+template <int NT>
+__device__ __forceinline__ const void* gemm_base_addr(const TsGemmParams& p, int64_t i, int64_t q) {
+  switch (p.base_mode) {
+    case kBaseGatherCols: return p.src + i + p.idx[q] * p.lds;
+    case kBaseGatherRowsT: return p.src + p.idx[q] + i * p.lds;
+    case kBaseContigCols: return p.src + i + (p.col0 + q) * p.lds;
+    case kBaseInPlaceRowMajor: return p.C0 + i * p.ldc0 + q;
+    default: return nullptr;
+  }
+}
+
+template <int NT, int WARPS, bool UB = false, bool BSM = false>
 __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&acc)[NT][4], double (&bv)[NT][4],
                                               double* gsm, int64_t i0, int64_t q0, int nvalid, int splits) {
   constexpr int THREADS = WARPS * 32;
@@ -172,7 +185,32 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
   // base values, and for the U block the Y^T rows to downdate and D_k's factors / Y(:,J_k)
   const bool finisher = blockIdx.z == 0;
   double yv[NTY][4];
-  if (!p.early_base) gemm_load_base<NT>(p, bv, r0, q0, nvalid);
+  double* sbase = gsm + NT * 4 * THREADS;  // BSM: [nt * 4 + v][THREADS], past the split-K buffer
+  if constexpr (BSM) {
+    __syncthreads();  // the ring's last stage may still be read by other warps
+    if (finisher) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq)
+#pragma unroll
+          for (int dr = 0; dr < 2; ++dr) {
+            const int ql = nt * 8 + 2 * t + dq;
+            const int64_t i = r0 + dr;
+            const bool in = ql < nvalid && i < p.M && p.base_mode != kBaseNone && p.base_mode != kBaseIdentityCols;
+            const void* src = in ? gemm_base_addr<NT>(p, i, q0 + ql) : nullptr;
+            double* dst = sbase + (nt * 4 + dr * 2 + dq) * THREADS + threadIdx.x;
+            if (src)
+              cp_async_8(dst, src, 8);
+            else
+              *dst = (in || p.base_mode != kBaseIdentityCols) ? 0.0 : 0.0;
+            if (p.base_mode == kBaseIdentityCols) *dst = (ql < nvalid && i < p.M && i == p.col0 + q0 + ql) ? 1.0 : 0.0;
+          }
+      cp_async_commit();
+    }
+  } else if (!p.early_base) {
+    gemm_load_base<NT>(p, bv, r0, q0, nvalid);
+  }
   double* s_lu = gsm + NT * 4 * THREADS;  // past the split-K exchange buffer
   double* s_yg = s_lu + W * W + W;  // (W reciprocals behind the LU block)
   if constexpr (UB) {
@@ -254,6 +292,7 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
   }
 
   ub_stamp(p, 2);
+  if constexpr (BSM) cp_async_wait<0>();  // this thread's own base slots
   // ---------------- epilogue: physical rows (2g, 2g+1), columns (2t, 2t+1) ----------
   double sq = 0.0;
 #pragma unroll
@@ -267,7 +306,8 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
       for (int dr = 0; dr < 2; ++dr) {
         const int64_t i = r0 + dr;
         if (i >= p.M) continue;
-        const double v = bv[nt][dr * 2 + dq] + p.alpha * acc[nt][dr * 2 + dq];
+        const double base = BSM ? sbase[(nt * 4 + dr * 2 + dq) * THREADS + threadIdx.x] : bv[nt][dr * 2 + dq];
+        const double v = base + p.alpha * acc[nt][dr * 2 + dq];
         sq = fma(v, v, sq);
         if (p.out_mode == kOutColMajor) {
           p.C0[i + q * p.ldc0] = v;
@@ -654,7 +694,7 @@ struct LeanCfg {
   static_assert(THREADS * NT * 4 <= STAGES * STAGE_ELEMS, "split-K reduction buffer must fit the ring");
 };
 
-template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
+template <int NT, int WARPS, int KT, int STAGES, bool UB = false, bool BSM = false>
 __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p) {
   using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
   extern __shared__ __align__(16) double gsm[];
@@ -739,7 +779,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
     for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
 
   double bv[NT][4];
-  if (p.early_base) gemm_load_base<NT>(p, bv, i0 + warp * 16 + 2 * g, q0, nvalid);
+  if (!BSM && p.early_base) gemm_load_base<NT>(p, bv, i0 + warp * 16 + 2 * g, q0, nvalid);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load(s, kb + s);
@@ -767,7 +807,7 @@ __global__ void __launch_bounds__(WARPS * 32) ts_gemm_lean_kernel(TsGemmParams p
   }
   cp_async_wait<0>();
   griddep_launch_dependents();
-  gemm_epilogue<NT, WARPS, UB>(p, acc, bv, gsm, i0, q0, nvalid, splits);
+  gemm_epilogue<NT, WARPS, UB, BSM>(p, acc, bv, gsm, i0, q0, nvalid, splits);
 }
 
 // CTA height: 64 rows (4 warps) unless overridden; measured best across the row-residual,
@@ -815,21 +855,22 @@ static cudaError_t launch_cfg(const TsGemmParams& p, cudaStream_t st) {
   return launch_split(ts_gemm_kernel<NT, WARPS>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
 }
 
-template <int NT, int WARPS, int KT, int STAGES, bool UB = false>
+template <int NT, int WARPS, int KT, int STAGES, bool UB = false, bool BSM = false>
 static cudaError_t launch_lean(const TsGemmParams& p, cudaStream_t st) {
   using Cfg = LeanCfg<NT, WARPS, KT, STAGES>;
+  static_assert(!BSM || 2 * NT * 4 * Cfg::THREADS <= STAGES * Cfg::STAGE_ELEMS, "base slots must fit the ring");
   static_assert(!UB || (NT * 4 * Cfg::THREADS + NT * 8 * NT * 8 + NT * 8 + (NT + 1) * 8 * (((NT * 8 + 15) / 16) * 16 + 8) <=
                         STAGES * Cfg::STAGE_ELEMS), "U-block epilogue buffers must fit the ring");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB>,
+    cudaError_t e = cudaFuncSetAttribute(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB, BSM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(p.M, Cfg::BM)), static_cast<unsigned>(ceil_div(p.N, NT * 8)));
   grid.z = static_cast<unsigned>(gemm_splits(static_cast<int64_t>(grid.x) * grid.y, p.k_plan > 0 ? p.k_plan : p.K, KT));
-  return launch_split(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
+  return launch_split(ts_gemm_lean_kernel<NT, WARPS, KT, STAGES, UB, BSM>, grid, Cfg::THREADS, Cfg::BYTES, p, st);
 }
 
 // lean main loop eligibility: 16-byte aligned A rows pairs (even lda and offsets), k-contiguous B
@@ -844,16 +885,33 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
   // 0 off, 1: KT16 x4, 2: KT32 x3, 3: KT32 x4, 4: KT16 x3, 5: KT32 x2; default by shape
   // (tools/time_stage.py gemm sweeps on B200: the lean loop wins for N <= 32 (KT32 x3 for the
   // taller M); for 33..72-wide blocks KT16 x3 / KT32 x2 beat the generic loop by 25-35%, e.g.
-  // 100000 x 50 x 256: 130 vs 201 us, 200000 x 64 x 1024: 958 vs 1193 us)
+  // 100000 x 50 x 256: 130 vs 201 us, 200000 x 64 x 1024: 958 vs 1193 us; with the base values
+  // staged in shared memory (128 instead of 168 registers) KT32 x2 reaches 125 / 882 us)
   static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
   const int64_t kp = p.k_plan > 0 ? p.k_plan : p.K;
-  const int lean = forced >= 0 ? forced : (NT > 4 ? (kp >= 512 ? 5 : 4) : (p.M >= 16000 ? 2 : 1));
+  const int lean = forced >= 0 ? forced : (NT > 4 ? (kp >= 256 ? 5 : 4) : (p.M >= 16000 ? 2 : 1));
   if (lean > 0 && lean_ok(p) && gemm_warps(p.M) == 4) {
+    // wide blocks without early base loads: base values staged through shared memory (A/B:
+    // ITERCUR_GEMM_BSM=0)
+    static const int bsm_env = env_int("ITERCUR_GEMM_BSM", 1);
+    constexpr bool fit4 = 2 * NT * 4 * 128 <= 3 * LeanCfg<NT, 4, 16, 3>::STAGE_ELEMS;
+    constexpr bool fit5 = 2 * NT * 4 * 128 <= 2 * LeanCfg<NT, 4, 32, 2>::STAGE_ELEMS;
+    if constexpr (NT > 4 && fit4) {
+      if (bsm_env && !p.early_base && lean == 4) return launch_lean<NT, 4, 16, 3, false, true>(p, st);
+    }
+    if constexpr (NT > 4 && fit5) {
+      if (bsm_env && !p.early_base && lean == 5) return launch_lean<NT, 4, 32, 2, false, true>(p, st);
+    }
+    constexpr bool fit6 = 2 * NT * 4 * 128 <= 2 * LeanCfg<NT, 4, 16, 2>::STAGE_ELEMS;
+    if constexpr (NT > 4 && fit6) {
+      if (bsm_env && !p.early_base && lean == 6) return launch_lean<NT, 4, 16, 2, false, true>(p, st);
+    }
     switch (lean) {
       case 1: return launch_lean<NT, 4, 16, 4>(p, st);
       case 2: return launch_lean<NT, 4, 32, 3>(p, st);
       case 4: return launch_lean<NT, 4, 16, 3>(p, st);
       case 5: return launch_lean<NT, 4, 32, 2>(p, st);
+      case 6: return launch_lean<NT, 4, 16, 2>(p, st);
       default: return launch_lean<NT, 4, 32, 4>(p, st);
     }
   }
