@@ -308,7 +308,8 @@ double device_sumsq(const double* x, int64_t rows, int64_t cols, int64_t ld, cud
 //   3  tcgen05 kind::i8 (sketch.cu sparse_sketch_umma_kernel): A as int8 slices of a per-column
 //      fixed-point form, written by the converter warps straight into TMEM as the MMA's A operand,
 //      int32 accumulators in TMEM, TMA-staged A tiles, persistent CTAs: 83-88% of HBM at c = 55;
-//   2  the same contraction on mma.sync s8 (register accumulators): 82% of HBM at c_pad = 24;
+//   2  the same contraction on mma.sync s8 (register accumulators): 83% of HBM at c_pad = 24 (the
+//      tcgen05 form: 79%, equal full-run time at config 2; tcgen05 is the default at every c_pad);
 //   0  FP64 DMMA over the materialised +-1 operator (FP64-bound once c_pad > ~24: 37% at c = 55);
 //   1  the sparse list walk (bitwise equal to the oracle's sparse loop; bound by shared-memory
 //      reads of every (row, target) pair: 3.9 ms vs DMMA 2.7 ms at 40000 x 20000, c = 55).
@@ -319,7 +320,7 @@ enum SparseMode { kSparseDense = 0, kSparseList = 1, kSparseImma = 2, kSparseUmm
 static int sparse_sketch_mode(int kind, int64_t c, int64_t cp, int zeta_eff, const double* A, int64_t lda) {
   if (kind != kSketchSparseSign) return kSparseDense;
   const char* e = getenv("ITERCUR_SPARSE_SKETCH");
-  const int want = (e && e[0]) ? atoi(e) : (cp > 32 ? kSparseUmma : kSparseImma);
+  const int want = (e && e[0]) ? atoi(e) : kSparseUmma;  // tcgen05 kind::i8 at every c_pad it supports
   if (want == kSparseList && sparse_sketch_supported(c, zeta_eff)) return kSparseList;
   if (want == kSparseUmma && sparse_sketch_umma_supported(A, 0, 0, lda, cp)) return kSparseUmma;
   if ((want == kSparseImma || want == kSparseUmma) && sparse_sketch_imma_supported(A, lda, cp)) return kSparseImma;
