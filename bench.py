@@ -196,8 +196,7 @@ def sketch_kernel_name(sketch, c):
     """The sketch-apply kernel the engine runs for this sketch kind (csrc/engine.cu sparse_sketch_mode)."""
     if sketch != "sparse_sign":
         return "sketch_dmma_kernel"
-    c_pad = ((c + 7) // 8) * 8
-    mode = os.environ.get("ITERCUR_SPARSE_SKETCH", "") or ("3" if c_pad > 32 else "2")
+    mode = os.environ.get("ITERCUR_SPARSE_SKETCH", "") or "3"  # tcgen05 kind::i8 at every c_pad <= 64
     return {"0": "sketch_dmma_kernel", "1": "sparse_sketch_kernel", "3": "sparse_sketch_umma_kernel"}.get(
         mode, "sparse_sketch_imma_kernel")
 
