@@ -197,14 +197,13 @@ __device__ __forceinline__ void gemm_epilogue(const TsGemmParams& p, double (&ac
           for (int dr = 0; dr < 2; ++dr) {
             const int ql = nt * 8 + 2 * t + dq;
             const int64_t i = r0 + dr;
-            const bool in = ql < nvalid && i < p.M && p.base_mode != kBaseNone && p.base_mode != kBaseIdentityCols;
+            const bool in = ql < nvalid && i < p.M;
             const void* src = in ? gemm_base_addr<NT>(p, i, q0 + ql) : nullptr;
             double* dst = sbase + (nt * 4 + dr * 2 + dq) * THREADS + threadIdx.x;
             if (src)
               cp_async_8(dst, src, 8);
-            else
-              *dst = (in || p.base_mode != kBaseIdentityCols) ? 0.0 : 0.0;
-            if (p.base_mode == kBaseIdentityCols) *dst = (ql < nvalid && i < p.M && i == p.col0 + q0 + ql) ? 1.0 : 0.0;
+            else  // no base, outside the tile, or the identity (kBaseIdentityCols)
+              *dst = (in && p.base_mode == kBaseIdentityCols && i == p.col0 + q0 + ql) ? 1.0 : 0.0;
           }
       cp_async_commit();
     }
@@ -889,11 +888,17 @@ static cudaError_t launch_nt(const TsGemmParams& p, cudaStream_t st) {
   // staged in shared memory (128 instead of 168 registers) KT32 x2 reaches 125 / 882 us)
   static const int forced = env_int("ITERCUR_GEMM_LEAN", -1);
   const int64_t kp = p.k_plan > 0 ? p.k_plan : p.K;
-  const int lean = forced >= 0 ? forced : (NT > 4 ? (kp >= 256 ? 5 : 4) : (p.M >= 16000 ? 2 : 1));
+  // (the U block's scattered A(I_k, :) base: KT16 x3 — 201 vs 246 us per call at config 4; the
+  // in-place downdate: KT32 x2 — 43 vs 50 us at config 5; per-role times: tools/gemm_roles.py)
+  const bool gather_rows = p.base_mode == kBaseGatherRowsT;
+  const bool kt32 = (kp >= 256 || p.base_mode == kBaseInPlaceRowMajor) && !gather_rows;
+  const int lean = forced >= 0 ? forced : (NT > 4 ? (kt32 ? 5 : 4) : (p.M >= 16000 ? 2 : 1));
   if (lean > 0 && lean_ok(p) && gemm_warps(p.M) == 4) {
     // wide blocks without early base loads: base values staged through shared memory (A/B:
-    // ITERCUR_GEMM_BSM=0)
-    static const int bsm_env = env_int("ITERCUR_GEMM_BSM", 1);
+    // ITERCUR_GEMM_BSM=0) — except the U block's scattered A(I_k, :) gather, whose 8-byte cp.asyncs
+    // ran slower than register loads (ncu, config 4: 226 vs 173 us)
+    static const int bsm_env_raw = env_int("ITERCUR_GEMM_BSM", 1);
+    const int bsm_env = bsm_env_raw && !gather_rows;
     constexpr bool fit4 = 2 * NT * 4 * 128 <= 3 * LeanCfg<NT, 4, 16, 3>::STAGE_ELEMS;
     constexpr bool fit5 = 2 * NT * 4 * 128 <= 2 * LeanCfg<NT, 4, 32, 2>::STAGE_ELEMS;
     if constexpr (NT > 4 && fit4) {

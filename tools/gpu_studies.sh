@@ -7,6 +7,7 @@
 #           -DITERCUR_RES_TRACE)
 #   exchange the pure exchange floor (tools/microbench/res_exchange.cu) and warp-reduction latency
 #   gemm    lean/generic x base-in-shared-memory sweep at the config 4/5 GEMM shapes
+#   roles   per-role times of the three per-iteration GEMMs in config 4/5 runs (tools/gemm_roles.py)
 #   solve   the row solves: tensor-core vs scalar blocked form (parity test + config 4/5 run times)
 #   sketch  tcgen05 vs mma.sync sparse-sign sketch at config 2
 case "$1" in
@@ -25,6 +26,12 @@ case "$1" in
       for v in "4 0" "4 1" "5 0" "5 1" "6 1" "-1 0"; do set -- $v
         ITERCUR_GEMM_LEAN=$1 ITERCUR_GEMM_BSM=$2 timeout 60 python tools/time_stage.py gemm $shape $K 10 | sed "s/^/lean=$1 bsm=$2 /"
       done; done; done > gpurun_out/gemm_sweep.txt 2>&1 ;;
+  roles)
+    for c in 4 5; do
+      ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/roles_cfg$c.csv \
+          python tools/profile_run.py --config $c --runs 1 > /dev/null 2>&1
+      python tools/gemm_roles.py gpurun_out/roles_cfg$c.csv > gpurun_out/roles_cfg$c.txt
+    done ;;
   solve)
     timeout 600 python -m pytest tests/test_gpu_stages.py -q -x -k rows_lu_solve > gpurun_out/solve_tests.log 2>&1
     for c in 4 5; do for blk in 0 1; do echo "config $c ITERCUR_ROWS_SOLVE_BLK=$blk"
@@ -35,5 +42,5 @@ case "$1" in
       ITERCUR_SPARSE_SKETCH=$m timeout 300 python tools/time_stage.py sketch 20000 10000 20 sparse_sign 20
       ITERCUR_SPARSE_SKETCH=$m timeout 600 python tools/time_runs.py --config 2 --runs 4 2>&1 | tail -2; done \
       > gpurun_out/sketch_ab.txt 2>&1 ;;
-  *) echo "usage: tools/gpu_studies.sh lupp|exchange|gemm|solve|sketch"; exit 1 ;;
+  *) echo "usage: tools/gpu_studies.sh lupp|exchange|gemm|roles|solve|sketch"; exit 1 ;;
 esac
