@@ -1713,7 +1713,7 @@ constexpr int kResMaxSteps = 64;
 constexpr int kResPanel = 4;              // shared-memory columns updated once per 4 pivot steps
 constexpr int kResRing = 8;  // pivot rows kept (>= kResPanel + 1; a power of two: slot = step & 7)
 constexpr int kResMaxG = 148;
-constexpr int kResRec = 4 + kResMaxSteps;  // header (key, row, runner-up key, 0) + row tail
+constexpr int kResRec = 4 + kResMaxSteps;  // words 0-1 unused, 2 runner-up key, 3 unused, 4 + t the row
 // region: norm partials [kResMaxG], compact headers [step][CTA][2] (a warp's poll touches 4 lines),
 // records [step][CTA][kResRec] (word 2 runner-up key, 3 RN(1/pivot), 4 + t the row)
 constexpr size_t kResHdrWords = static_cast<size_t>(kResMaxSteps) * kResMaxG * 2;
@@ -1915,26 +1915,28 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
 #endif
     double* Pn = Pr[s & (kResRing - 1)];
     double y = 0.0;
-    if (best.key) {  // words 2, 3: runner-up key, RN(1/pivot); 4 + t: the row
+    if (best.key) {  // word 2: the winning CTA's runner-up key; 4 + t: the row
+      // RN(1/|pivot|) from the header's key while the row is in flight (RN(1/-p) = -RN(1/p))
+      const double yabs = lane == 0 ? __drcp_rn(key_mag(best.key)) : 0.0;
       const uint64_t* wr = rec(s, static_cast<int>(best.idx / Rb));
       const int t0 = s + lane, t1 = s + lane + 32;
-      uint64_t u0 = 0, u1 = 0, uh0 = 0, uh1 = 0;
+      uint64_t u0 = 0, u1 = 0, uh0 = 0;
       bool w0 = t0 < steps, w1 = t1 < steps, wh = lane == 0;
       spins = 0;
       while (true) {
         if (w0) u0 = res_ld(wr + 4 + t0);
         if (w1) u1 = res_ld(wr + 4 + t1);
-        if (wh) res_ld2(wr + 2, uh0, uh1);
+        if (wh) uh0 = res_ld(wr + 2);
         w0 = w0 && u0 == kResEmpty;
         w1 = w1 && u1 == kResEmpty;
-        wh = wh && (uh0 == kResEmpty || uh1 == kResEmpty);
+        wh = wh && uh0 == kResEmpty;
         if (!(w0 || w1 || wh) || !wait(spins)) break;
       }
       if (t0 < steps) Pn[t0] = __longlong_as_double(static_cast<long long>(u0));
       if (t1 < steps) Pn[t1] = __longlong_as_double(static_cast<long long>(u1));
       if (lane == 0) {
         if (uh0) best.second = fmax(best.second, key_mag(uh0));
-        y = __longlong_as_double(static_cast<long long>(uh1));
+        y = (u0 >> 63) ? -yabs : yabs;  // lane 0 holds column s: the pivot itself
       }
     }
     if (s == 0 && need_norm) {  // the CTA partials in a fixed tree: every CTA forms the same sum
@@ -1985,6 +1987,10 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
       const int olr = static_cast<int>(cb.idx - r0), w = (olr % kResRowThreads) / 32 + 1;
       const double* orow = Ws + olr;
       if (lane == 0) res_st2(hdr(sp, g), cb.key, static_cast<uint64_t>(cb.idx));
+      if (lane == 1) res_st(r + 2, cb.second >= 0.0 ? mag_key(cb.second) : 0ull);
+      // the row, a lane per column; a shared-memory column t > sp owes its pending steps
+      // j0..sp-1 (res_last_update(t, sp - 1) + 1 = sp - 1 - ((sp - 2 - t) mod kResPanel), >= 0),
+      // at most kResPanel of them, their operands loaded together
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int t = sp + lane + 32 * h;
@@ -1992,10 +1998,19 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
         double v;
         if (t == sp) {
           v = stage[w][KR + 1];
-        } else if (t < R0) {  // shared-memory column: its pending steps (res_last_update(t, sp - 1), sp - 1]
+        } else if (t < R0) {
+          const int j0 = max(0, sp - 1 - ((sp - 2 - t) & (kResPanel - 1)));
+          double mq[kResPanel], pq[kResPanel];
+#pragma unroll
+          for (int q = 0; q < kResPanel; ++q) {
+            const int j = min(j0 + q, sp - 1 < 0 ? 0 : sp - 1);
+            mq[q] = orow[j * ldS];
+            pq[q] = Pr[j & (kResRing - 1)][t];
+          }
           v = orow[t * ldS];
-          for (int j = res_last_update(t, sp - 1) + 1; j < sp; ++j)
-            v = __dsub_rn(v, __dmul_rn(orow[j * ldS], Pr[j & (kResRing - 1)][t]));
+#pragma unroll
+          for (int q = 0; q < kResPanel; ++q)
+            if (j0 + q < sp) v = __dsub_rn(v, __dmul_rn(mq[q], pq[q]));
         } else {  // register column: current through step sp - 2, step sp - 1's term owed
           v = stage[w][t - R0];
           if (sp > 0) v = __dsub_rn(v, __dmul_rn(stage[w][KR], Pr[(sp - 1) & (kResRing - 1)][t]));
@@ -2003,13 +2018,9 @@ __global__ void __launch_bounds__(kResThreads, 1) lupp_resident_kernel(LuppResAr
         res_st(r + 4 + t, res_enc(v));
       }
       if (dbg && lane == 0 && sp > 0) dbg[(sp - 1) * 8 + 3] = clock64();
-      if (lane == 1)
-        res_st2(r + 2, cb.second >= 0.0 ? mag_key(cb.second) : 0ull,
-                static_cast<uint64_t>(__double_as_longlong(__drcp_rn(stage[w][KR + 1]))));
-      if (dbg && lane == 1 && sp > 0) dbg[(sp - 1) * 8 + 4] = clock64();
     } else if (lane == 0) {
       res_st2(hdr(sp, g), 0ull, 0ull);
-      res_st2(r + 2, 0ull, 0ull);
+      res_st(r + 2, 0ull);
     }
 #ifdef ITERCUR_RES_TRACE
     if (ka.gdbg && lane == 0) ka.gdbg[(static_cast<size_t>(sp) * G + g) * 4] = static_cast<long long>(res_now());
