@@ -306,6 +306,11 @@ ITERCUR_API int itercur_rows_lu_solve_device(const double* dX, int64_t ldx, int6
 
 ITERCUR_API int itercur_time_gemm(int64_t M, int32_t N, int64_t K, int32_t reps, void* stream, double* us_per_launch);
 
+/* Load every engine kernel now instead of on its first launch (CUDA lazy module loading): the first
+ * iterative_cur call in a process then pays no module loading. Called by the Python package at import
+ * when a CUDA device is present. functions_loaded (optional): how many kernels were loaded. */
+ITERCUR_API int itercur_preload(int32_t* functions_loaded);
+
 #ifdef __cplusplus
 }
 #endif

@@ -534,6 +534,33 @@ def gratton_tail(c, tau) -> float:
     return out.value
 
 
+def preload() -> int:
+    """Load every engine kernel on the current CUDA device now instead of on its first launch (CUDA
+    lazy module loading), so the first iterative_cur call pays no module loading; returns how many
+    kernels were loaded. Done at import when torch has already initialised CUDA."""
+    n = C.c_int32(0)
+    _check(_lib().itercur_preload(C.byref(n)))
+    return n.value
+
+
+preload_seconds = None  # wall time of the import-time preload (None: not done)
+
+
+def _preload_at_import():
+    global preload_seconds
+    try:
+        import time
+
+        import torch
+
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            t0 = time.perf_counter()
+            preload()
+            preload_seconds = time.perf_counter() - t0
+    except Exception:  # no device, no CUDA context yet, or the library not built: nothing to do
+        pass
+
+
 def sketch_rows_for_block(b: int) -> int:
     """floor(1.1 b) — proj/include/itercur/sketch.hpp:10."""
     return int(_lib().itercur_sketch_rows_for_block(int(b)))
@@ -541,5 +568,8 @@ def sketch_rows_for_block(b: int) -> int:
 
 __all__ = [
     "CurFactors", "IterationRecord", "MatrixHandle", "RunTrace", "__version__", "adjusted_threshold", "slupp_cur",
-    "gratton_tail", "iterative_cur", "sketch_rows_for_block", "sketched_relative_error", "true_relative_error",
+    "gratton_tail", "iterative_cur", "preload", "sketch_rows_for_block", "sketched_relative_error",
+    "true_relative_error",
 ]
+
+_preload_at_import()

@@ -35,7 +35,7 @@ EXPORTED = [
     "itercur_run_holds_matrix", "itercur_copy_to_host",
     "itercur_shard_range", "itercur_iterative_cur_sharded_device", "itercur_iterative_cur_sharded_emulated",
     "itercur_true_relative_error_sharded", "itercur_nccl_unique_id", "itercur_nccl_comm_init",
-    "itercur_nccl_comm_destroy", "itercur_fro_norm_host", "itercur_dense_apply_host",
+    "itercur_nccl_comm_destroy", "itercur_fro_norm_host", "itercur_dense_apply_host", "itercur_preload",
 ]
 
 
@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         "itercur_config_default": (None, [C.POINTER(Config)]),
         "itercur_last_error": (C.c_char_p, []),
         "itercur_abi_version": (C.c_int, []),
+        "itercur_preload": (C.c_int, [C.POINTER(C.c_int32)]),
         "itercur_iterative_cur_device": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Config), vp,
                                                    C.POINTER(runp)]),
         "itercur_iterative_cur_host": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Config),

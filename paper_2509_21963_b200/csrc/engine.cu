@@ -15,6 +15,7 @@
 // so CUR = L * Rt with C = A(:,J), R = A(I,:), core = A(I,J)^{-1} = (L(I,:) Rt(:,J))^{-1}
 // exported on demand. A is never re-read after the sketch except through the gathered
 // columns / rows of the selected blocks.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1816,6 +1817,53 @@ extern "C" {
 void itercur_config_default(itercur_config* cfg) { *cfg = default_config(); }
 const char* itercur_last_error(void) { return g_last_error.c_str(); }
 int itercur_abi_version(void) { return ITERCUR_B200_ABI_VERSION; }
+
+// Load every kernel of the engine's modules now (CUDA lazy loading would otherwise load each on its
+// first launch, inside the first iterative_cur call): one representative kernel per translation
+// unit gives its module; the driver enumerates and loads the module's functions.
+int itercur_preload(int32_t* functions_loaded) {
+  return guarded([&] {
+    require_device();
+    using FnGetModule = CUresult (*)(CUmodule*, CUfunction);
+    using FnCount = CUresult (*)(unsigned int*, CUmodule);
+    using FnEnum = CUresult (*)(CUfunction*, unsigned int, CUmodule);
+    using FnLoad = CUresult (*)(CUfunction);
+    auto entry = [](const char* name, int ver) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPointByVersion(name, &p, ver, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return p;
+    };
+    auto get_module = reinterpret_cast<FnGetModule>(entry("cuFuncGetModule", 11000));
+    auto count_fns = reinterpret_cast<FnCount>(entry("cuModuleGetFunctionCount", 12040));
+    auto enum_fns = reinterpret_cast<FnEnum>(entry("cuModuleEnumerateFunctions", 12040));
+    auto load_fn = reinterpret_cast<FnLoad>(entry("cuFuncLoad", 12040));
+    int32_t loaded = 0;
+    const void* anchors[] = {module_anchor_gemm(), module_anchor_lupp(), module_anchor_misc(),
+                             module_anchor_qrcp(), module_anchor_shard(), module_anchor_sketch()};
+    for (const void* k : anchors) {
+      cudaFunction_t f = nullptr;
+      if (cudaGetFuncBySymbol(&f, k) != cudaSuccess) continue;
+      if (!get_module || !count_fns || !enum_fns || !load_fn) {  // older driver: the anchor alone
+        cudaFuncAttributes attr;
+        if (cudaFuncGetAttributes(&attr, k) == cudaSuccess) ++loaded;
+        continue;
+      }
+      CUmodule mod = nullptr;
+      unsigned int nf = 0;
+      if (get_module(&mod, reinterpret_cast<CUfunction>(f)) != CUDA_SUCCESS || count_fns(&nf, mod) != CUDA_SUCCESS)
+        continue;
+      std::vector<CUfunction> fns(nf);
+      if (nf == 0 || enum_fns(fns.data(), nf, mod) != CUDA_SUCCESS) continue;
+      for (CUfunction fn : fns)
+        if (load_fn(fn) == CUDA_SUCCESS) ++loaded;
+    }
+    cudaGetLastError();
+    if (functions_loaded) *functions_loaded = loaded;
+  });
+}
 
 int itercur_iterative_cur_device(const double* dA, int64_t m, int64_t n, int64_t lda, const itercur_config* cfg,
                                  void* stream, itercur_run** out) {

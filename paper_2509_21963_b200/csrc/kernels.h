@@ -188,4 +188,12 @@ void set_lupp_force_path(int path);
 void set_lupp_debug_trace(long long* dbg);  // per-step clock64() trace of CTA 0 (grid path)
 void set_lupp_grid_trace(long long* gdbg);  // resident path: globaltimer stamps of every CTA per step
 
+// one kernel per translation unit (module): itercur_preload loads every function of each module
+const void* module_anchor_gemm();
+const void* module_anchor_lupp();
+const void* module_anchor_misc();
+const void* module_anchor_qrcp();
+const void* module_anchor_shard();
+const void* module_anchor_sketch();
+
 }  // namespace itercur_b200

@@ -2434,4 +2434,7 @@ cudaError_t run_lupp_with_scratch(const LuppArgs& a, void* scratch, cudaStream_t
                                      params, smem, st);
 }
 
+// a kernel of this translation unit (module), for itercur_preload
+const void* module_anchor_lupp() { return reinterpret_cast<const void*>(lupp_kernel); }
+
 }  // namespace itercur_b200

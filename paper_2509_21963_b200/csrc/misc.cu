@@ -984,4 +984,7 @@ cudaError_t launch_commit(IterCtl* ctl, IterState* slot, const IterArrays& arr, 
   return launch_ex(commit_kernel, dim3(1), dim3(256), 0, st, dim3(0, 0, 0), c, y_partials, y_parts);
 }
 
+// a kernel of this translation unit (module), for itercur_preload
+const void* module_anchor_misc() { return reinterpret_cast<const void*>(gather_kernel); }
+
 }  // namespace itercur_b200

@@ -206,4 +206,7 @@ cudaError_t run_qrcp(double* W, int64_t ncand, int len, const int* d_len, int64_
                                      params, 0, st);
 }
 
+// a kernel of this translation unit (module), for itercur_preload
+const void* module_anchor_qrcp() { return reinterpret_cast<const void*>(qrcp_kernel); }
+
 }  // namespace itercur_b200

@@ -93,4 +93,7 @@ cudaError_t launch_dense_lu(double* D, int w, int64_t ldd, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// a kernel of this translation unit (module), for itercur_preload
+const void* module_anchor_shard() { return reinterpret_cast<const void*>(dense_lu_kernel); }
+
 }  // namespace itercur_b200

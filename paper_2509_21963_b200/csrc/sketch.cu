@@ -1565,4 +1565,7 @@ cudaError_t run_sketch_apply_sparse_umma(const double* A, int64_t m, int64_t n, 
   return cudaGetLastError();
 }
 
+// a kernel of this translation unit (module), for itercur_preload
+const void* module_anchor_sketch() { return reinterpret_cast<const void*>(gen_gaussian_kernel); }
+
 }  // namespace itercur_b200

@@ -384,3 +384,14 @@ def test_fused_wide_ublock_matches_oracle(engine, oracle, monkeypatch, b, sketch
         assert f.col_indices == f2.col_indices and np.allclose(t.rhos, t2.rhos, rtol=1e-9, atol=1e-13)
     err = engine.true_relative_error(a, f)
     assert abs(err - oracle.true_relative_error(a, o.row_indices, o.col_indices)) <= 1e-8
+
+
+def test_preload_loads_every_engine_kernel(engine):
+    """itercur_preload loads the kernels of all engine modules up front (lazy module loading would
+    load each on its first launch inside the first iterative_cur call); runs still match after it."""
+    n = engine.preload()
+    assert n >= 100, n
+    assert engine.preload() == n  # idempotent
+    a = np.random.default_rng(3).standard_normal((300, 40)) @ np.random.default_rng(4).standard_normal((40, 250))
+    f, t = engine.iterative_cur(a, epsilon=1e-10, b=10, seed=1)
+    assert t.status in ("Converged", "ResidualExhausted") and 40 <= f.rank <= 50, (t.status, f.rank)
