@@ -333,12 +333,14 @@ def _collect(run_ptr, keepalive):
     _check(L.itercur_run_steps(run_ptr, sk.ctypes.data_as(C.POINTER(C.c_int32)),
                                si.ctypes.data_as(C.POINTER(C.c_int64)), sx.ctypes.data_as(C.POINTER(C.c_int64)),
                                sb.ctypes.data_as(C.POINTER(C.c_double)), ss.ctypes.data_as(C.POINTER(C.c_double))))
-    steps = [(int(sk[q]), int(si[q]), int(sx[q]), float(sb[q]), float(ss[q])) for q in range(ns)]
+    # tolist(): one C loop per array (a Python-level loop over numpy scalars cost ~2.5 ms per
+    # config-2 run — 4720 pivot steps — inside every caller's timed region)
+    steps = list(zip(sk[:ns].tolist(), si[:ns].tolist(), sx[:ns].tolist(), sb[:ns].tolist(), ss[:ns].tolist()))
     trace = RunTrace(_STATUS[L.itercur_run_status(run_ptr)], L.itercur_run_final_rho(run_ptr),
                      L.itercur_run_threshold(run_ptr), L.itercur_run_note(run_ptr).decode(), iters,
                      L.itercur_run_sketch_seconds(run_ptr), L.itercur_run_total_seconds(run_ptr),
                      L.itercur_run_ga_norm(run_ptr), steps, L.itercur_run_kernel_launches(run_ptr))
-    factors = CurFactors(run, [int(v) for v in I[:r]], [int(v) for v in J[:r]])
+    factors = CurFactors(run, I[:r].tolist(), J[:r].tolist())
     return factors, trace
 
 
@@ -356,8 +358,8 @@ class _ObservedFactors:
         J = np.zeros(max(r, 1), dtype=np.int64)
         _check(L.itercur_run_indices(run_ptr, I.ctypes.data_as(C.POINTER(C.c_int64)),
                                      J.ctypes.data_as(C.POINTER(C.c_int64))))
-        self.row_indices = [int(v) for v in I[:r]]
-        self.col_indices = [int(v) for v in J[:r]]
+        self.row_indices = I[:r].tolist()
+        self.col_indices = J[:r].tolist()
 
     @property
     def rank(self) -> int:

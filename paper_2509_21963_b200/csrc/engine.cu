@@ -423,7 +423,10 @@ void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
     CK(cudaMemcpyAsync(R2.p, run->Rt.p, sizeof(double) * run->ldR * run->r, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(D2.p, run->Dinv.p, sizeof(double) * run->bmax * run->r, cudaMemcpyDeviceToDevice, st));
   }
-  CK(cudaStreamSynchronize(st));
+  // the copies and the old buffers' frees are ordered on st; waiting here is only needed to keep
+  // the host from running ahead of a regrowth (an empty run has nothing in flight to wait for,
+  // and its first capacity is set up while the sketch is still running)
+  if (run->r > 0) CK(cudaStreamSynchronize(st));
   run->L.swap(L2);
   run->Rt.swap(R2);
   run->Dinv.swap(D2);
@@ -535,50 +538,66 @@ void run_iterative_cur(itercur_run* run) {
     }
   }
   CK(cudaEventRecord(e_sk1, st));
-  double hs[2] = {0, 0};
-  {
-    std::vector<double> hp(2 * nloc);
-    CK(cudaMemcpyAsync(hp.data(), ws.scal.p, sizeof(double) * 2 * nloc, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int sI = 0; sI < nloc; ++sI) {  // shard order (fixed)
-      hs[0] += hp[2 * sI];
-      hs[1] += hp[2 * sI + 1];
-    }
-    allreduce_host(hs, 2);
-  }
   ws.S.reset();
   ws.sk_ws.reset();
-  if (!std::isfinite(hs[0])) {
-    if (count_nonfinite_all() > 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
-  }
-  if (hs[0] == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
-  run->a_norm = std::sqrt(hs[0]);
-  const double ga_norm = std::sqrt(hs[1]);
-  run->ga_norm = ga_norm;
-  run->sketch_s = elapsed_s(e_sk0, e_sk1);
-
-  const double threshold =
-      cfg.risk_adjust ? adjusted_threshold_impl(cfg.epsilon, cfg.delta, cfg.alpha, c) : cfg.epsilon;
-  run->threshold = threshold;
-
-  // rho_0 (downdate with empty factors, sketch.cpp:27-30)
-  double rho = ga_norm > 0.0 ? 1.0 : 0.0;
-  if (rho <= threshold) {
-    run->status = ITERCUR_CONVERGED;
-    run->final_rho = rho;
-    run->note = "threshold at or above the initial estimate; empty factorization";
-    run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-    return;
-  }
-  // the reference validates the selection methods on the first select_* call
-  // per-method floors (SelectionMethod::pivot_floor, select.hpp:12-15); the column method is
-  // validated first, as select_columns runs before select_rows (select.cpp:24-28)
+  // per-method floors (SelectionMethod::pivot_floor, select.hpp:12-15)
   const double col_floor = cfg.pivot_floor;
   const double row_floor = cfg.row_pivot_floor > 0.0 ? cfg.row_pivot_floor : cfg.pivot_floor;
-  if (!(col_floor > 0.0 && col_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
-  if (!(row_floor > 0.0 && row_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
-  check_method(cfg.col_method);
-  check_method(cfg.row_method);
+  // The host's read of the sketch's norms — the zero / non-finite checks, rho_0 and the loop
+  // control's initial state — is deferred until the workspaces are set up and the first batch's
+  // graph is captured, instantiated and uploaded: all of that is independent of the data and
+  // runs on the host while the device streams A through the sketch (config 4: ~0.7 ms of device
+  // idle time between the sketch and the first iteration otherwise). The checks keep the
+  // reference's order (driver.cpp:51-54, then the first select_* call's validation).
+  double hs[2] = {0, 0};
+  double ga_norm = 0.0, threshold = 0.0, rho = 1.0;
+  std::function<void()> upload_ctl;  // set once the loop control's buffers exist
+  auto finish_sketch = [&]() -> bool {
+    {
+      std::vector<double> hp(2 * nloc);
+      CK(cudaMemcpyAsync(hp.data(), ws.scal.p, sizeof(double) * 2 * nloc, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int sI = 0; sI < nloc; ++sI) {  // shard order (fixed)
+        hs[0] += hp[2 * sI];
+        hs[1] += hp[2 * sI + 1];
+      }
+      allreduce_host(hs, 2);
+    }
+    if (!std::isfinite(hs[0])) {
+      if (count_nonfinite_all() > 0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix contains non-finite entries");
+    }
+    if (hs[0] == 0.0) fail(ITERCUR_E_INVALID_ARGUMENT, "matrix must be nonzero");
+    run->a_norm = std::sqrt(hs[0]);
+    ga_norm = std::sqrt(hs[1]);
+    run->ga_norm = ga_norm;
+    run->sketch_s = elapsed_s(e_sk0, e_sk1);
+
+    threshold = cfg.risk_adjust ? adjusted_threshold_impl(cfg.epsilon, cfg.delta, cfg.alpha, c) : cfg.epsilon;
+    run->threshold = threshold;
+
+    // rho_0 (downdate with empty factors, sketch.cpp:27-30)
+    rho = ga_norm > 0.0 ? 1.0 : 0.0;
+    if (rho <= threshold) {
+      run->status = ITERCUR_CONVERGED;
+      run->final_rho = rho;
+      run->note = "threshold at or above the initial estimate; empty factorization";
+      // nothing was selected: the factor buffers set up ahead of this check go back to the pool
+      run->L.reset();
+      run->Rt.reset();
+      run->Dinv.reset();
+      run->capL = 0;
+      run->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      return false;
+    }
+    // the reference validates the selection methods on the first select_* call; the column
+    // method is validated first, as select_columns runs before select_rows (select.cpp:24-28)
+    if (!(col_floor > 0.0 && col_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+    if (!(row_floor > 0.0 && row_floor < 1.0)) fail(ITERCUR_E_INVALID_ARGUMENT, "pivot_floor must lie in (0, 1)");
+    check_method(cfg.col_method);
+    check_method(cfg.row_method);
+    upload_ctl();
+    return true;
+  };
 
   // ---- workspaces ----
   const int B = static_cast<int>(b);
@@ -614,7 +633,7 @@ void run_iterative_cur(itercur_run* run) {
   char* slots = ws.state.p;
   IterCtl* d_ctl = reinterpret_cast<IterCtl*>(ws.state.p + slot_bytes * kBatch);
   ws.h_state = pinned_state(slot_bytes * kBatch + sizeof(IterCtl));
-  {
+  upload_ctl = [&, d_ctl, slot_bytes, kBatch, B]() {  // from finish_sketch, once the norms are on the host
     IterCtl h{};
     h.r = 0;
     h.k = 0;
@@ -630,7 +649,7 @@ void run_iterative_cur(itercur_run* run) {
     IterCtl* hc = reinterpret_cast<IterCtl*>(ws.h_state + slot_bytes * kBatch);
     *hc = h;
     CK(cudaMemcpyAsync(d_ctl, hc, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
-  }
+  };
   // QRCP rows are not in pivot order: D_k is factored with partial pivoting (cross_lu) and
   // its permutation kept per block for the solves and the core export
   if (row_qrcp) run->Piv.alloc(std::max<int64_t>(max_rank + b, 1));
@@ -856,10 +875,9 @@ void run_iterative_cur(itercur_run* run) {
   std::vector<size_t> iter_events;
   bool done = false;
   static const bool host_trace = env_flag("ITERCUR_HOST_TRACE");
-  if (host_trace)
-    fprintf(stderr, "[itercur setup] %.0fus before the iteration loop (sketch %.0fus)\n",
-            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count(),
-            run->sketch_s * 1e6);
+  bool sketch_pending = true;
+  const double setup_us =
+      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
   using hclock = std::chrono::steady_clock;
   auto us_since = [](hclock::time_point t0) {
     return std::chrono::duration<double, std::micro>(hclock::now() - t0).count();
@@ -1220,23 +1238,46 @@ void run_iterative_cur(itercur_run* run) {
       e.launches = batch_launches;
       return e;
     };
+    GraphEntry* ge = nullptr;
     if (use_graph) {
       if (graph_cap != run->capL || at_new) {
         graphs.clear();
         graph_cap = run->capL;
       }
-      GraphEntry* ge = graphs.find(plan_sig);
+      ge = graphs.find(plan_sig);
       if (!ge) {
         graphs.v.emplace_back(plan_sig, capture(k_plan));
         ge = &graphs.v.back().second;
+        // first batch: the sketch is still running — place the executable graph on the device now
+        // (on the side stream), so its launch after the norm checks costs microseconds
+        if (sketch_pending) {
+          SideStream& ss = side_stream();
+          if (cudaGraphUpload(ge->exec, ss.s) == cudaSuccess) {
+            CK(cudaEventRecord(ss.join, ss.s));
+            CK(cudaStreamWaitEvent(st, ss.join, 0));
+          } else {
+            cudaGetLastError();
+          }
+        }
         t_capture = us_since(tc0);
       }
+    }
+    if (sketch_pending) {  // the norm checks, rho_0 and the loop control's upload (see finish_sketch)
+      sketch_pending = false;
+      const auto tf0 = hclock::now();
+      if (!finish_sketch()) return;
+      if (host_trace)
+        fprintf(stderr, "[itercur setup] %.0fus before the first batch (sketch %.0fus, waited %.0fus for it)\n",
+                us_since(tb0) + setup_us, run->sketch_s * 1e6, us_since(tf0));
+    }
+    const auto tl0 = hclock::now();
+    if (use_graph) {
       CK(cudaGraphLaunch(ge->exec, st));
       batch_launches = ge->launches;
     } else {
       enqueue_batch();
     }
-    t_launch = us_since(tc0) - t_capture;
+    t_launch = us_since(tl0);
     run->launches += batch_launches;
     // one D2H read per batch: the batch's records + the loop control
     CK(cudaMemcpyAsync(ws.h_state, ws.state.p, slot_bytes * kBatch + sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
