@@ -415,9 +415,18 @@ void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
   if (cap < need) cap = need;
   cap = (cap + 1) & ~int64_t(1);  // even: 16-byte aligned gathered columns (lean GEMM loads)
   DevBuf<double> L2, R2, D2;
+  static const bool trace = env_flag("ITERCUR_HOST_TRACE");
+  const auto t0 = std::chrono::steady_clock::now();
   L2.alloc(static_cast<size_t>(run->ldL) * cap);
+  const auto t1 = std::chrono::steady_clock::now();
   R2.alloc(static_cast<size_t>(run->ldR) * cap);
+  const auto t2 = std::chrono::steady_clock::now();
   D2.alloc(static_cast<size_t>(run->bmax) * cap);
+  if (trace)
+    fprintf(stderr, "[itercur grow] L %.0f MB in %.0fus, R~ %.0f MB in %.0fus, D in %.0fus\n",
+            8e-6 * run->ldL * cap, std::chrono::duration<double, std::micro>(t1 - t0).count(), 8e-6 * run->ldR * cap,
+            std::chrono::duration<double, std::micro>(t2 - t1).count(),
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t2).count());
   if (run->r > 0) {
     CK(cudaMemcpyAsync(L2.p, run->L.p, sizeof(double) * run->ldL * run->r, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(R2.p, run->Rt.p, sizeof(double) * run->ldR * run->r, cudaMemcpyDeviceToDevice, st));
@@ -520,26 +529,97 @@ void run_iterative_cur(itercur_run* run) {
   evs.on = cfg.profile != 0;
   Workspace ws;
   const int nloc = sh.nloc;
+  const int B = static_cast<int>(b);
+  const int kBatch = cfg.observer ? 1 : 8;  // iterations per batch graph (see the loop control below)
+  const int64_t ldn = even(n), ldm = even(m);
+  // ITERCUR_HOST_TRACE: where the host's set-up time goes
+  static const bool setup_trace = env_flag("ITERCUR_HOST_TRACE");
+  auto t_mark = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!setup_trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[itercur setup] %s %.0fus\n", what,
+            std::chrono::duration<double, std::micro>(now - t_mark).count());
+    t_mark = now;
+  };
+  // The run's large buffers first (factor capacity, the row-major copy of A), then the small
+  // workspaces: the pool then serves the GB-sized requests from the previous runs' freed blocks of
+  // the same sizes before small requests have carved them up.
+  run->capL = 0;
+  {
+    // factor capacity: the whole max_rank + b up front when it is a small share of free HBM
+    // (no regrowth copies, one graph capture per run), else grow by doubling
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    mark("cudaMemGetInfo");
+    const int64_t full = max_rank + b;
+    const double full_bytes = 8.0 * static_cast<double>(run->ldL + run->ldR + b) * static_cast<double>(full);
+    int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
+                        ? full
+                        : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
+    if (use_nccl) {
+      // the capacity sizes the packed block every rank allreduces (and the graphs' shapes): the
+      // ranks' free memory differs with their shards, so they agree on the smallest choice
+      double v = static_cast<double>(first);
+      CK(cudaMemcpyAsync(red.p, &v, sizeof(double), cudaMemcpyHostToDevice, st));
+      nck(nc->AllReduce(red.p, red.p, 1, ncclDouble, ncclMin, sh.comm, st), "allreduce capacity");
+      CK(cudaMemcpyAsync(&v, red.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      first = static_cast<int64_t>(v);
+    }
+    grow_factors(run, first, st);
+  }
+  // row-major copy of A (when it is a modest share of free HBM): the U block's base A(I_k, :)
+  // then reads |I_k| contiguous rows instead of one DRAM burst per element (~8 us per
+  // iteration at config 2).
+  // Made up front for A <= 2 GB (transpose <= ~0.6 ms; config 2: 32.3 ms eager vs 33.1 lazy after
+  // 24 iterations — the lazy path's 1.6 GB pool allocation stalls the host between batches);
+  // larger matrices skip it unless forced (config 3, 8 iterations, would pay 6 ms for 20 GB).
+  // ITERCUR_ROWMAJOR_A=1 forces it, ITERCUR_NO_ROWMAJOR_A=1 disables it.
+  static const bool at_off = env_flag("ITERCUR_NO_ROWMAJOR_A"), at_force = env_flag("ITERCUR_ROWMAJOR_A");
+  auto maybe_make_rowmajor_a = [&](int64_t iters_done) -> bool {
+    if (at_off || ws.At.p || iters_done > 0) return false;
+    const double bytes = 8.0 * static_cast<double>(ldn) * static_cast<double>(m);
+    if (!at_force && bytes > 2e9) return false;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > 0.3 * static_cast<double>(free_b)) return false;
+    mark("before the row-major copy's allocation");
+    ws.At.alloc(static_cast<size_t>(ldn) * m);
+    mark("row-major copy allocated");
+    ws.ldAt = ldn;
+    CK(launch_transpose(A, m, n, lda, ws.At.p, ldn, st));
+    run->launches += 1;
+    return true;
+  };
+  const bool at_early = maybe_make_rowmajor_a(0);
+  (void)at_early;
+  mark("factor capacity and row-major copy");
   ws.scal.alloc(2 * nloc + 2);
   ws.Y.alloc(static_cast<size_t>(cp) * n);
 
   // ---- sketch (make_sketch, sketch.cpp:10-24), ||A|| fused; one apply per local shard (the
   //      operator is regenerated from (seed, i) wherever it is needed) ----
   cudaEvent_t e_sk0 = evs.get(0), e_sk1 = evs.get(1);
-  CK(cudaEventRecord(e_sk0, st));
-  {
-    const int kind = cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
-    SketchBuffers sb;
-    for (int sI = 0; sI < nloc; ++sI) {
-      SketchStats stats{ws.scal.p + 2 * sI, ws.scal.p + 2 * sI + 1};
-      run->launches += apply_sketch(A + loc(sI) * lda, m, sh.cnt[sI], lda, kind, cfg.sparse_nnz, cfg.seed,
-                                    cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch,
-                                    c, cp, ws.Y.p + loc(sI) * cp, stats, sb, st, nullptr, sI > 0 && sb.S.p != nullptr);
+  // enqueued once every buffer of the run is allocated (below): allocations issued while a long
+  // kernel occupies the stream fell off the pool's fast path now and then (4 ms per GB-sized
+  // buffer, ITERCUR_HOST_TRACE), so the stream is idle while the run's memory is set up
+  auto enqueue_sketch = [&]() {
+    CK(cudaEventRecord(e_sk0, st));
+    {
+      const int kind = cfg.sketch_kind == ITERCUR_SKETCH_SPARSE_SIGN ? kSketchSparseSign : kSketchGaussian;
+      SketchBuffers sb;
+      for (int sI = 0; sI < nloc; ++sI) {
+        SketchStats stats{ws.scal.p + 2 * sI, ws.scal.p + 2 * sI + 1};
+        run->launches += apply_sketch(A + loc(sI) * lda, m, sh.cnt[sI], lda, kind, cfg.sparse_nnz, cfg.seed,
+                                      cfg.sketch_stream > 0 ? static_cast<uint32_t>(cfg.sketch_stream) : kStreamSketch,
+                                      c, cp, ws.Y.p + loc(sI) * cp, stats, sb, st, nullptr, sI > 0 && sb.S.p != nullptr);
+      }
     }
-  }
-  CK(cudaEventRecord(e_sk1, st));
-  ws.S.reset();
-  ws.sk_ws.reset();
+    CK(cudaEventRecord(e_sk1, st));
+    ws.S.reset();
+    ws.sk_ws.reset();
+  };
   // per-method floors (SelectionMethod::pivot_floor, select.hpp:12-15)
   const double col_floor = cfg.pivot_floor;
   const double row_floor = cfg.row_pivot_floor > 0.0 ? cfg.row_pivot_floor : cfg.pivot_floor;
@@ -600,10 +680,8 @@ void run_iterative_cur(itercur_run* run) {
   };
 
   // ---- workspaces ----
-  const int B = static_cast<int>(b);
   // ldn: this process's columns (Y, R~, the U block); ldng: the replicated Wc over all columns
   // (NCCL mode: room for world equal blocks, so Wc's rows gather in place column by column)
-  const int64_t ldn = even(n), ldm = even(m);
   const int64_t blk = use_nccl ? shard_block(n_glob, sh.world) : 0;  // rank r owns [r*blk, min((r+1)*blk, n))
   const int64_t ldng = use_nccl ? std::max(even(n_glob), blk * sh.world) : even(n_glob);
   ws.Wc.alloc(static_cast<size_t>(ldng) * B);
@@ -627,7 +705,6 @@ void run_iterative_cur(itercur_run* run) {
   // iteration after the stop returns immediately.
   // With an IterationObserver every batch is one iteration, so the observer sees each
   // iteration's factors (driver.cpp:154) before the next one starts.
-  const int kBatch = cfg.observer ? 1 : 8;
   const size_t slot_bytes = round_up(iter_state_bytes(B), 64);
   ws.state.alloc(slot_bytes * kBatch + sizeof(IterCtl));
   char* slots = ws.state.p;
@@ -655,29 +732,6 @@ void run_iterative_cur(itercur_run* run) {
   if (row_qrcp) run->Piv.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dI.alloc(std::max<int64_t>(max_rank + b, 1));
   run->dJ.alloc(std::max<int64_t>(max_rank + b, 1));
-  run->capL = 0;
-  {
-    // factor capacity: the whole max_rank + b up front when it is a small share of free HBM
-    // (no regrowth copies, one graph capture per run), else grow by doubling
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    const int64_t full = max_rank + b;
-    const double full_bytes = 8.0 * static_cast<double>(run->ldL + run->ldR + b) * static_cast<double>(full);
-    int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
-                        ? full
-                        : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
-    if (use_nccl) {
-      // the capacity sizes the packed block every rank allreduces (and the graphs' shapes): the
-      // ranks' free memory differs with their shards, so they agree on the smallest choice
-      double v = static_cast<double>(first);
-      CK(cudaMemcpyAsync(red.p, &v, sizeof(double), cudaMemcpyHostToDevice, st));
-      nck(nc->AllReduce(red.p, red.p, 1, ncclDouble, ncclMin, sh.comm, st), "allreduce capacity");
-      CK(cudaMemcpyAsync(&v, red.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      first = static_cast<int64_t>(v);
-    }
-    grow_factors(run, first, st);
-  }
   ws.Bg.alloc(static_cast<size_t>(run->capL) * B);
   // sharded runs: the selected block's columns [A(:,J_k) | R~(0:r,J_k) | Y(:,J_k)] assembled from
   // their owners (NCCL: one sum-allreduce of disjoint contributions; emulation: each shard writes
@@ -693,27 +747,6 @@ void run_iterative_cur(itercur_run* run) {
   auto packA = [&]() { return pack.p; };
   auto packR = [&]() { return pack.p + ldm * B; };
   auto packY = [&]() { return pack.p + (ldm + pack_ldr) * B; };
-  // row-major copy of A (when it is a modest share of free HBM): the U block's base A(I_k, :)
-  // then reads |I_k| contiguous rows instead of one DRAM burst per element (~8 us per
-  // iteration at config 2).
-  // Made up front for A <= 2 GB (transpose <= ~0.6 ms; config 2: 32.3 ms eager vs 33.1 lazy after
-  // 24 iterations — the lazy path's 1.6 GB pool allocation stalls the host between batches);
-  // larger matrices skip it unless forced (config 3, 8 iterations, would pay 6 ms for 20 GB).
-  // ITERCUR_ROWMAJOR_A=1 forces it, ITERCUR_NO_ROWMAJOR_A=1 disables it.
-  static const bool at_off = env_flag("ITERCUR_NO_ROWMAJOR_A"), at_force = env_flag("ITERCUR_ROWMAJOR_A");
-  auto maybe_make_rowmajor_a = [&](int64_t iters_done) -> bool {
-    if (at_off || ws.At.p || iters_done > 0) return false;
-    const double bytes = 8.0 * static_cast<double>(ldn) * static_cast<double>(m);
-    if (!at_force && bytes > 2e9) return false;
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    if (bytes > 0.3 * static_cast<double>(free_b)) return false;
-    ws.At.alloc(static_cast<size_t>(ldn) * m);
-    ws.ldAt = ldn;
-    CK(launch_transpose(A, m, n, lda, ws.At.p, ldn, st));
-    run->launches += 1;
-    return true;
-  };
   // optional U-block trace (ITERCUR_UB_TRACE=k: phases and CTA spans at iteration k)
   const char* ub_trace_env = getenv("ITERCUR_UB_TRACE");
   const int64_t ub_trace_k = ub_trace_env ? atoll(ub_trace_env) : 0;
@@ -838,6 +871,9 @@ void run_iterative_cur(itercur_run* run) {
     nck(nc->GroupEnd(), "group end");
   };
 
+  mark("workspaces");
+  enqueue_sketch();
+  mark("sketch enqueued");
   // initial Wc = Y^T(:, 0:b)
   for (int sI = 0; sI < nloc; ++sI) {
     CK(launch_transpose_rows(ws.Y.p + loc(sI) * cp, cp, sh.cnt[sI], B, ws.Wc.p + sh.goff[sI], ldng, st));
@@ -1355,7 +1391,14 @@ void run_iterative_cur(itercur_run* run) {
     run->r = r_host;
     rho = hc->rho;
     done = hc->done != 0;
-    if (done) run->status = hc->status;
+    if (done) {
+      run->status = hc->status;
+    } else if (r_host >= max_rank || k_host >= max_iters) {
+      // the next iteration's begin would stop here with MaxRank (iter_begin_kernel): no need to
+      // launch a batch of early-returning kernels to learn it (config 5: ~0.15 ms)
+      done = true;
+      run->status = ITERCUR_MAX_RANK;
+    }
   }
   if (evs.on) {
     for (size_t q = 0; q < run->iters.size() && q < iter_events.size(); ++q) {
