@@ -432,9 +432,8 @@ void grow_factors(itercur_run* run, int64_t need, cudaStream_t st) {
     CK(cudaMemcpyAsync(R2.p, run->Rt.p, sizeof(double) * run->ldR * run->r, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(D2.p, run->Dinv.p, sizeof(double) * run->bmax * run->r, cudaMemcpyDeviceToDevice, st));
   }
-  // the copies and the old buffers' frees are ordered on st; waiting here is only needed to keep
-  // the host from running ahead of a regrowth (an empty run has nothing in flight to wait for,
-  // and its first capacity is set up while the sketch is still running)
+  // the copies and the old buffers' frees are ordered on st; waiting here only keeps the host from
+  // running ahead of a regrowth (an empty run has nothing in flight to wait for)
   if (run->r > 0) CK(cudaStreamSynchronize(st));
   run->L.swap(L2);
   run->Rt.swap(R2);
@@ -601,9 +600,9 @@ void run_iterative_cur(itercur_run* run) {
   // ---- sketch (make_sketch, sketch.cpp:10-24), ||A|| fused; one apply per local shard (the
   //      operator is regenerated from (seed, i) wherever it is needed) ----
   cudaEvent_t e_sk0 = evs.get(0), e_sk1 = evs.get(1);
-  // enqueued once every buffer of the run is allocated (below): allocations issued while a long
-  // kernel occupies the stream fell off the pool's fast path now and then (4 ms per GB-sized
-  // buffer, ITERCUR_HOST_TRACE), so the stream is idle while the run's memory is set up
+  // enqueued once every buffer of the run is allocated, so the pool's requests are made on an idle
+  // stream as they always were (allocating while the sketch ran would hide ~0.2 ms more, but was
+  // only measured on boxes whose GB-sized pool requests took milliseconds either way)
   auto enqueue_sketch = [&]() {
     CK(cudaEventRecord(e_sk0, st));
     {
