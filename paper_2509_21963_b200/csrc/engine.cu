@@ -548,14 +548,28 @@ void run_iterative_cur(itercur_run* run) {
   {
     // factor capacity: the whole max_rank + b up front when it is a small share of free HBM
     // (no regrowth copies, one graph capture per run), else grow by doubling
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    mark("cudaMemGetInfo");
     const int64_t full = max_rank + b;
     const double full_bytes = 8.0 * static_cast<double>(run->ldL + run->ldR + b) * static_cast<double>(full);
-    int64_t first = full_bytes <= 0.25 * static_cast<double>(free_b)
-                        ? full
-                        : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
+    // free memory is only queried when the answer can depend on it: a capacity above a quarter of
+    // the device's TOTAL memory (configs 3/4 without a rank cap) grows by doubling whatever is free.
+    // cudaMemGetInfo sits on the run's critical path (~0.1 ms, at times milliseconds beside NVML
+    // readers or large frees).
+    static std::atomic<size_t> total_mem[kMaxDevices] = {};
+    const int dev_ix = current_device();
+    size_t free_b = 0, total_b = total_mem[dev_ix].load();
+    bool have_free = false;
+    if (total_b == 0) {
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      total_mem[dev_ix].store(total_b);
+      have_free = true;
+    }
+    bool fits = full_bytes <= 0.25 * static_cast<double>(total_b);
+    if (fits) {
+      if (!have_free) CK(cudaMemGetInfo(&free_b, &total_b));
+      fits = full_bytes <= 0.25 * static_cast<double>(free_b);
+      mark("cudaMemGetInfo");
+    }
+    int64_t first = fits ? full : std::min<int64_t>(full, std::max<int64_t>(kBatch * b, 256));
     if (use_nccl) {
       // the capacity sizes the packed block every rank allreduces (and the graphs' shapes): the
       // ranks' free memory differs with their shards, so they agree on the smallest choice
